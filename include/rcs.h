@@ -1,0 +1,198 @@
+/*
+ * rcs.h -- C ABI of the B200-native random-circuit-sampling (RCS) hot path.
+ *
+ * The calls follow the paper's statement of the problem (§3.2, lines 34-39):
+ *   "circuits are initially constructed from Google's QASM-format files"   -> rcs_circuit_load_qasm
+ *   "construct the complete quantum state from the circuit definition"      -> rcs_state_build
+ *   "performs 2.5x10^6/N measurement shots"                                  -> rcs_sample
+ *   "calculates the linear cross-entropy benchmarking (XEB) score"           -> rcs_xeb
+ * with the conventions, operations and errors of SPEC.md (S:42-50 parse, S:122-126 build,
+ * S:138-140 probability, S:244-247 sample, S:378-380 XEB) and the readings listed in
+ * DESIGN.md §3 (V1-V15).  All arithmetic runs in this library's sm_100a CUDA kernels.
+ *
+ * General rules
+ *  - Every function returns rcs_status (0 = RCS_OK) and never throws across the ABI.
+ *  - On error, `err` (if non-NULL) receives code, message and, for parse errors, the
+ *    1-based line/column; outputs are left untouched.
+ *  - Ownership: the CALLER owns every buffer passed in (device amplitude and scratch
+ *    buffers typically come from torch.empty on the context's device).  The library owns
+ *    only the opaque host handles it returns, small device plan buffers and a bounded
+ *    device staging area inside each rcs_state, all released by the matching *_free.
+ *  - Synchrony: calls are stream-ordered on the context's CUDA stream and return after
+ *    that stream has drained, so results are ready and timings are explicit.
+ *  - Multi-GPU (SPMD): with world > 1 every rank makes the same calls in the same order;
+ *    build, norm, sample, probabilities and XEB are collectives over the context's NCCL
+ *    communicator (NVLink / NVSwitch).
+ *  - Bit order (reading V1): amplitude index i encodes qubit q as bit q
+ *    (qubit 0 = least significant); bitstrings are uint64 with the same encoding, n <= 63.
+ *  - Amplitudes are complex64, interleaved (re, im) float32 -- the layout of
+ *    torch.complex64.  A rank's shard holds 2^(n-g) amplitudes, g = log2(world).
+ */
+#ifndef RCS_H
+#define RCS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RCS_OK = 0,
+    RCS_ERR_PARSE = 1,          /* QASM syntax error; err->line/col set          */
+    RCS_ERR_UNKNOWN_GATE = 2,   /* gate name outside the dialect                  */
+    RCS_ERR_QUBIT_RANGE = 3,    /* qubit index >= declared qreg size                          */
+    RCS_ERR_ARITY = 4,          /* wrong parameter / qubit count, or a repeated qubit         */
+    RCS_ERR_MEMORY = 5,         /* buffer too small; err->bytes_required set     */
+    RCS_ERR_NORM = 6,           /* |T - 1| > 1e-5 at sampling (BASELINE tolerance) */
+    RCS_ERR_SIZE = 7,           /* bitstring >= 2^n                              */
+    RCS_ERR_ARG = 8,            /* invalid argument / unsupported configuration               */
+    RCS_ERR_CUDA = 9,           /* CUDA runtime error (message has cudaGetErrorString)        */
+    RCS_ERR_NCCL = 10           /* NCCL error (message has ncclGetErrorString)                */
+} rcs_status;
+
+typedef struct {
+    int code;                   /* rcs_status */
+    int line, col;              /* 1-based position of a parse error, else 0 */
+    uint64_t bytes_required;    /* set with RCS_ERR_MEMORY */
+    char msg[256];
+} rcs_error;
+
+typedef struct rcs_circuit rcs_circuit;   /* parsed circuit: host, immutable, thread-safe to share */
+typedef struct rcs_context rcs_context;   /* one per rank: device, stream, NCCL communicator */
+typedef struct rcs_state rcs_state;       /* small host handle describing a built state */
+typedef struct rcs_plan rcs_plan;         /* host-only execution plan (fused passes + remaps) */
+
+/* gate kinds: */
+enum { RCS_GATE_SX = 0, RCS_GATE_SY = 1, RCS_GATE_SW = 2, RCS_GATE_RZ = 3, RCS_GATE_FSIM = 4 };
+
+typedef struct {
+    int n_qubits, n_moments, n_gates, n_measure;
+    int n_sx, n_sy, n_sw, n_rz, n_fsim;   /* per-kind counts */
+} rcs_circuit_counts;
+
+typedef struct {
+    int fuse_k;              /* max qubits per fused dense block, 1..5 (0 -> 4)                 */
+    int block_bits;          /* sampling block: 2^b amplitudes per fp64 CDF entry (0 -> 6)      */
+    int virtual_global;      /* world == 1 only: treat the top g qubits as global and run every
+                                remap as an in-device bit swap (tests the sharded plan on 1 GPU) */
+    int timing;              /* 1: record a CUDA-event pair around every pass / remap             */
+    uint64_t staging_bytes;  /* bound of the remap staging area (0 -> 256 MiB)                   */
+} rcs_build_opts;
+
+typedef struct {
+    int n_passes;            /* fused dense gate passes (K1) executed on this rank              */
+    int n_remaps;            /* global<->local qubit remaps (all-to-all exchanges)               */
+    int n_swaps;             /* local bit-swap passes (final layout restore)                     */
+    int fuse_k;
+    double plan_ms;          /* host: fusion + remap planning                                    */
+    double build_ms;         /* device: init .. final norm, CUDA events on the context stream    */
+    double pass_ms;          /* timing=1: sum of gate-pass kernel times                          */
+    double pass_ms_min, pass_ms_max;
+    double remap_ms;         /* timing=1: sum of remap times (pack + NCCL + unpack)              */
+    double blocksum_ms;      /* timing=1: block-sum + scan (sampling CDF) time                   */
+    uint64_t pass_bytes;     /* algorithmic bytes of all gate passes on this rank (16 B/amp/pass) */
+    uint64_t remap_bytes;    /* bytes this rank sent over NCCL                                   */
+    double norm;             /* sum |psi|^2 over all ranks                                       */
+} rcs_build_report;
+
+typedef struct {
+    uint64_t shots;
+    double total_prob;       /* T used for t_s = u_s * T (reading V13)                           */
+    double sample_ms;        /* device time of the per-shot search + gather                       */
+} rcs_sample_report;
+
+typedef struct {
+    int n_qubits;
+    uint64_t shots;
+    double F;                /* 2^n * mean p(x_s) - 1   (reading V14)                */
+    double sigma;            /* 2^n * stdev(p, ddof=1) / sqrt(S)                                  */
+    double mean_p;
+    double fstar;            /* 2^n * sum_x p_x^2 - 1 of the built state (ideal-sampler XEB)      */
+} rcs_xeb_report;
+
+/* Plan inspection (host only, no GPU): one item per device step. */
+enum { RCS_ITEM_PASS = 0, RCS_ITEM_REMAP = 1, RCS_ITEM_SWAP = 2 };
+typedef struct {
+    int type;                /* RCS_ITEM_*                                                        */
+    int k;                   /* PASS: block width; REMAP/SWAP: number of position pairs           */
+    int qubits[8];           /* PASS: logical qubits, matrix bit i <-> qubits[i] (ascending)      */
+    int pos[8];              /* PASS: physical bit position of matrix bit i                       */
+    int a[8], b[8];          /* REMAP: a = global position, b = local position (swapped pairwise);
+                                SWAP: disjoint local position pairs swapped in one pass            */
+    int n_gates;             /* PASS: source gates fused into this block                          */
+} rcs_plan_item;
+
+const char *rcs_status_string(int status);
+/* Cumulative number of CUDA kernels this library has launched in this process (all
+ * contexts); benchmarks difference it around a timed region. */
+uint64_t rcs_kernel_launches(void);
+
+/* ---- circuit (host) ------------------------------------------------------------------ */
+/* Parse `len` bytes of QASM (dialect: DESIGN.md §3 V5). */
+rcs_status rcs_circuit_load_qasm(const char *text, size_t len, rcs_circuit **out, rcs_error *err);
+rcs_status rcs_circuit_stats(const rcs_circuit *c, rcs_circuit_counts *out);
+/* Gate i in source order; q1 = -1 for 1-qubit gates; rz stores its angle in *phi. */
+rcs_status rcs_circuit_gate(const rcs_circuit *c, int i, int *kind, int *q0, int *q1,
+                            double *theta, double *phi, int *moment);
+void rcs_circuit_free(rcs_circuit *c);
+
+/* ---- plan (host) -------------------------------------------------------------------- */
+/* Fuse the circuit into dense blocks of <= fuse_k qubits and schedule remaps for
+ * n_global = log2(world) global qubits (BASELINE.json north_star).  The fusion is
+ * independent of n_global. */
+rcs_status rcs_plan_create(const rcs_circuit *c, int fuse_k, int n_global, rcs_plan **out, rcs_error *err);
+rcs_status rcs_plan_summary(const rcs_plan *p, int *n_items, int *n_passes, int *n_remaps, int *n_swaps);
+/* matrix_out (may be NULL): 2 * 4^k doubles, row-major interleaved complex, fp64 product. */
+rcs_status rcs_plan_item_get(const rcs_plan *p, int i, rcs_plan_item *out, double *matrix_out);
+void rcs_plan_free(rcs_plan *p);
+
+/* ---- context ------------------------------------------------------------------------ */
+/* NCCL bootstrap: rank 0 calls rcs_nccl_unique_id (128 bytes) and the caller broadcasts the
+ * bytes to every rank (e.g. torch.distributed.broadcast_object_list). */
+int rcs_nccl_unique_id_bytes(void);
+rcs_status rcs_nccl_unique_id(void *out_bytes, rcs_error *err);
+/* world must be a power of two; nccl_id is ignored (may be NULL) when world == 1.
+ * cuda_stream: a cudaStream_t on `device` (NULL = legacy default stream). */
+rcs_status rcs_context_create(int device, int rank, int world, const void *nccl_id,
+                              void *cuda_stream, rcs_context **out, rcs_error *err);
+void rcs_context_free(rcs_context *ctx);
+
+/* ---- state -------------------------------------------------------------------------- */
+/* Device scratch needed by rcs_state_build (fp64 block-CDF + remap staging). */
+rcs_status rcs_state_scratch_bytes(const rcs_context *ctx, const rcs_circuit *c,
+                                   const rcs_build_opts *opts, uint64_t *bytes);
+/* Build psi = U_G ... U_1 |0...0> into the caller's device buffer d_amps
+ * (2^(n-g) complex64 = amps_bytes; rank r holds logical indices [r 2^(n-g), (r+1) 2^(n-g))
+ * on return, i.e. canonical order).  d_scratch must hold rcs_state_scratch_bytes; the state
+ * keeps pointers to both buffers until rcs_state_free.  RCS_ERR_MEMORY (bytes_required) if a
+ * buffer is too small. */
+rcs_status rcs_state_build(rcs_context *ctx, const rcs_circuit *c, const rcs_build_opts *opts,
+                           void *d_amps, uint64_t amps_bytes, void *d_scratch, uint64_t scratch_bytes,
+                           rcs_state **out, rcs_build_report *rep, rcs_error *err);
+/* Per-pass kernel times (ms) of the last build (timing=1), in plan order; *n = count. */
+rcs_status rcs_state_pass_times(const rcs_state *s, float *ms, int cap, int *n);
+rcs_status rcs_state_norm(const rcs_state *s, double *norm);          /* collective */
+/* Copy `count` amplitudes starting at GLOBAL logical index `first` (must lie in this rank's
+ * shard) to dst (host or device memory, complex64). */
+rcs_status rcs_state_copy_out(const rcs_state *s, uint64_t first, uint64_t count, void *dst, rcs_error *err);
+/* p_out[i] = |psi_{x[i]}|^2; x and p_out host or device; collective. */
+rcs_status rcs_probabilities(const rcs_state *s, const uint64_t *x, uint64_t count, double *p_out,
+                             rcs_error *err);
+/* Draw `shots` bitstrings (readings V12/V13): u_s from SplitMix64(shot_seed) output
+ * shot_offset+s+1, t_s = u_s T, x_s = min{x : C(x) > t_s}.  out_x (host or device, `shots`
+ * entries in shot order) is filled on every rank.  Refuses |T - 1| > 1e-5 (RCS_ERR_NORM). */
+rcs_status rcs_sample(rcs_state *s, uint64_t shots, uint64_t shot_seed, uint64_t shot_offset,
+                      uint64_t *out_x, rcs_sample_report *rep, rcs_error *err);
+/* Test hook: the same search with caller-supplied uniforms u[s] in [0, 1) (host or device). */
+rcs_status rcs_sample_uniforms(rcs_state *s, const double *u, uint64_t shots, uint64_t *out_x,
+                               rcs_sample_report *rep, rcs_error *err);
+/* Linear XEB of bitstrings x (host or device) against this state. */
+rcs_status rcs_xeb(const rcs_state *s, const uint64_t *x, uint64_t count, rcs_xeb_report *out, rcs_error *err);
+void rcs_state_free(rcs_state *s);   /* frees the handle and its device plan/staging buffers */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RCS_H */

@@ -1,0 +1,269 @@
+"""B200-native exact state-vector RCS hot path (arXiv 2512.07311 problem statement).
+
+Thin Python binding over librcs.so (include/rcs.h).  Every step of the path -- gate
+fusion planning, state construction, remaps, sampling, XEB -- runs inside the library
+(C++ host planner + sm_100a CUDA kernels + NCCL).  This module only marshals arguments;
+PyTorch provides device memory, CUDA streams and the process group used to bootstrap NCCL.
+
+    from paper_2512_07311_b200 import Circuit, Context, State
+    c = Circuit.from_qasm(text)                      # PAPER §3.2 l.34
+    ctx = Context()                                  # cuda:0, world 1  (or Context.from_process_group())
+    st = State.build(ctx, c, fuse_k=4)               # PAPER §3.2 l.36
+    x = st.sample(1_000_000, seed=2512)              # PAPER §3.2 l.38
+    rep = st.xeb(x)                                  # PAPER §3.2 l.39, §5.1
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import (RcsError, check, lib, rcs_build_opts, rcs_build_report, rcs_circuit_counts, rcs_error,
+                   rcs_plan_item, rcs_sample_report, rcs_xeb_report)
+
+__all__ = ["Circuit", "Plan", "Context", "State", "RcsError", "lib"]
+
+KIND_NAMES = {0: "sx", 1: "sy", 2: "sw", 3: "rz", 4: "fsim"}
+ITEM_NAMES = {0: "pass", 1: "remap", 2: "swap"}
+
+
+def _ptr(t):
+    """Raw pointer of a torch tensor or numpy array."""
+    if hasattr(t, "data_ptr"):
+        return C.c_void_p(t.data_ptr())
+    return C.c_void_p(t.ctypes.data)
+
+
+class Circuit:
+    """Parsed QASM circuit (host; rcs_circuit_load_qasm)."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+
+    @classmethod
+    def from_qasm(cls, text: str) -> "Circuit":
+        b = text.encode()
+        h = C.c_void_p()
+        err = rcs_error()
+        check(lib().rcs_circuit_load_qasm(b, len(b), C.byref(h), C.byref(err)), err, "rcs_circuit_load_qasm")
+        return cls(h.value)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().rcs_circuit_free(h)
+            self._h = None
+
+    def stats(self) -> dict:
+        s = rcs_circuit_counts()
+        check(lib().rcs_circuit_stats(self._h, C.byref(s)), None, "rcs_circuit_stats")
+        return {f: getattr(s, f) for f, _ in s._fields_}
+
+    @property
+    def n_qubits(self) -> int:
+        return self.stats()["n_qubits"]
+
+    def gates(self) -> list:
+        out = []
+        k, q0, q1, m = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        th, ph = C.c_double(), C.c_double()
+        for i in range(self.stats()["n_gates"]):
+            check(lib().rcs_circuit_gate(self._h, i, C.byref(k), C.byref(q0), C.byref(q1), C.byref(th),
+                                         C.byref(ph), C.byref(m)), None, "rcs_circuit_gate")
+            qs = (q0.value,) if q1.value < 0 else (q0.value, q1.value)
+            out.append((KIND_NAMES[k.value], qs, th.value, ph.value, m.value))
+        return out
+
+
+class Plan:
+    """Host-only fused plan (rcs_plan_create): blocks, remaps, restore swaps."""
+
+    def __init__(self, circuit: Circuit, fuse_k: int = 4, n_global: int = 0):
+        self.circuit = circuit
+        h = C.c_void_p()
+        err = rcs_error()
+        check(lib().rcs_plan_create(circuit._h, fuse_k, n_global, C.byref(h), C.byref(err)), err, "rcs_plan_create")
+        self._h = h
+        ni, npa, nr, ns = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        lib().rcs_plan_summary(h, C.byref(ni), C.byref(npa), C.byref(nr), C.byref(ns))
+        self.n_items, self.n_passes, self.n_remaps, self.n_swaps = ni.value, npa.value, nr.value, ns.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().rcs_plan_free(h)
+            self._h = None
+
+    def items(self) -> list:
+        out = []
+        it = rcs_plan_item()
+        for i in range(self.n_items):
+            mat = np.zeros(2 * 4 ** 5, dtype=np.float64)
+            check(lib().rcs_plan_item_get(self._h, i, C.byref(it), mat.ctypes.data_as(C.POINTER(C.c_double))),
+                  None, "rcs_plan_item_get")
+            d = {"type": ITEM_NAMES[it.type], "k": it.k}
+            if it.type == 0:
+                D = 1 << it.k
+                d["qubits"] = list(it.qubits[:it.k])
+                d["pos"] = list(it.pos[:it.k])
+                d["n_gates"] = it.n_gates
+                d["matrix"] = mat[:2 * D * D].view(np.complex128).reshape(D, D).copy()
+            else:
+                d["a"] = list(it.a[:it.k])
+                d["b"] = list(it.b[:it.k])
+            out.append(d)
+        return out
+
+
+class Context:
+    """One per rank: device, CUDA stream and (world > 1) the NCCL communicator."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None, stream=None):
+        import torch
+        self.device = device
+        self.rank, self.world = rank, world
+        torch.cuda.set_device(device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
+        h = C.c_void_p()
+        err = rcs_error()
+        idbuf = C.create_string_buffer(nccl_id, len(nccl_id)) if nccl_id else None
+        check(lib().rcs_context_create(device, rank, world, idbuf, C.c_void_p(self.stream.cuda_stream),
+                                       C.byref(h), C.byref(err)), err, "rcs_context_create")
+        self._h = h
+
+    @classmethod
+    def from_process_group(cls, device: int | None = None) -> "Context":
+        """SPMD bootstrap over an initialised torch.distributed process group (any backend):
+        rank 0 draws the NCCL unique id and broadcasts it."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        if device is None:
+            device = rank % max(1, torch.cuda.device_count())
+        nid = None
+        if world > 1:
+            obj = [None]
+            if rank == 0:
+                n = lib().rcs_nccl_unique_id_bytes()
+                buf = C.create_string_buffer(n)
+                err = rcs_error()
+                check(lib().rcs_nccl_unique_id(buf, C.byref(err)), err, "rcs_nccl_unique_id")
+                obj = [bytes(buf.raw)]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
+        return cls(device, rank, world, nid)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().rcs_context_free(h)
+            self._h = None
+
+
+class State:
+    """A built state: amplitudes in a torch complex64 tensor owned by this object."""
+
+    def __init__(self):
+        self._h = None
+
+    @classmethod
+    def build(cls, ctx: Context, circuit: Circuit, fuse_k: int = 4, block_bits: int = 0, virtual_global: int = 0,
+              timing: bool = False, staging_bytes: int = 0, amps=None, scratch=None) -> "State":
+        import torch
+        n = circuit.n_qubits
+        g = ctx.world.bit_length() - 1
+        opts = rcs_build_opts(fuse_k, block_bits, virtual_global, 1 if timing else 0, staging_bytes)
+        sb = C.c_uint64()
+        check(lib().rcs_state_scratch_bytes(ctx._h, circuit._h, C.byref(opts), C.byref(sb)), None,
+              "rcs_state_scratch_bytes")
+        dev = torch.device("cuda", ctx.device)
+        if amps is None:
+            amps = torch.empty(1 << (n - g), dtype=torch.complex64, device=dev)
+        if scratch is None or scratch.numel() < sb.value:
+            scratch = torch.empty(sb.value, dtype=torch.uint8, device=dev)
+        self = cls()
+        self.ctx, self.circuit, self.n, self.g = ctx, circuit, n, g
+        self.amps, self.scratch = amps, scratch
+        h = C.c_void_p()
+        rep = rcs_build_report()
+        err = rcs_error()
+        # the library runs on ctx.stream; order it after torch's allocations/initialisation
+        ctx.stream.wait_stream(torch.cuda.current_stream(dev))
+        check(lib().rcs_state_build(ctx._h, circuit._h, C.byref(opts), _ptr(amps), amps.numel() * 8, _ptr(scratch),
+                                    scratch.numel(), C.byref(h), C.byref(rep), C.byref(err)), err, "rcs_state_build")
+        self._h = h
+        self.report = {f: getattr(rep, f) for f, _ in rep._fields_}
+        return self
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().rcs_state_free(h)
+            self._h = None
+
+    def free(self):
+        self.__del__()
+
+    @property
+    def norm(self) -> float:
+        v = C.c_double()
+        check(lib().rcs_state_norm(self._h, C.byref(v)), None, "rcs_state_norm")
+        return v.value
+
+    def pass_times(self) -> np.ndarray:
+        n = C.c_int()
+        lib().rcs_state_pass_times(self._h, None, 0, C.byref(n))
+        out = np.zeros(n.value, dtype=np.float32)
+        lib().rcs_state_pass_times(self._h, out.ctypes.data_as(C.POINTER(C.c_float)), n.value, C.byref(n))
+        return out
+
+    def copy_out(self, first: int = None, count: int = None) -> np.ndarray:
+        """complex64 amplitudes [first, first+count) (global logical index, this rank's shard)."""
+        nl = self.n - self.g
+        base = self.ctx.rank << nl
+        first = base if first is None else first
+        count = (1 << nl) - (first - base) if count is None else count
+        out = np.empty(count, dtype=np.complex64)
+        err = rcs_error()
+        check(lib().rcs_state_copy_out(self._h, first, count, _ptr(out), C.byref(err)), err, "rcs_state_copy_out")
+        return out
+
+    def probabilities(self, x) -> np.ndarray:
+        xa = np.ascontiguousarray(np.asarray(x, dtype=np.uint64)) if not hasattr(x, "data_ptr") else x
+        p = np.empty(len(xa), dtype=np.float64)
+        err = rcs_error()
+        check(lib().rcs_probabilities(self._h, _ptr(xa), len(xa), _ptr(p), C.byref(err)), err, "rcs_probabilities")
+        return p
+
+    def sample(self, shots: int, seed: int = 2512, offset: int = 0, device: bool = False):
+        """Bitstrings (uint64, qubit 0 = LSB) in shot order: numpy (host) or torch (device)."""
+        import torch
+        if device:
+            out = torch.empty(shots, dtype=torch.int64, device=torch.device("cuda", self.ctx.device))
+        else:
+            out = np.empty(shots, dtype=np.uint64)
+        rep = rcs_sample_report()
+        err = rcs_error()
+        check(lib().rcs_sample(self._h, shots, seed, offset, _ptr(out), C.byref(rep), C.byref(err)), err, "rcs_sample")
+        self.last_sample = {f: getattr(rep, f) for f, _ in rep._fields_}
+        return out
+
+    def sample_uniforms(self, u) -> np.ndarray:
+        u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+        out = np.empty(u.size, dtype=np.uint64)
+        rep = rcs_sample_report()
+        err = rcs_error()
+        check(lib().rcs_sample_uniforms(self._h, _ptr(u), u.size, _ptr(out), C.byref(rep), C.byref(err)), err,
+              "rcs_sample_uniforms")
+        return out
+
+    def xeb(self, x) -> dict:
+        if not hasattr(x, "data_ptr"):
+            x = np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
+            n = x.size
+        else:
+            n = x.numel()
+        rep = rcs_xeb_report()
+        err = rcs_error()
+        check(lib().rcs_xeb(self._h, _ptr(x), n, C.byref(rep), C.byref(err)), err, "rcs_xeb")
+        return {f: getattr(rep, f) for f, _ in rep._fields_}

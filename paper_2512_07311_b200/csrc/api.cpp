@@ -1,0 +1,729 @@
+// api.cpp -- the C ABI of include/rcs.h: orchestration of plan items on the context stream,
+// NCCL remaps (grouped send/recv over NVLink), sampling and XEB collectives.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.h"
+
+using namespace rcs;
+
+struct rcs_context {
+    int device = 0, rank = 0, world = 1, g = 0;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+};
+
+struct rcs_state {
+    rcs_context* ctx = nullptr;
+    int n = 0, g = 0, nl = 0;       // g: real global bits (log2 world)
+    float2* amps = nullptr;
+    uint64_t n_amps = 0;
+    // scratch carve-up
+    double* inc = nullptr;          // block sums -> inclusive prefix
+    uint64_t nblocks = 0;
+    int b = 0;
+    double* scan_tmp = nullptr;
+    double* part_sq = nullptr;
+    double* misc = nullptr;         // small device results
+    float2* staging = nullptr;
+    uint64_t staging_elems = 0;
+    // library-owned device buffers
+    unsigned long long* xbuf = nullptr;  // shot / bitstring chunk
+    double* dbuf = nullptr;              // uniforms / probabilities chunk
+    double* xeb_part = nullptr;
+    int* bad = nullptr;
+    uint64_t chunk = 0;
+    // sampling CDF summary
+    double T_r = 0, T_total = 0, E_r = 0, sum_sq = 0;
+    int owns_tail = 0, owns_any = 0;
+    std::vector<float> pass_ms;
+};
+
+namespace {
+
+constexpr uint64_t kChunkShots = 1ull << 22;
+constexpr uint64_t kAlign = 256;
+
+uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e__ = (expr);                                                          \
+        if (e__ != cudaSuccess) {                                                          \
+            set_error(err, RCS_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e__));        \
+            return RCS_ERR_CUDA;                                                           \
+        }                                                                                  \
+    } while (0)
+
+#define NCCL_TRY(expr)                                                                     \
+    do {                                                                                   \
+        ncclResult_t r__ = (expr);                                                         \
+        if (r__ != ncclSuccess) {                                                          \
+            set_error(err, RCS_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r__));        \
+            return RCS_ERR_NCCL;                                                           \
+        }                                                                                  \
+    } while (0)
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int log2_exact(int w) {
+    int g = 0;
+    while ((1 << g) < w) g++;
+    return (1 << g) == w ? g : -1;
+}
+
+struct Layout {
+    int b;
+    uint64_t nblocks, inc_off, tmp_off, part_off, misc_off, stage_off, total;
+};
+
+Layout scratch_layout(int nl, int world, int virt, uint64_t staging_bytes, int block_bits) {
+    Layout L{};
+    int b = block_bits > 0 ? block_bits : 6;
+    if (b > 6) b = 6;
+    if (b > nl) b = nl;
+    L.b = b;
+    L.nblocks = 1ull << (nl - b);
+    L.inc_off = 0;
+    L.tmp_off = align_up(L.inc_off + L.nblocks * 8);
+    L.part_off = align_up(L.tmp_off + dev::scan_tmp_doubles(L.nblocks) * 8);
+    L.misc_off = align_up(L.part_off + (uint64_t)dev::block_sums_grid() * 8);
+    L.stage_off = align_up(L.misc_off + 64 * 8);
+    uint64_t st = 0;
+    if (world > 1) st = staging_bytes ? staging_bytes : (256ull << 20);
+    (void)virt;
+    L.total = align_up(L.stage_off + st);
+    return L;
+}
+
+// Exchange for one REMAP item over NCCL: swap global positions a[i] with local b[i].
+rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_error* err) {
+    rcs_context* c = s->ctx;
+    const int j = it.k, nl = s->nl;
+    int lpos[8];
+    for (int i = 0; i < j; i++) lpos[i] = it.b[i];
+    std::sort(lpos, lpos + j);
+    int my_code = 0;
+    for (int i = 0; i < j; i++) my_code |= ((c->rank >> (it.a[i] - nl)) & 1) << i;
+    std::vector<int> codes, peers;
+    std::vector<uint64_t> masks;
+    for (int code = 0; code < (1 << j); code++) {
+        if (code == my_code) continue;
+        int peer = c->rank;
+        uint64_t mask = 0;
+        for (int i = 0; i < j; i++) {
+            const int gb = it.a[i] - nl;
+            peer = (peer & ~(1 << gb)) | (((code >> i) & 1) << gb);
+            if ((code >> i) & 1) mask |= 1ull << it.b[i];
+        }
+        codes.push_back(code);
+        peers.push_back(peer);
+        masks.push_back(mask);
+    }
+    const int np = (int)peers.size();
+    const uint64_t count = 1ull << (nl - j);
+    uint64_t E = s->staging_elems / (2ull * np);
+    if (E > count) E = count;
+    if (E == 0) {
+        set_error(err, RCS_ERR_MEMORY, "remap staging too small");
+        return RCS_ERR_MEMORY;
+    }
+    for (uint64_t m0 = 0; m0 < count; m0 += E) {
+        const uint64_t e = std::min(E, count - m0);
+        for (int p = 0; p < np; p++)
+            CUDA_TRY(dev::pack(s->amps, s->staging + (uint64_t)p * E, j, lpos, masks[p], m0, e, c->stream));
+        NCCL_TRY(ncclGroupStart());
+        for (int p = 0; p < np; p++) {
+            NCCL_TRY(ncclSend(s->staging + (uint64_t)p * E, e * 2, ncclFloat, peers[p], c->comm, c->stream));
+            NCCL_TRY(ncclRecv(s->staging + (uint64_t)(np + p) * E, e * 2, ncclFloat, peers[p], c->comm, c->stream));
+        }
+        NCCL_TRY(ncclGroupEnd());
+        for (int p = 0; p < np; p++)
+            CUDA_TRY(dev::unpack(s->amps, s->staging + (uint64_t)(np + p) * E, j, lpos, masks[p], m0, e, c->stream));
+        *bytes_sent += e * 8ull * np;
+    }
+    return RCS_OK;
+}
+
+// block sums + scan + shard totals (collective); fills s->T_*, E_r, sum_sq, ownership
+rcs_status compute_cdf(rcs_state* s, rcs_error* err) {
+    rcs_context* c = s->ctx;
+    CUDA_TRY(dev::block_sums(s->amps, s->nblocks, s->b, s->inc, s->part_sq, c->stream));
+    CUDA_TRY(dev::scan_inclusive(s->inc, s->nblocks, s->scan_tmp, c->stream));
+    CUDA_TRY(dev::reduce_sum(s->part_sq, dev::block_sums_grid(), s->misc + 1, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->misc, s->inc + (s->nblocks - 1), sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    std::vector<double> tot(c->world, 0.0);
+    double sq = 0.0;
+    if (c->world > 1) {
+        // misc[8..8+world): gathered shard totals; misc[2]: global sum p^2
+        NCCL_TRY(ncclAllGather(s->misc, s->misc + 8, 1, ncclDouble, c->comm, c->stream));
+        NCCL_TRY(ncclAllReduce(s->misc + 1, s->misc + 2, 1, ncclDouble, ncclSum, c->comm, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(tot.data(), s->misc + 8, sizeof(double) * c->world, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(&sq, s->misc + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(tot.data(), s->misc, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaMemcpyAsync(&sq, s->misc + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    double E = 0.0, T = 0.0;
+    int last_owner = -1;
+    for (int r = 0; r < c->world; r++) {
+        if (r == c->rank) s->E_r = E;
+        E += tot[r];
+        if (tot[r] > 0) last_owner = r;
+    }
+    T = E;
+    s->T_r = tot[c->rank];
+    s->T_total = T;
+    s->sum_sq = sq;
+    s->owns_any = s->T_r > 0 ? 1 : 0;
+    s->owns_tail = c->rank == last_owner ? 1 : 0;
+    return RCS_OK;
+}
+
+rcs_status ensure_buffers(rcs_state* s, rcs_error* err) {
+    if (s->xbuf) return RCS_OK;
+    s->chunk = kChunkShots;
+    CUDA_TRY(cudaMalloc(&s->xbuf, s->chunk * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMalloc(&s->dbuf, s->chunk * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&s->xeb_part, (size_t)dev::xeb_grid() * 3 * sizeof(double) + 64));
+    CUDA_TRY(cudaMalloc(&s->bad, sizeof(int)));
+    return RCS_OK;
+}
+
+rcs_status sample_impl(rcs_state* s, uint64_t shots, uint64_t seed, uint64_t offset, const double* u,
+                       uint64_t* out_x, rcs_sample_report* rep, rcs_error* err) {
+    if (!s || (!out_x && shots)) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    rcs_context* c = s->ctx;
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (!(std::fabs(s->T_total - 1.0) <= 1e-5)) {
+        set_error(err, RCS_ERR_NORM, "state norm %.9g deviates from 1 by more than 1e-5", s->T_total);
+        return RCS_ERR_NORM;
+    }
+    rcs_status st = ensure_buffers(s, err);
+    if (st) return st;
+    const bool out_dev = is_device_ptr(out_x);
+    const bool u_dev = u ? is_device_ptr(u) : false;
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, c->stream));
+    for (uint64_t s0 = 0; s0 < shots; s0 += s->chunk) {
+        const uint64_t cnt = std::min(s->chunk, shots - s0);
+        unsigned long long* xo = out_dev ? reinterpret_cast<unsigned long long*>(out_x) + s0 : s->xbuf;
+        dev::SampleArgs A{};
+        A.amps = s->amps;
+        A.inc = s->inc;
+        A.nblocks = s->nblocks;
+        A.b = s->b;
+        A.T_total = s->T_total;
+        A.E_r = s->E_r;
+        A.T_r = s->T_r;
+        A.owns_tail = s->owns_tail;
+        A.owns_any = s->owns_any;
+        A.seed = seed;
+        A.shot0 = offset + s0;
+        A.shots = cnt;
+        A.u_in = nullptr;
+        if (u) {
+            if (u_dev) {
+                A.u_in = u + s0;
+            } else {
+                CUDA_TRY(cudaMemcpyAsync(s->dbuf, u + s0, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                A.u_in = s->dbuf;
+            }
+        }
+        A.base_index = (uint64_t)c->rank << s->nl;
+        A.x_out = xo;
+        CUDA_TRY(dev::sample(A, c->stream));
+        if (c->world > 1)
+            NCCL_TRY(ncclAllReduce(xo, xo, cnt, ncclUint64, ncclSum, c->comm, c->stream));
+        if (!out_dev)
+            CUDA_TRY(cudaMemcpyAsync(out_x + s0, xo, cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(cudaEventRecord(e1, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rep) {
+        rep->shots = shots;
+        rep->total_prob = s->T_total;
+        rep->sample_ms = ms;
+    }
+    return RCS_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char* rcs_status_string(int s) {
+    switch (s) {
+        case RCS_OK: return "RCS_OK";
+        case RCS_ERR_PARSE: return "RCS_ERR_PARSE";
+        case RCS_ERR_UNKNOWN_GATE: return "RCS_ERR_UNKNOWN_GATE";
+        case RCS_ERR_QUBIT_RANGE: return "RCS_ERR_QUBIT_RANGE";
+        case RCS_ERR_ARITY: return "RCS_ERR_ARITY";
+        case RCS_ERR_MEMORY: return "RCS_ERR_MEMORY";
+        case RCS_ERR_NORM: return "RCS_ERR_NORM";
+        case RCS_ERR_SIZE: return "RCS_ERR_SIZE";
+        case RCS_ERR_ARG: return "RCS_ERR_ARG";
+        case RCS_ERR_CUDA: return "RCS_ERR_CUDA";
+        case RCS_ERR_NCCL: return "RCS_ERR_NCCL";
+        default: return "RCS_ERR_UNKNOWN";
+    }
+}
+
+rcs_status rcs_circuit_load_qasm(const char* text, size_t len, rcs_circuit** out, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!text || !out) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    rcs_circuit* c = new (std::nothrow) rcs_circuit();
+    if (!c) { set_error(err, RCS_ERR_MEMORY, "out of host memory"); return RCS_ERR_MEMORY; }
+    rcs_status st = parse_qasm(text, len, c->c, err);
+    if (st != RCS_OK) { delete c; return st; }
+    *out = c;
+    return RCS_OK;
+}
+
+rcs_status rcs_circuit_stats(const rcs_circuit* c, rcs_circuit_counts* o) {
+    if (!c || !o) return RCS_ERR_ARG;
+    std::memset(o, 0, sizeof *o);
+    o->n_qubits = c->c.n;
+    o->n_moments = c->c.n_moments;
+    o->n_gates = (int)c->c.gates.size();
+    o->n_measure = c->c.n_measure;
+    for (const auto& g : c->c.gates) {
+        switch (g.kind) {
+            case RCS_GATE_SX: o->n_sx++; break;
+            case RCS_GATE_SY: o->n_sy++; break;
+            case RCS_GATE_SW: o->n_sw++; break;
+            case RCS_GATE_RZ: o->n_rz++; break;
+            default: o->n_fsim++;
+        }
+    }
+    return RCS_OK;
+}
+
+rcs_status rcs_circuit_gate(const rcs_circuit* c, int i, int* kind, int* q0, int* q1, double* theta, double* phi,
+                            int* moment) {
+    if (!c || i < 0 || i >= (int)c->c.gates.size()) return RCS_ERR_ARG;
+    const Gate& g = c->c.gates[i];
+    if (kind) *kind = g.kind;
+    if (q0) *q0 = g.q0;
+    if (q1) *q1 = g.q1;
+    if (theta) *theta = g.theta;
+    if (phi) *phi = g.phi;
+    if (moment) *moment = g.moment;
+    return RCS_OK;
+}
+
+void rcs_circuit_free(rcs_circuit* c) { delete c; }
+
+uint64_t rcs_kernel_launches(void) { return dev::launches(); }
+
+rcs_status rcs_plan_create(const rcs_circuit* c, int fuse_k, int n_global, rcs_plan** out, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!c || !out) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    rcs_plan* p = new (std::nothrow) rcs_plan();
+    if (!p) return RCS_ERR_MEMORY;
+    rcs_status st = build_plan(c->c, fuse_k, n_global, p->p, err);
+    if (st) { delete p; return st; }
+    *out = p;
+    return RCS_OK;
+}
+
+rcs_status rcs_plan_summary(const rcs_plan* p, int* n_items, int* n_passes, int* n_remaps, int* n_swaps) {
+    if (!p) return RCS_ERR_ARG;
+    if (n_items) *n_items = (int)p->p.items.size();
+    if (n_passes) *n_passes = p->p.n_passes;
+    if (n_remaps) *n_remaps = p->p.n_remaps;
+    if (n_swaps) *n_swaps = p->p.n_swaps;
+    return RCS_OK;
+}
+
+rcs_status rcs_plan_item_get(const rcs_plan* p, int i, rcs_plan_item* o, double* matrix_out) {
+    if (!p || !o || i < 0 || i >= (int)p->p.items.size()) return RCS_ERR_ARG;
+    const Item& it = p->p.items[i];
+    std::memset(o, 0, sizeof *o);
+    o->type = it.type;
+    o->k = it.k;
+    for (int t = 0; t < 8; t++) {
+        o->pos[t] = it.pos[t];
+        o->a[t] = it.a[t];
+        o->b[t] = it.b[t];
+        o->qubits[t] = -1;
+    }
+    if (it.type == RCS_ITEM_PASS) {
+        const Block& B = p->p.blocks[it.block];
+        for (int t = 0; t < it.k; t++) o->qubits[t] = B.qubits[t];
+        o->n_gates = (int)B.gate_ids.size();
+        if (matrix_out)
+            for (size_t e = 0; e < B.matrix.size(); e++) {
+                matrix_out[2 * e] = B.matrix[e].re;
+                matrix_out[2 * e + 1] = B.matrix[e].im;
+            }
+    }
+    return RCS_OK;
+}
+
+void rcs_plan_free(rcs_plan* p) { delete p; }
+
+int rcs_nccl_unique_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
+
+rcs_status rcs_nccl_unique_id(void* out, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!out) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof id);
+    return RCS_OK;
+}
+
+rcs_status rcs_context_create(int device, int rank, int world, const void* nccl_id, void* stream, rcs_context** out,
+                              rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!out || world < 1 || rank < 0 || rank >= world) { set_error(err, RCS_ERR_ARG, "bad rank/world"); return RCS_ERR_ARG; }
+    const int g = log2_exact(world);
+    if (g < 0) { set_error(err, RCS_ERR_ARG, "world=%d is not a power of two", world); return RCS_ERR_ARG; }
+    if (world > 1 && !nccl_id) { set_error(err, RCS_ERR_ARG, "world > 1 needs an NCCL unique id"); return RCS_ERR_ARG; }
+    CUDA_TRY(cudaSetDevice(device));
+    rcs_context* c = new (std::nothrow) rcs_context();
+    if (!c) return RCS_ERR_MEMORY;
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    c->g = g;
+    c->stream = reinterpret_cast<cudaStream_t>(stream);
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            set_error(err, RCS_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+            delete c;
+            return RCS_ERR_NCCL;
+        }
+    }
+    *out = c;
+    return RCS_OK;
+}
+
+void rcs_context_free(rcs_context* c) {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+}
+
+rcs_status rcs_state_scratch_bytes(const rcs_context* ctx, const rcs_circuit* c, const rcs_build_opts* opts,
+                                   uint64_t* bytes) {
+    if (!ctx || !c || !bytes) return RCS_ERR_ARG;
+    rcs_build_opts o{};
+    if (opts) o = *opts;
+    const int nl = c->c.n - ctx->g;
+    if (nl < 1) return RCS_ERR_ARG;
+    *bytes = scratch_layout(nl, ctx->world, o.virtual_global, o.staging_bytes, o.block_bits).total;
+    return RCS_OK;
+}
+
+rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_build_opts* opts, void* d_amps,
+                           uint64_t amps_bytes, void* d_scratch, uint64_t scratch_bytes, rcs_state** out,
+                           rcs_build_report* rep, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!ctx || !circ || !d_amps || !out) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    rcs_build_opts o{};
+    if (opts) o = *opts;
+    const int n = circ->c.n;
+    const int g = ctx->g;
+    if (o.virtual_global && ctx->world > 1) {
+        set_error(err, RCS_ERR_ARG, "virtual_global needs world == 1");
+        return RCS_ERR_ARG;
+    }
+    const int plan_g = ctx->world > 1 ? g : o.virtual_global;
+    const int nl = n - g;
+    if (nl < 1) { set_error(err, RCS_ERR_ARG, "n=%d too small for world=%d", n, ctx->world); return RCS_ERR_ARG; }
+    const uint64_t n_amps = 1ull << nl;
+    if (amps_bytes < n_amps * 8) {
+        set_error(err, RCS_ERR_MEMORY, "amplitude buffer too small: need %llu bytes", (unsigned long long)(n_amps * 8));
+        if (err) err->bytes_required = n_amps * 8;
+        return RCS_ERR_MEMORY;
+    }
+    const Layout L = scratch_layout(nl, ctx->world, o.virtual_global, o.staging_bytes, o.block_bits);
+    if (!d_scratch || scratch_bytes < L.total) {
+        set_error(err, RCS_ERR_MEMORY, "scratch buffer too small: need %llu bytes", (unsigned long long)L.total);
+        if (err) err->bytes_required = L.total;
+        return RCS_ERR_MEMORY;
+    }
+    CUDA_TRY(cudaSetDevice(ctx->device));
+
+    auto t0 = std::chrono::steady_clock::now();
+    Plan P;
+    rcs_status st = build_plan(circ->c, o.fuse_k, plan_g, P, err);
+    if (st) return st;
+    auto t1 = std::chrono::steady_clock::now();
+
+    rcs_state* s = new (std::nothrow) rcs_state();
+    if (!s) return RCS_ERR_MEMORY;
+    s->ctx = ctx;
+    s->n = n;
+    s->g = g;
+    s->nl = nl;
+    s->amps = reinterpret_cast<float2*>(d_amps);
+    s->n_amps = n_amps;
+    char* sc = reinterpret_cast<char*>(d_scratch);
+    s->b = L.b;
+    s->nblocks = L.nblocks;
+    s->inc = reinterpret_cast<double*>(sc + L.inc_off);
+    s->scan_tmp = reinterpret_cast<double*>(sc + L.tmp_off);
+    s->part_sq = reinterpret_cast<double*>(sc + L.part_off);
+    s->misc = reinterpret_cast<double*>(sc + L.misc_off);
+    s->staging = reinterpret_cast<float2*>(sc + L.stage_off);
+    s->staging_elems = (L.total - L.stage_off) / sizeof(float2);
+
+    auto fail = [&](rcs_status code) {
+        delete s;
+        return code;
+    };
+#define BUILD_TRY(expr)                                                                    \
+    do {                                                                                   \
+        cudaError_t e__ = (expr);                                                          \
+        if (e__ != cudaSuccess) {                                                          \
+            set_error(err, RCS_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e__));        \
+            return fail(RCS_ERR_CUDA);                                                     \
+        }                                                                                  \
+    } while (0)
+
+    cudaStream_t stream = ctx->stream;
+    cudaEvent_t eb0, eb1, ec0;
+    BUILD_TRY(cudaEventCreate(&eb0));
+    BUILD_TRY(cudaEventCreate(&eb1));
+    BUILD_TRY(cudaEventCreate(&ec0));
+    std::vector<cudaEvent_t> ev;
+    if (o.timing) {
+        ev.resize(2 * P.items.size());
+        for (auto& e : ev) BUILD_TRY(cudaEventCreate(&e));
+    }
+    BUILD_TRY(cudaEventRecord(eb0, stream));
+    BUILD_TRY(dev::init_basis(s->amps, n_amps, ctx->rank == 0, stream));
+    uint64_t pass_bytes = 0, remap_bytes = 0;
+    std::vector<float> mbuf;
+    for (size_t ii = 0; ii < P.items.size(); ii++) {
+        const Item& it = P.items[ii];
+        if (o.timing) BUILD_TRY(cudaEventRecord(ev[2 * ii], stream));
+        if (it.type == RCS_ITEM_PASS) {
+            const Block& B = P.blocks[it.block];
+            mbuf.resize(2 * B.matrix.size());
+            for (size_t e = 0; e < B.matrix.size(); e++) {
+                mbuf[2 * e] = (float)B.matrix[e].re;
+                mbuf[2 * e + 1] = (float)B.matrix[e].im;
+            }
+            BUILD_TRY(dev::gate_pass(s->amps, nl, it.k, it.pos, mbuf.data(), stream));
+            pass_bytes += 16ull * n_amps;
+        } else if (it.type == RCS_ITEM_SWAP) {
+            BUILD_TRY(dev::bit_swap(s->amps, nl, it.k, it.a, it.b, stream));
+        } else {  // REMAP
+            if (ctx->world == 1) {
+                BUILD_TRY(dev::bit_swap(s->amps, nl, it.k, it.a, it.b, stream));
+            } else {
+                rcs_status r = do_remap_nccl(s, it, &remap_bytes, err);
+                if (r) return fail(r);
+            }
+        }
+        if (o.timing) BUILD_TRY(cudaEventRecord(ev[2 * ii + 1], stream));
+    }
+    BUILD_TRY(cudaEventRecord(ec0, stream));
+    st = compute_cdf(s, err);
+    if (st) return fail(st);
+    BUILD_TRY(cudaEventRecord(eb1, stream));
+    BUILD_TRY(cudaStreamSynchronize(stream));
+
+    rcs_build_report R{};
+    R.n_passes = P.n_passes;
+    R.n_remaps = P.n_remaps;
+    R.n_swaps = P.n_swaps;
+    R.fuse_k = P.fuse_k;
+    R.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, eb0, eb1);
+    R.build_ms = ms;
+    float cdf_ms = 0.f;
+    cudaEventElapsedTime(&cdf_ms, ec0, eb1);
+    R.pass_ms_min = 1e30;
+    R.pass_ms_max = 0;
+    s->pass_ms.clear();
+    if (o.timing) {
+        R.blocksum_ms = cdf_ms;
+        for (size_t ii = 0; ii < P.items.size(); ii++) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[2 * ii], ev[2 * ii + 1]);
+            if (P.items[ii].type == RCS_ITEM_PASS) {
+                R.pass_ms += t;
+                R.pass_ms_min = std::min(R.pass_ms_min, (double)t);
+                R.pass_ms_max = std::max(R.pass_ms_max, (double)t);
+                s->pass_ms.push_back(t);
+            } else {
+                R.remap_ms += t;
+            }
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+    if (R.pass_ms_min > R.pass_ms_max) R.pass_ms_min = 0;
+    cudaEventDestroy(eb0);
+    cudaEventDestroy(eb1);
+    cudaEventDestroy(ec0);
+    R.pass_bytes = pass_bytes;
+    R.remap_bytes = remap_bytes;
+    R.norm = s->T_total;
+    if (rep) *rep = R;
+    *out = s;
+    return RCS_OK;
+#undef BUILD_TRY
+}
+
+rcs_status rcs_state_pass_times(const rcs_state* s, float* ms, int cap, int* n) {
+    if (!s) return RCS_ERR_ARG;
+    const int k = (int)s->pass_ms.size();
+    if (n) *n = k;
+    if (ms)
+        for (int i = 0; i < std::min(cap, k); i++) ms[i] = s->pass_ms[i];
+    return RCS_OK;
+}
+
+rcs_status rcs_state_norm(const rcs_state* s, double* norm) {
+    if (!s || !norm) return RCS_ERR_ARG;
+    *norm = s->T_total;
+    return RCS_OK;
+}
+
+rcs_status rcs_state_copy_out(const rcs_state* s, uint64_t first, uint64_t count, void* dst, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!s || (!dst && count)) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    const uint64_t base = (uint64_t)s->ctx->rank << s->nl;
+    if (first < base || first + count > base + s->n_amps || first + count < first) {
+        set_error(err, RCS_ERR_ARG, "range [%llu, +%llu) not on this rank", (unsigned long long)first,
+                  (unsigned long long)count);
+        return RCS_ERR_ARG;
+    }
+    CUDA_TRY(cudaSetDevice(s->ctx->device));
+    CUDA_TRY(cudaMemcpyAsync(dst, s->amps + (first - base), count * sizeof(float2), cudaMemcpyDefault, s->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->ctx->stream));
+    return RCS_OK;
+}
+
+rcs_status rcs_probabilities(const rcs_state* s_, const uint64_t* x, uint64_t count, double* p_out, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    rcs_state* s = const_cast<rcs_state*>(s_);
+    if (!s || ((!x || !p_out) && count)) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    rcs_context* c = s->ctx;
+    CUDA_TRY(cudaSetDevice(c->device));
+    rcs_status st = ensure_buffers(s, err);
+    if (st) return st;
+    const bool xd = count ? is_device_ptr(x) : true, pd = count ? is_device_ptr(p_out) : true;
+    CUDA_TRY(cudaMemsetAsync(s->bad, 0, sizeof(int), c->stream));
+    for (uint64_t i0 = 0; i0 < count; i0 += s->chunk) {
+        const uint64_t cnt = std::min(s->chunk, count - i0);
+        const unsigned long long* xi = reinterpret_cast<const unsigned long long*>(x) + i0;
+        if (!xd) {
+            CUDA_TRY(cudaMemcpyAsync(s->xbuf, x + i0, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+            xi = s->xbuf;
+        }
+        double* po = pd ? p_out + i0 : s->dbuf;
+        CUDA_TRY(dev::gather_prob(s->amps, xi, cnt, s->nl, (uint64_t)c->rank, s->n, po, s->bad, c->stream));
+        if (c->world > 1) NCCL_TRY(ncclAllReduce(po, po, cnt, ncclDouble, ncclSum, c->comm, c->stream));
+        if (!pd) CUDA_TRY(cudaMemcpyAsync(p_out + i0, po, cnt * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    int bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, s->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (bad) { set_error(err, RCS_ERR_SIZE, "bitstring >= 2^%d", s->n); return RCS_ERR_SIZE; }
+    return RCS_OK;
+}
+
+rcs_status rcs_sample(rcs_state* s, uint64_t shots, uint64_t seed, uint64_t offset, uint64_t* out_x,
+                      rcs_sample_report* rep, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    return sample_impl(s, shots, seed, offset, nullptr, out_x, rep, err);
+}
+
+rcs_status rcs_sample_uniforms(rcs_state* s, const double* u, uint64_t shots, uint64_t* out_x, rcs_sample_report* rep,
+                               rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!u && shots) { set_error(err, RCS_ERR_ARG, "null uniforms"); return RCS_ERR_ARG; }
+    return sample_impl(s, shots, 0, 0, u, out_x, rep, err);
+}
+
+rcs_status rcs_xeb(const rcs_state* s_, const uint64_t* x, uint64_t count, rcs_xeb_report* out, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    rcs_state* s = const_cast<rcs_state*>(s_);
+    if (!s || !out || (!x && count)) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    if (count == 0) { set_error(err, RCS_ERR_ARG, "XEB needs at least one bitstring"); return RCS_ERR_ARG; }
+    rcs_context* c = s->ctx;
+    CUDA_TRY(cudaSetDevice(c->device));
+    rcs_status st = ensure_buffers(s, err);
+    if (st) return st;
+    const bool xd = is_device_ptr(x);
+    const int grid = dev::xeb_grid();
+    double* acc = s->xeb_part + 3 * grid;   // 3 running totals (fixed chunk order)
+    std::vector<double> tot(3, 0.0);
+    CUDA_TRY(cudaMemsetAsync(s->bad, 0, sizeof(int), c->stream));
+    for (uint64_t i0 = 0; i0 < count; i0 += s->chunk) {
+        const uint64_t cnt = std::min(s->chunk, count - i0);
+        const unsigned long long* xi = reinterpret_cast<const unsigned long long*>(x) + i0;
+        if (!xd) {
+            CUDA_TRY(cudaMemcpyAsync(s->xbuf, x + i0, cnt * 8, cudaMemcpyHostToDevice, c->stream));
+            xi = s->xbuf;
+        }
+        CUDA_TRY(dev::xeb_partials(s->amps, xi, cnt, s->nl, (uint64_t)c->rank, s->n, s->xeb_part, s->bad, c->stream));
+        CUDA_TRY(dev::xeb_finalize(s->xeb_part, grid, acc, c->stream));
+        if (c->world > 1) NCCL_TRY(ncclAllReduce(acc, acc, 3, ncclDouble, ncclSum, c->comm, c->stream));
+        double part[3];
+        CUDA_TRY(cudaMemcpyAsync(part, acc, sizeof part, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        for (int q = 0; q < 3; q++) tot[q] += part[q];
+    }
+    int bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, s->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (bad) { set_error(err, RCS_ERR_SIZE, "bitstring >= 2^%d", s->n); return RCS_ERR_SIZE; }
+    const double S = (double)count;
+    const double mean = tot[0] / S;
+    double var = count > 1 ? (tot[1] - S * mean * mean) / (S - 1.0) : 0.0;
+    if (var < 0) var = 0;
+    out->n_qubits = s->n;
+    out->shots = count;
+    out->mean_p = mean;
+    out->F = std::ldexp(mean, s->n) - 1.0;
+    out->sigma = std::ldexp(std::sqrt(var), s->n) / std::sqrt(S);
+    out->fstar = std::ldexp(s->sum_sq, s->n) - 1.0;
+    return RCS_OK;
+}
+
+void rcs_state_free(rcs_state* s) {
+    if (!s) return;
+    if (s->ctx) cudaSetDevice(s->ctx->device);
+    if (s->xbuf) cudaFree(s->xbuf);
+    if (s->dbuf) cudaFree(s->dbuf);
+    if (s->xeb_part) cudaFree(s->xeb_part);
+    if (s->bad) cudaFree(s->bad);
+    delete s;
+}
+
+}  // extern "C"

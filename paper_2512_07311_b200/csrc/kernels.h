@@ -1,0 +1,74 @@
+// kernels.h -- launchers for the sm_100a kernels of kernels.cu (all stream-ordered).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rcs {
+namespace dev {
+
+// launches issued by this library (every launcher below increments it)
+uint64_t launches();
+
+// a6 (K1) fused dense gate pass: amps <- M (x) over every group of 2^k amplitudes that
+// differ only in the physical bits pos[0..k) (matrix bit i <-> pos[i]); M is 2^k x 2^k
+// complex64 row-major (interleaved float pairs).  n_local_bits = log2(#amps).
+cudaError_t gate_pass(float2* amps, int n_local_bits, int k, const int* pos, const float* m_interleaved,
+                      cudaStream_t st);
+
+// in-place involution: swap physical bits a[i] <-> b[i] (disjoint pairs) over 2^nbits amps
+cudaError_t bit_swap(float2* amps, int nbits, int npairs, const int* a, const int* b, cudaStream_t st);
+
+// remap staging: buf[t] = amps[l(m0 + t)] (pack) or amps[l(m0 + t)] = buf[t] (unpack), where
+// l(m) inserts the j code bits `codemask` at the (ascending) local positions lpos[0..j)
+cudaError_t pack(const float2* amps, float2* buf, int j, const int* lpos_sorted, uint64_t codemask,
+                 uint64_t m0, uint64_t count, cudaStream_t st);
+cudaError_t unpack(float2* amps, const float2* buf, int j, const int* lpos_sorted, uint64_t codemask,
+                   uint64_t m0, uint64_t count, cudaStream_t st);
+
+// a9 (K5): bsum[blk] = sum_{x in blk} |a_x|^2 (fp64) for blocks of 2^b amps; part[c] = per-CTA
+// partial sum of p^2 (fixed grid => deterministic).  Returns the number of partials used.
+int block_sums_grid();
+cudaError_t block_sums(const float2* amps, uint64_t nblocks, int b, double* bsum, double* part_sq,
+                       cudaStream_t st);
+
+// a10 (K6): in-place inclusive scan of d[0..n) in fp64, deterministic; tmp must hold
+// scan_tmp_doubles(n) doubles.
+uint64_t scan_tmp_doubles(uint64_t n);
+cudaError_t scan_inclusive(double* d, uint64_t n, double* tmp, cudaStream_t st);
+
+// fixed-order reduction of n doubles -> out[0] (single CTA)
+cudaError_t reduce_sum(const double* in, int n, double* out, cudaStream_t st);
+
+struct SampleArgs {
+    const float2* amps;
+    const double* inc;      // inclusive block prefix of this rank's shard
+    uint64_t nblocks;
+    int b;
+    double T_total, E_r, T_r;
+    int owns_tail;          // 1: this rank owns every t >= E_r (last rank with T_r > 0)
+    int owns_any;           // 0: owns nothing (T_r == 0)
+    uint64_t seed, shot0, shots;
+    const double* u_in;     // optional caller uniforms (chunk-local), else SplitMix64
+    uint64_t base_index;    // rank * 2^n_local
+    unsigned long long* x_out;  // chunk-local, 0 for shots owned by other ranks
+};
+// a11 (K7): per-shot binary search over block prefixes + warp-cooperative in-block scan
+cudaError_t sample(const SampleArgs& a, cudaStream_t st);
+
+// a13 (K8): per-CTA partial (sum p, sum p^2, count) over owned bitstrings; bad_flag set if
+// any x >= 2^n.  Returns grid size used.
+int xeb_grid();
+cudaError_t xeb_partials(const float2* amps, const unsigned long long* x, uint64_t count, int n_local_bits,
+                         uint64_t rank, int n_bits, double* part /* 3*grid */, int* bad_flag, cudaStream_t st);
+cudaError_t xeb_finalize(const double* part, int grid, double* out3, cudaStream_t st);
+
+// p_out[i] = |a_{x_i}|^2 if x_i is on this rank else 0
+cudaError_t gather_prob(const float2* amps, const unsigned long long* x, uint64_t count, int n_local_bits,
+                        uint64_t rank, int n_bits, double* p_out, int* bad_flag, cudaStream_t st);
+
+cudaError_t init_basis(float2* amps, uint64_t n_amps, int set_one, cudaStream_t st);
+
+}  // namespace dev
+}  // namespace rcs

@@ -1,0 +1,367 @@
+// plan.cpp -- host planner: k-qubit gate fusion + global-qubit remap schedule.
+//
+// BASELINE.json north_star: "gates are fused into k-qubit dense blocks and applied in
+// place ... The state vector shards ... on its top log2(P) 'global' qubits.  Gates touching
+// global qubits trigger a qubit-remap all-to-all".  The paper itself publishes no algorithm
+// (SURVEY §0), so the fuser and planner below are this library's design.
+//
+// 1. Fusion (independent of P, so P = 1/2/4/8 states are bit-identical):
+//    closure-greedy.  A block starts from the earliest unassigned gate; its qubit set S is
+//    grown one extension at a time (the qubits of a gate at the block's frontier) choosing
+//    the extension whose closure -- every gate that becomes applicable inside S, repeatedly
+//    -- absorbs the most gates, until |S| = k or nothing grows.  Gates inside a block are
+//    applied in absorption order, which respects every per-qubit dependency.  The block
+//    matrix is the fp64 product of its gates (cast to complex64 on upload).
+// 2. Remaps (P > 1): logical->physical layout; when a block needs qubits living on global
+//    positions, each is swapped with a local qubit chosen by Belady (farthest next use).
+//    Physical positions < kPinnedLow never move.
+// 3. Final restore: <= 3 remaps bring the top-g qubits home, then <= 2 involutive bit-swap
+//    passes (a cycle is the product of two reflections) restore canonical local order.
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "internal.h"
+
+namespace rcs {
+
+namespace {
+
+struct Fuser {
+    const Circuit& C;
+    int k;
+    std::vector<std::vector<int>> per_q;   // gate ids per qubit, source order
+    std::vector<int> head;                 // first unassigned position in per_q[q]
+    std::vector<char> assigned;
+
+    Fuser(const Circuit& c, int k_) : C(c), k(k_) {
+        per_q.assign(c.n, {});
+        for (int i = 0; i < (int)c.gates.size(); i++) {
+            per_q[c.gates[i].q0].push_back(i);
+            if (c.gates[i].q1 >= 0) per_q[c.gates[i].q1].push_back(i);
+        }
+        head.assign(c.n, 0);
+        assigned.assign(c.gates.size(), 0);
+    }
+
+    int nq(int g) const { return C.gates[g].q1 >= 0 ? 2 : 1; }
+    int qb(int g, int j) const { return j == 0 ? C.gates[g].q0 : C.gates[g].q1; }
+
+    // gates absorbed by qubit set S (sorted) starting from the current heads
+    std::vector<int> closure(const std::vector<int>& S) const {
+        std::map<int, int> h;
+        for (int q : S) h[q] = head[q];
+        std::vector<int> got;
+        bool progress = true;
+        while (progress) {
+            progress = false;
+            for (int q : S) {
+                int pos = h[q];
+                if (pos >= (int)per_q[q].size()) continue;
+                int g = per_q[q][pos];
+                bool ok = true;
+                for (int j = 0; j < nq(g); j++) {
+                    auto it = h.find(qb(g, j));
+                    if (it == h.end() || it->second >= (int)per_q[qb(g, j)].size() ||
+                        per_q[qb(g, j)][it->second] != g) {
+                        ok = false;
+                        break;
+                    }
+                }
+                if (!ok) continue;
+                for (int j = 0; j < nq(g); j++) h[qb(g, j)]++;
+                got.push_back(g);
+                progress = true;
+            }
+        }
+        return got;
+    }
+
+    static std::vector<int> merged(const std::vector<int>& S, const std::vector<int>& ext) {
+        std::vector<int> r = S;
+        for (int q : ext)
+            if (!std::count(r.begin(), r.end(), q)) r.push_back(q);
+        std::sort(r.begin(), r.end());
+        return r;
+    }
+
+    bool next_block(Block& B) {
+        int g0 = -1;
+        for (int i = 0; i < (int)assigned.size(); i++)
+            if (!assigned[i]) { g0 = i; break; }
+        if (g0 < 0) return false;
+        std::vector<int> S;
+        for (int j = 0; j < nq(g0); j++) S.push_back(qb(g0, j));
+        std::sort(S.begin(), S.end());
+        std::vector<int> cur = closure(S);
+        while ((int)S.size() < k) {
+            // candidate extensions: qubits of gates at the heads reachable after the closure
+            std::map<int, int> h;
+            for (int q : S) h[q] = head[q];
+            for (int g : cur)
+                for (int j = 0; j < nq(g); j++) h[qb(g, j)]++;
+            std::set<std::vector<int>> cands;
+            for (int q : S) {
+                if (h[q] >= (int)per_q[q].size()) continue;
+                int g = per_q[q][h[q]];
+                std::vector<int> ext;
+                for (int j = 0; j < nq(g); j++)
+                    if (!std::count(S.begin(), S.end(), qb(g, j))) ext.push_back(qb(g, j));
+                if (!ext.empty() && (int)(S.size() + ext.size()) <= k) cands.insert(ext);
+            }
+            // gates that are ready elsewhere (disjoint from S)
+            for (int q = 0; q < C.n; q++) {
+                if (std::count(S.begin(), S.end(), q) || head[q] >= (int)per_q[q].size()) continue;
+                int g = per_q[q][head[q]];
+                bool ready = true;
+                std::vector<int> ext;
+                for (int j = 0; j < nq(g); j++) {
+                    int qq = qb(g, j);
+                    if (per_q[qq][head[qq]] != g) ready = false;
+                    if (!std::count(S.begin(), S.end(), qq)) ext.push_back(qq);
+                }
+                if (ready && (int)(S.size() + ext.size()) <= k) {
+                    std::sort(ext.begin(), ext.end());
+                    cands.insert(ext);
+                }
+            }
+            int best_score = (int)cur.size();
+            std::vector<int> best_ext, best_cl;
+            for (const auto& ext : cands) {
+                std::vector<int> cl = closure(merged(S, ext));
+                // weight 2q gates double: they are what forces extra passes
+                int score = 0;
+                for (int g : cl) score += nq(g);
+                int base = 0;
+                for (int g : cur) base += nq(g);
+                int gain = score - base;
+                int bgain = 0;
+                if (!best_cl.empty()) {
+                    for (int g : best_cl) bgain += nq(g);
+                    bgain -= base;
+                }
+                if (gain <= 0) continue;
+                // prefer larger gain per added qubit, then fewer qubits
+                if (best_cl.empty() || gain * (int)best_ext.size() > bgain * (int)ext.size() ||
+                    (gain * (int)best_ext.size() == bgain * (int)ext.size() && ext.size() < best_ext.size())) {
+                    best_ext = ext;
+                    best_cl = cl;
+                }
+            }
+            (void)best_score;
+            if (best_cl.empty()) break;
+            S = merged(S, best_ext);
+            cur = best_cl;
+        }
+        // commit
+        B.qubits = S;
+        B.gate_ids = cur;
+        for (int g : cur) {
+            assigned[g] = 1;
+            for (int j = 0; j < nq(g); j++) head[qb(g, j)]++;
+        }
+        return true;
+    }
+};
+
+// U <- G_embedded U  for every column, G acting on block-local bits lb0 (, lb1)
+void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb1) {
+    const int D = 1 << kb;
+    cplx m[16];
+    gate_matrix(g, m);
+    if (g.q1 < 0) {
+        for (int col = 0; col < D; col++)
+            for (int i = 0; i < D; i++) {
+                if (i & (1 << lb0)) continue;
+                const int i1 = i | (1 << lb0);
+                cplx a = U[(size_t)i * D + col], b = U[(size_t)i1 * D + col];
+                U[(size_t)i * D + col] = {m[0].re * a.re - m[0].im * a.im + m[1].re * b.re - m[1].im * b.im,
+                                          m[0].re * a.im + m[0].im * a.re + m[1].re * b.im + m[1].im * b.re};
+                U[(size_t)i1 * D + col] = {m[2].re * a.re - m[2].im * a.im + m[3].re * b.re - m[3].im * b.im,
+                                           m[2].re * a.im + m[2].im * a.re + m[3].re * b.im + m[3].im * b.re};
+            }
+        return;
+    }
+    for (int col = 0; col < D; col++)
+        for (int i = 0; i < D; i++) {
+            if (i & ((1 << lb0) | (1 << lb1))) continue;
+            int idx[4] = {i, i | (1 << lb0), i | (1 << lb1), i | (1 << lb0) | (1 << lb1)};
+            cplx v[4], o[4];
+            for (int t = 0; t < 4; t++) v[t] = U[(size_t)idx[t] * D + col];
+            for (int r = 0; r < 4; r++) {
+                double re = 0, im = 0;
+                for (int c = 0; c < 4; c++) {
+                    re += m[4 * r + c].re * v[c].re - m[4 * r + c].im * v[c].im;
+                    im += m[4 * r + c].re * v[c].im + m[4 * r + c].im * v[c].re;
+                }
+                o[r] = {re, im};
+            }
+            for (int t = 0; t < 4; t++) U[(size_t)idx[t] * D + col] = o[t];
+        }
+}
+
+}  // namespace
+
+rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err) {
+    if (fuse_k <= 0) fuse_k = 4;
+    if (fuse_k > 5) {
+        set_error(err, RCS_ERR_ARG, "fuse_k must be in [1, 5] (got %d)", fuse_k);
+        return RCS_ERR_ARG;
+    }
+    const int n = c.n;
+    if (n_global < 0 || n_global >= n) {
+        set_error(err, RCS_ERR_ARG, "n_global=%d invalid for n=%d", n_global, n);
+        return RCS_ERR_ARG;
+    }
+    const int n_local = n - n_global;
+    int k = std::min(fuse_k, n_local);
+    if (n_global > 0 && n_local - kPinnedLow < k) {
+        set_error(err, RCS_ERR_ARG, "too many global qubits: n=%d g=%d leaves %d movable local qubits < k=%d",
+                  n, n_global, n_local - kPinnedLow, k);
+        return RCS_ERR_ARG;
+    }
+    Plan P;
+    P.n = n;
+    P.n_global = n_global;
+    P.fuse_k = k;
+
+    // ---- 1. fusion
+    Fuser F(c, k);
+    Block B;
+    while (F.next_block(B)) {
+        const int kb = (int)B.qubits.size();
+        const int D = 1 << kb;
+        B.matrix.assign((size_t)D * D, {0.0, 0.0});
+        for (int i = 0; i < D; i++) B.matrix[(size_t)i * D + i] = {1.0, 0.0};
+        for (int gid : B.gate_ids) {
+            const Gate& g = c.gates[gid];
+            int lb0 = (int)(std::find(B.qubits.begin(), B.qubits.end(), g.q0) - B.qubits.begin());
+            int lb1 = g.q1 >= 0 ? (int)(std::find(B.qubits.begin(), B.qubits.end(), g.q1) - B.qubits.begin()) : -1;
+            apply_to_block(B.matrix, kb, g, lb0, lb1);
+        }
+        P.blocks.push_back(B);
+        B = Block();
+    }
+
+    // ---- 2. layout + remaps
+    std::vector<int> pos(n), occ(n);
+    for (int q = 0; q < n; q++) pos[q] = occ[q] = q;
+    // next use: per qubit, ascending block indices
+    std::vector<std::vector<int>> uses(n);
+    for (int bi = 0; bi < (int)P.blocks.size(); bi++)
+        for (int q : P.blocks[bi].qubits) uses[q].push_back(bi);
+    auto next_use = [&](int q, int from) {
+        auto it = std::lower_bound(uses[q].begin(), uses[q].end(), from);
+        return it == uses[q].end() ? INT_MAX : *it;
+    };
+    auto emit_remap = [&](const std::vector<std::pair<int, int>>& pairs) {
+        Item it;
+        it.type = RCS_ITEM_REMAP;
+        it.k = (int)pairs.size();
+        for (int i = 0; i < it.k; i++) {
+            it.a[i] = pairs[i].first;
+            it.b[i] = pairs[i].second;
+            int qa = occ[pairs[i].first], qb = occ[pairs[i].second];
+            std::swap(occ[pairs[i].first], occ[pairs[i].second]);
+            pos[qa] = pairs[i].second;
+            pos[qb] = pairs[i].first;
+        }
+        P.items.push_back(it);
+        P.n_remaps++;
+    };
+    for (int bi = 0; bi < (int)P.blocks.size(); bi++) {
+        const Block& blk = P.blocks[bi];
+        std::vector<int> need;
+        for (int q : blk.qubits)
+            if (pos[q] >= n_local) need.push_back(q);
+        if (!need.empty()) {
+            std::vector<int> cand;
+            for (int p = kPinnedLow; p < n_local; p++) {
+                int q = occ[p];
+                if (!std::count(blk.qubits.begin(), blk.qubits.end(), q)) cand.push_back(q);
+            }
+            std::stable_sort(cand.begin(), cand.end(), [&](int a, int b2) {
+                int na = next_use(a, bi), nb = next_use(b2, bi);
+                if (na != nb) return na > nb;
+                return pos[a] > pos[b2];
+            });
+            std::vector<std::pair<int, int>> pairs;
+            for (size_t i = 0; i < need.size(); i++) pairs.push_back({pos[need[i]], pos[cand[i]]});
+            emit_remap(pairs);
+        }
+        Item it;
+        it.type = RCS_ITEM_PASS;
+        it.block = bi;
+        it.k = (int)blk.qubits.size();
+        for (int i = 0; i < it.k; i++) it.pos[i] = pos[blk.qubits[i]];
+        P.items.push_back(it);
+        P.n_passes++;
+    }
+
+    // ---- 3. final restore: globals home
+    for (int round = 0; round < 3 && n_global > 0; round++) {
+        std::vector<std::pair<int, int>> pairs;
+        for (int G = n_local; G < n; G++)
+            if (occ[G] != G && pos[G] < n_local) pairs.push_back({G, pos[G]});
+        if (!pairs.empty()) emit_remap(pairs);
+        std::vector<int> wrong;
+        for (int G = n_local; G < n; G++)
+            if (occ[G] != G) wrong.push_back(G);
+        if (wrong.empty()) break;
+        // canonical qubits sitting on the wrong global position: park them locally first
+        pairs.clear();
+        int L = kPinnedLow;
+        for (int G : wrong) {
+            while (L < n_local && occ[L] >= n_local) L++;
+            pairs.push_back({G, L++});
+        }
+        emit_remap(pairs);
+    }
+    // local permutation -> two involutions (reflections of every cycle)
+    {
+        std::vector<char> seen(n_local, 0);
+        std::vector<std::pair<int, int>> r1, r2;
+        for (int p0 = 0; p0 < n_local; p0++) {
+            if (seen[p0] || occ[p0] == p0) { seen[p0] = 1; continue; }
+            std::vector<int> cyc;   // data at cyc[i] must move to cyc[i+1]
+            int p = p0;
+            while (!seen[p]) { seen[p] = 1; cyc.push_back(p); p = occ[p]; }
+            const int m = (int)cyc.size();
+            for (int i = 0; i < m; i++) {
+                int j1 = ((-i) % m + m) % m;
+                if (i < j1) r1.push_back({cyc[i], cyc[j1]});
+                int j2 = ((1 - i) % m + m) % m;
+                if (i < j2) r2.push_back({cyc[i], cyc[j2]});
+            }
+        }
+        for (auto* rr : {&r1, &r2}) {
+            if (rr->empty()) continue;
+            for (size_t off = 0; off < rr->size(); off += 8) {
+                Item it;
+                it.type = RCS_ITEM_SWAP;
+                it.k = (int)std::min<size_t>(8, rr->size() - off);
+                for (int i = 0; i < it.k; i++) {
+                    auto pr = (*rr)[off + i];
+                    it.a[i] = pr.first;
+                    it.b[i] = pr.second;
+                    std::swap(occ[pr.first], occ[pr.second]);
+                }
+                P.items.push_back(it);
+                P.n_swaps++;
+            }
+        }
+    }
+    for (int p = 0; p < n; p++) {
+        if (occ[p] != p) {
+            set_error(err, RCS_ERR_ARG, "internal planner error: layout not restored (pos %d holds %d)", p, occ[p]);
+            return RCS_ERR_ARG;
+        }
+    }
+    out = std::move(P);
+    return RCS_OK;
+}
+
+}  // namespace rcs

@@ -1,0 +1,217 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star):
+  amplitudes  max |d psi| <= 1e-5 and ||d psi||_2 <= 1e-5 (reading G16), norm within 1e-5
+  bitstrings  identical except where the uniform lies within 1e-6 of the CDF boundary that
+              separates the two picks (reading G17)
+  XEB         same-sample |F(x; p_gpu) - F(x; p_oracle)| <= 1e-3 (reading G18)
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from rcs_workload import SHOT_SEED, config_qasm, emit_qasm, generate, random_qasm
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rcs(cuda_ok):
+    from paper_2512_07311_b200 import build
+    build.build()
+    import paper_2512_07311_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(rcs):
+    return rcs.Context(0)
+
+
+def gpu_state(rcs, ctx, text, **kw):
+    c = rcs.Circuit.from_qasm(text)
+    st = rcs.State.build(ctx, c, **kw)
+    return st, st.copy_out().astype(np.complex128)
+
+
+def check_amps(psi, ref):
+    d = psi - ref
+    assert np.abs(d).max() <= 1e-5
+    assert np.linalg.norm(d) <= 1e-5
+    assert abs(np.vdot(psi, psi).real - 1) <= 1e-5
+
+
+def excused(x_g, x_o, u, p_o):
+    """G17: a GPU pick differing from the oracle's is excused iff the oracle CDF interval
+    of the GPU pick, widened by 1e-6, contains t = u T_o."""
+    C = np.cumsum(p_o)
+    T = C[-1]
+    t = u * T
+    diff = np.nonzero(x_g != x_o)[0]
+    xg = x_g[diff].astype(np.int64)
+    lo = np.where(xg > 0, C[np.maximum(xg - 1, 0)], 0.0) - 1e-6
+    hi = C[xg] + 1e-6
+    ok = (t[diff] >= lo) & (t[diff] <= hi)
+    return len(diff), int((~ok).sum())
+
+
+# ------------------------------------------------------------------ state parity
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("seed", range(6))
+def test_random_circuits_all_k(rcs, ctx, k, seed):
+    n = [1, 2, 5, 7, 10, 13][seed]
+    text = random_qasm(n, 12 * n + 5, 77 + seed)
+    ref = oracle.build_state(text)
+    st, psi = gpu_state(rcs, ctx, text, fuse_k=k)
+    check_amps(psi, ref)
+    assert abs(st.norm - 1) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_baseline_configs_state(rcs, ctx, cfg):
+    text = config_qasm(cfg)
+    ref = oracle.build_state(text)
+    st, psi = gpu_state(rcs, ctx, text, fuse_k=4, timing=True)
+    check_amps(psi, ref)
+    assert st.report["n_passes"] == len(st.pass_times())
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_virtual_global_bitwise_equals_single(rcs, ctx, g):
+    text = emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=g))
+    ref = oracle.build_state(text)
+    _, psi1 = gpu_state(rcs, ctx, text)
+    stg, psig = gpu_state(rcs, ctx, text, virtual_global=g)
+    assert stg.report["n_remaps"] > 0
+    assert np.array_equal(psi1, psig)            # P-invariance of the fused arithmetic
+    check_amps(psig, ref)
+
+
+def test_empty_and_tiny_circuits(rcs, ctx):
+    for n in (1, 2, 3, 7):
+        st, psi = gpu_state(rcs, ctx, f"OPENQASM 2.0;\nqreg q[{n}];\n")
+        e = np.zeros(1 << n); e[0] = 1
+        assert np.array_equal(psi, e)
+        x = st.sample(1000)
+        assert (x == 0).all()
+    st, psi = gpu_state(rcs, ctx, "OPENQASM 2.0;\nqreg q[1];\nx_1_2 q[0];\n")
+    np.testing.assert_allclose(psi, [0.5 + 0.5j, 0.5 - 0.5j], atol=1e-7)
+
+
+def test_product_state_closed_form_n26(rcs, ctx):
+    circ = generate(2, 13, 8, "ABCD", seed=4, two_qubit=False)
+    c = oracle.parse(emit_qasm(circ))
+    v = [np.array([1, 0], complex) for _ in range(26)]
+    for g in c.gates:
+        v[g.qubits[0]] = oracle.gate_matrix(g.kind) @ v[g.qubits[0]]
+    st = rcs.State.build(ctx, rcs.Circuit.from_qasm(emit_qasm(circ)))
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, 1 << 26, 4096)
+    full = st.copy_out()
+    for x in idx[:4096]:
+        a = np.prod([v[q][(x >> q) & 1] for q in range(26)])
+        assert abs(full[x] - a) <= 1e-6
+
+
+# ------------------------------------------------------------------ sampling + XEB parity
+@pytest.mark.parametrize("cfg,shots", [("c1", 10_000), ("c2", 100_000)])
+def test_sampling_and_xeb_parity(rcs, ctx, cfg, shots):
+    text = config_qasm(cfg)
+    ref = oracle.build_state(text)
+    st, psi = gpu_state(rcs, ctx, text)
+    x_g = st.sample(shots, seed=SHOT_SEED)
+    u = oracle.uniforms(SHOT_SEED, shots)
+    x_o, T_o = oracle.sample(ref, u)
+    p_o = np.abs(ref) ** 2
+    nd, bad = excused(x_g, x_o, u, p_o)
+    assert bad == 0, f"{bad} unexcused of {nd} differing shots"
+    assert nd <= max(10, shots // 100)
+    # XEB: same-sample check and independent comparison
+    xr = st.xeb(x_g)
+    F_o_same, _, _ = oracle.xeb(ref, x_g)
+    assert abs(xr["F"] - F_o_same) <= 1e-3
+    F_o, sig_o, _ = oracle.xeb(ref, x_o)
+    assert abs(xr["F"] - F_o) <= 1e-3
+    assert abs(xr["fstar"] - oracle.fstar(ref)) <= 1e-4
+    assert abs(xr["F"] - xr["fstar"]) <= 5 * xr["sigma"]
+
+
+def test_sample_uniforms_hook_and_offsets(rcs, ctx):
+    text = config_qasm("c1")
+    ref = oracle.build_state(text)
+    st, _ = gpu_state(rcs, ctx, text, block_bits=3)
+    u = oracle.uniforms(9, 5000)
+    xa = st.sample_uniforms(u)
+    xb = st.sample(5000, seed=9)
+    assert np.array_equal(xa, xb)
+    xc = st.sample(1000, seed=9, offset=2000)
+    assert np.array_equal(xc, xb[2000:3000])
+    x_o, _ = oracle.sample(ref, u)
+    nd, bad = excused(xa, x_o, u, np.abs(ref) ** 2)
+    assert bad == 0
+    # device output
+    xd = st.sample(5000, seed=9, device=True)
+    assert np.array_equal(xd.cpu().numpy().view(np.uint64), xb)
+
+
+def test_probabilities_and_errors(rcs, ctx):
+    text = config_qasm("c1")
+    ref = oracle.build_state(text)
+    st, _ = gpu_state(rcs, ctx, text)
+    x = np.arange(0, 4096, 7, dtype=np.uint64)
+    p = st.probabilities(x)
+    np.testing.assert_allclose(p, np.abs(ref[x.astype(np.int64)]) ** 2, atol=1e-9)
+    with pytest.raises(rcs.RcsError) as e:
+        st.probabilities(np.array([4096], np.uint64))
+    assert e.value.status == "RCS_ERR_SIZE"
+    with pytest.raises(rcs.RcsError) as e:
+        st.xeb(np.array([1, 1 << 12], np.uint64))
+    assert e.value.status == "RCS_ERR_SIZE"
+
+
+def test_memory_errors(rcs, ctx):
+    import torch
+    c = rcs.Circuit.from_qasm(config_qasm("c1"))
+    small = torch.empty(100, dtype=torch.complex64, device="cuda")
+    with pytest.raises(rcs.RcsError) as e:
+        rcs.State.build(ctx, c, amps=small)
+    assert e.value.status == "RCS_ERR_MEMORY" and e.value.bytes_required == 8 * 4096
+
+
+def test_uniform_and_ideal_xeb_calibration(rcs, ctx):
+    text = config_qasm("c2", n_qubits=20, rows=4, cols=5)
+    st, _ = gpu_state(rcs, ctx, text)
+    S = 200_000
+    u = oracle.uniforms(5, S)
+    xu = np.floor(u * (1 << 20)).astype(np.uint64)
+    r = st.xeb(xu)
+    assert abs(r["F"]) <= 5 * r["sigma"]
+    r = st.xeb(st.sample(S, seed=6))
+    assert abs(r["F"] - r["fstar"]) <= 5 * r["sigma"]
+
+
+# ------------------------------------------------------------------ full size (BASELINE C3, bench launch config)
+def test_full_size_c3_properties(rcs, ctx):
+    """n = 32 (C3): oracle state is 64 GiB fp64, so parity at this size is checked by
+    properties: norm, F* ~ 1 (Porter-Thomas), samples' XEB within 5 sigma of F*, and the
+    circuit followed by its inverse returning e_0."""
+    text = config_qasm("c3")
+    c = rcs.Circuit.from_qasm(text)
+    st = rcs.State.build(ctx, c, fuse_k=4)
+    assert abs(st.norm - 1) <= 1e-5
+    x = st.sample(1_000_000, seed=SHOT_SEED)
+    r = st.xeb(x)
+    assert abs(r["fstar"] - 1) < 0.05
+    assert abs(r["F"] - r["fstar"]) <= 5 * r["sigma"]
+    del st
+    import torch
+    torch.cuda.empty_cache()
+    from tests.test_oracle_pins import inverse_qasm
+    both = text + inverse_qasm(oracle.parse(text))
+    st2 = rcs.State.build(ctx, rcs.Circuit.from_qasm(both), fuse_k=4)
+    head = st2.copy_out(0, 1024)
+    assert abs(abs(head[0]) - 1) <= 1e-4
+    p = st2.probabilities(np.array([0, 1, 12345, (1 << 32) - 1], np.uint64))
+    assert abs(p[0] - 1) < 2e-4 and p[1:].max() < 1e-8

@@ -1,0 +1,151 @@
+"""Host-side (no GPU) tests of the C-ABI library: symbol exports, the library's own QASM
+parser against the oracle's, and the fused plan / remap planner via a NumPy executor."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from rcs_workload import config_qasm, emit_qasm, generate, random_qasm
+from tests.plan_exec import run_plan
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def rcs():
+    from paper_2512_07311_b200 import build
+    build.build()
+    import paper_2512_07311_b200 as m
+    return m
+
+
+def test_library_exports_every_header_symbol(rcs):
+    hdr = open(os.path.join(ROOT, "include", "rcs.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    names = set(re.findall(r"\b(rcs_[a-z_0-9]+)\s*\(", hdr))
+    assert len(names) >= 20
+    L = rcs.lib()
+    for nm in sorted(names):
+        assert hasattr(L, nm), nm
+    from paper_2512_07311_b200._lib import SIGNATURES
+    assert names == set(SIGNATURES), names ^ set(SIGNATURES)
+    assert L.rcs_status_string(6) == b"RCS_ERR_NORM"
+
+
+def _lib_gates(rcs, text):
+    return rcs.Circuit.from_qasm(text).gates()
+
+
+@pytest.mark.parametrize("src", ["c1", "c2", "c3", "c4", "c5", "rand0", "rand1", "rand2", "meas"])
+def test_parser_matches_oracle_parser(rcs, src):
+    if src.startswith("rand"):
+        text = random_qasm(7, 120, int(src[4:]))
+    elif src == "meas":
+        text = emit_qasm(generate(2, 3, 4, "ABCD", 9), measure=True)
+    else:
+        text = config_qasm(src)
+    o = oracle.parse(text)
+    c = rcs.Circuit.from_qasm(text)
+    st = c.stats()
+    assert st["n_qubits"] == o.n_qubits and st["n_moments"] == o.n_moments and st["n_measure"] == o.n_measure
+    lg = c.gates()
+    assert len(lg) == len(o.gates)
+    for (k, qs, th, ph, m), g in zip(lg, o.gates):
+        assert (k, qs, m) == (g.kind, g.qubits, g.moment)
+        assert th == g.theta and ph == g.phi          # bit-identical angle parsing
+
+
+@pytest.mark.parametrize("text", [
+    "OPENQASM 2.0;\nqreg q[2];\nfoo q[0];\n",
+    "OPENQASM 2.0;\nqreg q[2];\nsx q[2];\n",
+    "OPENQASM 2.0;\nqreg q[2];\nfsim(0.1) q[0],q[1];\n",
+    "OPENQASM 2.0;\nqreg q[2];\nsx q[0],q[1];\n",
+    "OPENQASM 2.0;\nqreg q[2];\nfsim(1,2) q[1],q[1];\n",
+    "OPENQASM 2.0;\nqreg q[2];\n  sx q[0]\n",
+    "OPENQASM 2.0;\nsx q[0];\n",
+    "OPENQASM 2.0;\nqreg q[3];\nrz(pi*) q[0];\n",
+])
+def test_parser_errors_match_oracle(rcs, text):
+    with pytest.raises(oracle.OracleError) as eo:
+        oracle.parse(text)
+    with pytest.raises(rcs.RcsError) as el:
+        rcs.Circuit.from_qasm(text)
+    assert el.value.status == "RCS_ERR_" + eo.value.name
+    assert (el.value.line, el.value.col) == (eo.value.line, eo.value.col)
+
+
+def test_block_matrices_unitary_and_cover_all_gates(rcs):
+    c = rcs.Circuit.from_qasm(config_qasm("c2"))
+    for k in (2, 3, 4, 5):
+        p = rcs.Plan(c, k, 0)
+        items = p.items()
+        tot = 0
+        for it in items:
+            assert it["type"] == "pass" and 1 <= it["k"] <= k
+            M = it["matrix"]
+            assert np.abs(M.conj().T @ M - np.eye(M.shape[0])).max() < 1e-12
+            assert it["qubits"] == sorted(it["qubits"]) and it["pos"] == it["qubits"]
+            tot += it["n_gates"]
+        assert tot == c.stats()["n_gates"]
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_plan_executor_matches_oracle_random(rcs, seed, k):
+    n = 4 + seed % 6
+    text = random_qasm(n, 60, 1000 + seed)
+    ref = oracle.build_state(text)
+    c = rcs.Circuit.from_qasm(text)
+    p = rcs.Plan(c, k, 0)
+    psi = run_plan(p.items(), n)
+    assert np.abs(psi - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+@pytest.mark.parametrize("grid", [(3, 4, 14, "EFGH"), (2, 5, 20, "ABCDCDAB"), (3, 3, 12, "ABCD")])
+def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
+    rows, cols, cyc, pat = grid
+    n = rows * cols
+    if n - g - 3 < 4:
+        pytest.skip("too few local qubits")
+    text = emit_qasm(generate(rows, cols, cyc, pat, seed=g))
+    ref = oracle.build_state(text)
+    c = rcs.Circuit.from_qasm(text)
+    p = rcs.Plan(c, 4, g)
+    items = p.items()
+    nl = n - g
+    for it in items:
+        if it["type"] == "pass":
+            assert max(it["pos"]) < nl                          # blocks only touch local bits
+        elif it["type"] == "remap":
+            assert all(a >= nl for a in it["a"]) and all(3 <= b < nl for b in it["b"])
+        else:
+            assert all(3 <= a < nl and 3 <= b < nl for a, b in zip(it["a"], it["b"]))
+    # the fusion is independent of the number of global qubits (P-invariance)
+    p0 = rcs.Plan(c, 4, 0)
+    b0 = [i for i in p0.items() if i["type"] == "pass"]
+    bg = [i for i in items if i["type"] == "pass"]
+    assert len(b0) == len(bg)
+    for x, y in zip(b0, bg):
+        assert x["qubits"] == y["qubits"] and np.array_equal(x["matrix"], y["matrix"])
+    psi = run_plan(items, n)
+    assert np.abs(psi - ref).max() < 1e-12
+
+
+def test_plan_rejects_bad_arguments(rcs):
+    c = rcs.Circuit.from_qasm(config_qasm("c1"))
+    with pytest.raises(rcs.RcsError):
+        rcs.Plan(c, 6, 0)
+    with pytest.raises(rcs.RcsError):
+        rcs.Plan(c, 4, 9)   # 12 - 9 - 3 < 4 movable local qubits
+
+
+def test_pass_counts_reported(rcs):
+    # fusion quality guard: k=4 passes for the BASELINE configs
+    want = {"c1": 22, "c2": 52, "c3": 68, "c4": 86, "c5": 93}
+    for cfg, cap in want.items():
+        p = rcs.Plan(rcs.Circuit.from_qasm(config_qasm(cfg)), 4, 0)
+        assert p.n_passes <= cap, (cfg, p.n_passes)
