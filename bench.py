@@ -39,9 +39,13 @@ METRIC = "fused gate-pass HBM GB/s (whole RCS step: state build + shots + XEB)"
 # Fused passes per config and fuse_k of the library's planner (P-independent).  The reference
 # arm converts oracle time into the same unit with this table instead of calling our engine;
 # tests/test_bench.py keeps it equal to rcs_plan_create's output.
-PLAN_PASSES = {'c1': {3: 32, 4: 20, 5: 15}, 'c2': {3: 102, 4: 50, 5: 40}, 'c3': {3: 101, 4: 65, 5: 47},
-               'c4': {3: 154, 4: 84, 5: 61}, 'c5': {3: 163, 4: 91, 5: 66}, 'w33': {3: 119, 4: 77, 5: 56},
-               'w35': {3: 161, 4: 86, 5: 60}}
+PLAN_PASSES = {'c1': {3: 32, 4: 20, 5: 15, 6: 11},
+               'c2': {3: 102, 4: 50, 5: 40, 6: 29},
+               'c3': {3: 101, 4: 65, 5: 47, 6: 37},
+               'c4': {3: 154, 4: 84, 5: 61, 6: 42},
+               'c5': {3: 163, 4: 91, 5: 66, 6: 47},
+               'w33': {3: 119, 4: 77, 5: 56, 6: 42},
+               'w35': {3: 161, 4: 86, 5: 60, 6: 49}}
 
 
 def parse_args():
@@ -51,7 +55,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--fuse-k", type=int, default=4)
+    ap.add_argument("--fuse-k", type=int, default=6)
     ap.add_argument("--shots", type=int, default=0, help="override the config's shot count")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="default: --steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")

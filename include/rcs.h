@@ -73,7 +73,8 @@ typedef struct {
 } rcs_circuit_counts;
 
 typedef struct {
-    int fuse_k;              /* max qubits per fused dense block, 1..5 (0 -> 4)                 */
+    int fuse_k;              /* max qubits per fused dense block, 1..6; 6-qubit blocks run on the
+                                tensor cores (needs n-g >= 12).  0 -> 6 if n-g >= 12, else 4        */
     int block_bits;          /* sampling block: 2^b amplitudes per fp64 CDF entry (0 -> 6)      */
     int virtual_global;      /* world == 1 only: treat the top g qubits as global and run every
                                 remap as an in-device bit swap (tests the sharded plan on 1 GPU) */
@@ -95,6 +96,7 @@ typedef struct {
     uint64_t pass_bytes;     /* algorithmic bytes of all gate passes on this rank (16 B/amp/pass) */
     uint64_t remap_bytes;    /* bytes this rank sent over NCCL                                   */
     double norm;             /* sum |psi|^2 over all ranks                                       */
+    int n_tc_passes;         /* of n_passes, 6-qubit passes run on the tensor cores (K9)          */
 } rcs_build_report;
 
 typedef struct {

@@ -98,7 +98,7 @@ class Plan:
         out = []
         it = rcs_plan_item()
         for i in range(self.n_items):
-            mat = np.zeros(2 * 4 ** 5, dtype=np.float64)
+            mat = np.zeros(2 * 4 ** 6, dtype=np.float64)
             check(lib().rcs_plan_item_get(self._h, i, C.byref(it), mat.ctypes.data_as(C.POINTER(C.c_double))),
                   None, "rcs_plan_item_get")
             d = {"type": ITEM_NAMES[it.type], "k": it.k}
@@ -167,7 +167,7 @@ class State:
         self._h = None
 
     @classmethod
-    def build(cls, ctx: Context, circuit: Circuit, fuse_k: int = 4, block_bits: int = 0, virtual_global: int = 0,
+    def build(cls, ctx: Context, circuit: Circuit, fuse_k: int = 0, block_bits: int = 0, virtual_global: int = 0,
               timing: bool = False, staging_bytes: int = 0, amps=None, scratch=None) -> "State":
         import torch
         n = circuit.n_qubits

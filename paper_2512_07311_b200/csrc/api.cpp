@@ -18,8 +18,13 @@ using namespace rcs;
 
 struct rcs_context {
     int device = 0, rank = 0, world = 1, g = 0;
+    int num_sms = 148;
     cudaStream_t stream = nullptr;
     ncclComm_t comm = nullptr;
+    // device plan buffer for the tensor-core passes' A matrices (+ pinned host staging)
+    uint32_t* d_tc = nullptr;
+    uint32_t* h_tc = nullptr;
+    size_t tc_cap = 0;   // words
 };
 
 struct rcs_state {
@@ -413,6 +418,7 @@ rcs_status rcs_context_create(int device, int rank, int world, const void* nccl_
     c->world = world;
     c->g = g;
     c->stream = reinterpret_cast<cudaStream_t>(stream);
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (world > 1) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof id);
@@ -429,6 +435,9 @@ rcs_status rcs_context_create(int device, int rank, int world, const void* nccl_
 
 void rcs_context_free(rcs_context* c) {
     if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->d_tc) cudaFree(c->d_tc);
+    if (c->h_tc) cudaFreeHost(c->h_tc);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -521,14 +530,44 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         ev.resize(2 * P.items.size());
         for (auto& e : ev) BUILD_TRY(cudaEventCreate(&e));
     }
+    // tensor-core passes: A_hi/A_lo of every 6-qubit block, one H2D copy per build
+    std::vector<int> tc_slot(P.items.size(), -1);
+    int n_tc = 0;
+    for (size_t ii = 0; ii < P.items.size(); ii++)
+        if (P.items[ii].type == RCS_ITEM_PASS && P.items[ii].k == 6) tc_slot[ii] = n_tc++;
+    const size_t tc_words_each = dev::tc_matrix_words();
+    const size_t tc_floats = (size_t)n_tc * tc_words_each;
+    if (n_tc > 0) {
+        if (ctx->tc_cap < tc_floats) {
+            if (ctx->d_tc) cudaFree(ctx->d_tc);
+            if (ctx->h_tc) cudaFreeHost(ctx->h_tc);
+            ctx->d_tc = nullptr;
+            ctx->h_tc = nullptr;
+            ctx->tc_cap = 0;
+            BUILD_TRY(cudaMalloc(&ctx->d_tc, tc_floats * sizeof(uint32_t)));
+            BUILD_TRY(cudaMallocHost(&ctx->h_tc, tc_floats * sizeof(uint32_t)));
+            ctx->tc_cap = tc_floats;
+        }
+        BUILD_TRY(cudaStreamSynchronize(stream));   // previous build may still read h_tc
+        for (size_t ii = 0; ii < P.items.size(); ii++)
+            if (tc_slot[ii] >= 0)
+                dev::tc_pack_matrix(reinterpret_cast<const double*>(P.blocks[P.items[ii].block].matrix.data()),
+                                    ctx->h_tc + (size_t)tc_slot[ii] * tc_words_each);
+    }
     BUILD_TRY(cudaEventRecord(eb0, stream));
+    if (n_tc > 0)
+        BUILD_TRY(cudaMemcpyAsync(ctx->d_tc, ctx->h_tc, tc_floats * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
     BUILD_TRY(dev::init_basis(s->amps, n_amps, ctx->rank == 0, stream));
     uint64_t pass_bytes = 0, remap_bytes = 0;
     std::vector<float> mbuf;
     for (size_t ii = 0; ii < P.items.size(); ii++) {
         const Item& it = P.items[ii];
         if (o.timing) BUILD_TRY(cudaEventRecord(ev[2 * ii], stream));
-        if (it.type == RCS_ITEM_PASS) {
+        if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
+            BUILD_TRY(dev::gate_pass_tc(s->amps, nl, it.pos, ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
+                                        ctx->num_sms, stream));
+            pass_bytes += 16ull * n_amps;
+        } else if (it.type == RCS_ITEM_PASS) {
             const Block& B = P.blocks[it.block];
             mbuf.resize(2 * B.matrix.size());
             for (size_t e = 0; e < B.matrix.size(); e++) {
@@ -592,6 +631,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     R.pass_bytes = pass_bytes;
     R.remap_bytes = remap_bytes;
     R.norm = s->T_total;
+    R.n_tc_passes = n_tc;
     if (rep) *rep = R;
     *out = s;
     return RCS_OK;

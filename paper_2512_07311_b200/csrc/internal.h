@@ -56,6 +56,8 @@ struct Plan {
 // low physical positions never moved by remaps (keeps qubit 0 at bit 0 for the
 // 128-bit pair loads of the gate-pass kernel and keeps short runs contiguous)
 constexpr int kPinnedLow = 3;
+// the tensor-core pass tiles 6 target + 6 column bits
+constexpr int kTcMinLocal = 12;
 
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err);
 

@@ -491,6 +491,7 @@ unsigned grid_for(uint64_t n, unsigned cap = 148u * 16u) {
 // launchers
 // ------------------------------------------------------------------------------------
 uint64_t launches() { return g_launches.load(); }
+void count_launch() { note_launch(); }
 
 cudaError_t gate_pass(float2* amps, int nb, int k, const int* pos, const float* m, cudaStream_t st) {
     switch (k) {

@@ -10,6 +10,15 @@ namespace dev {
 
 // launches issued by this library (every launcher below increments it)
 uint64_t launches();
+void count_launch();
+
+// K9: 6-qubit fused pass on tensor cores (tc_pass.cu).  d_a = tc_matrix_words() words made
+// by tc_pack_matrix from the fp64 64x64 block matrix (fp16 hi/lo split of the real 128x128
+// embedding, scaled by 2^14).
+size_t tc_matrix_words();
+void tc_pack_matrix(const double* u_re_im, uint32_t* out);
+cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const uint32_t* d_a, int num_sms,
+                         cudaStream_t st);
 
 // a6 (K1) fused dense gate pass: amps <- M (x) over every group of 2^k amplitudes that
 // differ only in the physical bits pos[0..k) (matrix bit i <-> pos[i]); M is 2^k x 2^k

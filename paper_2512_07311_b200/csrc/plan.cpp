@@ -206,9 +206,8 @@ void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb
 }  // namespace
 
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err) {
-    if (fuse_k <= 0) fuse_k = 4;
-    if (fuse_k > 5) {
-        set_error(err, RCS_ERR_ARG, "fuse_k must be in [1, 5] (got %d)", fuse_k);
+    if (fuse_k > 6) {
+        set_error(err, RCS_ERR_ARG, "fuse_k must be in [1, 6] (got %d)", fuse_k);
         return RCS_ERR_ARG;
     }
     const int n = c.n;
@@ -217,6 +216,10 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         return RCS_ERR_ARG;
     }
     const int n_local = n - n_global;
+    // default: 6-qubit blocks on the tensor cores when a 12-bit tile fits, else 4 on CUDA cores
+    if (fuse_k <= 0) fuse_k = n_local >= kTcMinLocal ? 6 : 4;
+    // 6-qubit blocks run only on the tensor-core pass, which needs n_local >= 12
+    if (fuse_k == 6 && n_local < kTcMinLocal) fuse_k = 5;
     int k = std::min(fuse_k, n_local);
     if (n_global > 0 && n_local - kPinnedLow < k) {
         set_error(err, RCS_ERR_ARG, "too many global qubits: n=%d g=%d leaves %d movable local qubits < k=%d",

@@ -1,0 +1,493 @@
+// tc_pass.cu -- K9: 6-qubit fused gate pass on the 5th-gen tensor cores (tcgen05, sm_100a).
+//
+// A 6-qubit dense block U (64x64 complex) applied to the state is a real GEMM
+//     [Y_re; Y_im] (128 x N) = [[U_re, -U_im], [U_im, U_re]] (128 x 128) . [X_re; X_im] (128 x N)
+// over the columns j = the non-target index (BASELINE.json north_star: "tensor cores only if
+// fused-gate width makes it a real dense contraction").  A's rows are interleaved (row 2t =
+// Y_re[t], row 2t+1 = Y_im[t]) so one TMEM lane pair holds re/im of one output amplitude.
+//
+// Precision: fp32-level results from fp16 tensor cores by a scaled two-term split
+//     x * 2^s = hi + lo  (hi = fp16(x 2^s), lo = fp16(x 2^s - hi); 22 significant bits)
+//     A B ~= 2^-(sA+sB) (A_hi B_hi + A_hi B_lo + A_lo B_hi)
+// with sA = 14 (|A| <= 1) and sB = 14 - e per tile, e = exponent of the tile's max |x|, so the
+// scaled tile max lies in [2^14, 2^15) (no fp16 overflow at any amplitude scale).  The fp32
+// accumulation in TMEM truncates, so the small cross terms are accumulated first into acc 0
+// and the main term is split over 3 accumulators by K-steps, summed round-to-nearest in the
+// epilogue (scripts/micro/tc_f16.cu: norm^2 drift -1.4e-7 per pass, rms error 1.2e-7).
+//
+// Tile = 64 columns x 64 target combinations = 4096 amplitudes (32 KB), a 12-bit sub-cube of
+// the index: the 6 target bits plus the 6 lowest non-target bits, so every tile is a set of
+// 2^(12-r) contiguous runs of 2^r >= 64 amplitudes.  Persistent kernel, one CTA per SM:
+//   warp  13   producer: cp.async.bulk (TMA) of the tile's runs into raw stage r (4 stages,
+//                         up to 128 KB in flight per SM, no registers) -> rfull[r] (complete_tx)
+//   warps 0-7  converters: raw smem -> tile max exponent (named barrier) -> hi/lo split ->
+//                         STS into B stage (K-major, interleaved core matrices) -> full[s]
+//   warp  12   MMA     : 8 K-steps x 3 terms = 24 tcgen05.mma kind::f16 (M=128, N=64, K=16,
+//                         A in TMEM) into D[d] -> commit empty[s], tfull[d]; tile exponent
+//                         forwarded to the epilogue through meta[d] / mfull[d]
+//   warps 8-11 epilogue: tcgen05.ld 3 accumulators of D[d] -> tempty[d] -> sum, unscale ->
+//                         STS staging [t][j] -> coalesced LDS/STG (each thread owns one
+//                         column, rows t0 + 2i: hoisted offsets, immediate staging offsets)
+// Shared memory: raw 4 x 32 KB + B 2 x 32 KB + staging 33 KB + control = 227 KB.
+// TMEM (512 cols): A_hi [0,64), A_lo [64,128) (fp16 pairs), D[d] = [128 + 192 d, +192) holding
+// 3 accumulators of 64 columns.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace rcs {
+namespace dev {
+namespace {
+
+constexpr int kLoadWarps = 8, kEpiWarp0 = 8, kMmaWarp = 12, kProdWarp = 13, kWarps = 14, kThreadsTC = kWarps * 32;
+constexpr int TN = 64;                       // columns per tile (MMA N)
+constexpr int TK = 128;                      // real K
+constexpr int kStages = 2;                   // B stages
+constexpr int kRaw = 4;                      // raw (TMA) stages
+constexpr uint32_t kRawBytes = 4096 * 8;
+constexpr uint32_t kBBytes = TN * TK * 2;    // 16 KB per fp16 hi or lo tile
+constexpr uint32_t kStageBytes = 2 * kBBytes;
+constexpr uint32_t kSBO = (TK / 8) * 128;    // next 8-row group (16 chunks of 16 B)
+constexpr int kPitchF = 130;                 // staging row pitch in floats (520 B): conflict-free
+constexpr uint32_t kStagingBytes = 64 * kPitchF * 4;
+constexpr uint32_t kCtlBytes = 2560;   // barriers + offset tables; total <= 227 KB
+// control block: 18 mbarriers + 3 x 64 offsets (8 B) + 24 ints + 2 x 64 uint16
+static_assert(18 * 8 + 3 * 64 * 8 + 24 * 4 + 2 * 64 * 2 <= 2048, "control block overflow");
+constexpr uint32_t kSmemBytes = kRaw * kRawBytes + kStages * kStageBytes + kStagingBytes + kCtlBytes;
+constexpr int kAccCols = 3 * TN;             // one D buffer
+
+struct TcArgs {
+    float2* amps;
+    const uint32_t* a;       // [2][128][64] packed fp16 pairs: A_hi then A_lo (row m, column c = k/2)
+    uint64_t ntiles;
+    int pos[6];              // physical position of matrix bit i
+    int jpos[6];             // the 6 lowest non-target positions (column bits, ascending)
+    int sub[12];             // all 12 sub-cube positions, ascending (for the tile base deposit)
+    int r;                   // sub[0..r) == 0..r-1: runs of 2^r contiguous amplitudes
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t ins0(uint64_t x, int s) {
+    return ((x >> s) << (s + 1)) | (x & ((1ull << s) - 1));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(su32(b)), "r"(parity), "r"(0x2000)   // suspend-time hint (ns): sleep, don't spin
+                     : "memory");
+    } while (!done);
+}
+
+__device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
+    // K-major, SWIZZLE_NONE: core matrix = 8 rows x 16 B; LBO (next K chunk) = 128 B,
+    // SBO (next 8-row group) = 2048 B; version 1 (sm100)
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)(128 >> 4) << 16;
+    d |= (uint64_t)(kSBO >> 4) << 32;
+    d |= 1ull << 46;
+    return d;
+}
+
+// byte offset of the 16-B chunk holding B elements (column n, k = 8c .. 8c+7)
+__device__ __forceinline__ uint32_t bchunk(int n, int c) {
+    return (uint32_t)((n >> 3) * kSBO + c * 128 + (n & 7) * 16);
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+    return (uint32_t)__half_as_ushort(__float2half_rn(a)) | ((uint32_t)__half_as_ushort(__float2half_rn(b)) << 16);
+}
+
+#define TMEM_ST32(addr, R)                                                                                       \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+                 "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),         \
+                 "r"(R[0]), "r"(R[1]), "r"(R[2]), "r"(R[3]), "r"(R[4]), "r"(R[5]), "r"(R[6]), "r"(R[7]),          \
+                 "r"(R[8]), "r"(R[9]), "r"(R[10]), "r"(R[11]), "r"(R[12]), "r"(R[13]), "r"(R[14]), "r"(R[15]),    \
+                 "r"(R[16]), "r"(R[17]), "r"(R[18]), "r"(R[19]), "r"(R[20]), "r"(R[21]), "r"(R[22]), "r"(R[23]),  \
+                 "r"(R[24]), "r"(R[25]), "r"(R[26]), "r"(R[27]), "r"(R[28]), "r"(R[29]), "r"(R[30]), "r"(R[31]))
+
+#define TMEM_LD32(addr, R)                                                                                     \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+                 "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"               \
+                 : "=r"(R[0]), "=r"(R[1]), "=r"(R[2]), "=r"(R[3]), "=r"(R[4]), "=r"(R[5]), "=r"(R[6]),        \
+                   "=r"(R[7]), "=r"(R[8]), "=r"(R[9]), "=r"(R[10]), "=r"(R[11]), "=r"(R[12]), "=r"(R[13]),    \
+                   "=r"(R[14]), "=r"(R[15]), "=r"(R[16]), "=r"(R[17]), "=r"(R[18]), "=r"(R[19]),              \
+                   "=r"(R[20]), "=r"(R[21]), "=r"(R[22]), "=r"(R[23]), "=r"(R[24]), "=r"(R[25]),              \
+                   "=r"(R[26]), "=r"(R[27]), "=r"(R[28]), "=r"(R[29]), "=r"(R[30]), "=r"(R[31])               \
+                 : "r"(addr))
+
+#define MMA_F16(d, a, b, idesc, acc)                                                                         \
+    asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, " #acc ";" ::"r"(d), "r"(a), "l"(b), \
+                 "r"(idesc))
+
+__global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant__ TcArgs p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    float2* raw = reinterpret_cast<float2*>(smem);                                   // [kRaw][4096]
+    uint8_t* stages = smem + kRaw * kRawBytes;                                       // [kStages][hi|lo]
+    float* staging = reinterpret_cast<float*>(stages + kStages * kStageBytes);       // run-padded tile
+    uint8_t* ctl = reinterpret_cast<uint8_t*>(staging) + kStagingBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ctl);   // [kStages]
+    uint64_t* empty = full + kStages;                     // [kStages]
+    uint64_t* tfull = empty + kStages;                    // [2]
+    uint64_t* tempty = tfull + 2;                         // [2]
+    uint64_t* mfull = tempty + 2;                         // [2]
+    uint64_t* rfull = mfull + 2;                          // [kRaw]
+    uint64_t* rempty = rfull + kRaw;                      // [kRaw]
+    uint64_t* offt = rempty + kRaw;                       // [64] target-combination offsets (global)
+    uint64_t* offj = offt + 64;                           // [64] column offsets (global)
+    uint64_t* offr = offj + 64;                           // [64] run offsets (global)
+    int* wmax = reinterpret_cast<int*>(offr + 64);        // [2][8] per-warp max |x| (float bits)
+    uint16_t* soft = reinterpret_cast<uint16_t*>(wmax + 24);   // [64] sub-cube index of target combo t
+    uint16_t* sofj = soft + 64;                                // [64] sub-cube index of column j
+    int* texp = wmax + 16;                                // [kStages] tile exponent per stage
+    int* meta = texp + kStages;                           // [2] tile exponent per D buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(meta + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; s++) {
+            mbar_init(&full[s], kLoadWarps * 32);
+            mbar_init(&empty[s], 1);
+        }
+        for (int d = 0; d < 2; d++) {
+            mbar_init(&tfull[d], 1);
+            mbar_init(&tempty[d], 128);
+            mbar_init(&mfull[d], 1);
+        }
+        for (int r = 0; r < kRaw; r++) {
+            mbar_init(&rfull[r], 1);
+            mbar_init(&rempty[r], kLoadWarps * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (threadIdx.x < 64) {
+        const int x = threadIdx.x;
+        uint64_t ot = 0, oj = 0, orr = 0;
+        int st = 0, sj = 0;
+        for (int i = 0; i < 6; i++) {
+            int rt = 0, rj = 0;   // rank of pos[i] / jpos[i] among the sorted sub-cube bits
+            for (int b = 0; b < 12; b++) {
+                rt += p.sub[b] < p.pos[i];
+                rj += p.sub[b] < p.jpos[i];
+            }
+            if ((x >> i) & 1) {
+                ot |= 1ull << p.pos[i];
+                oj |= 1ull << p.jpos[i];
+                st |= 1 << rt;
+                sj |= 1 << rj;
+            }
+        }
+        for (int b = p.r; b < 12; b++)
+            if ((x >> (b - p.r)) & 1) orr |= 1ull << p.sub[b];
+        offt[x] = ot;
+        offj[x] = oj;
+        offr[x] = orr;
+        soft[x] = (uint16_t)st;
+        sofj[x] = (uint16_t)sj;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    // A (hi, lo; packed fp16 pairs) -> TMEM by the epilogue warps (warp q owns lanes 32q..)
+    if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+        const int q = warp - kEpiWarp0;
+        const int m = q * 32 + lane;
+        for (int h = 0; h < 2; h++)
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                uint32_t r[32];
+                const uint4* src = reinterpret_cast<const uint4*>(p.a + (size_t)h * 128 * 64 + (size_t)m * 64 + c0);
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    const uint4 v = __ldg(src + c);
+                    r[4 * c] = v.x;
+                    r[4 * c + 1] = v.y;
+                    r[4 * c + 2] = v.z;
+                    r[4 * c + 3] = v.w;
+                }
+                TMEM_ST32(tmem + ((uint32_t)(q * 32) << 16) + h * 64 + c0, r);
+            }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    const uint64_t ntiles = p.ntiles;
+    auto tile_base = [&](uint64_t tile) {
+        uint64_t b = tile;
+#pragma unroll
+        for (int i = 0; i < 12; i++) b = ins0(b, p.sub[i]);
+        return b;
+    };
+
+    if (warp == kProdWarp) {
+        // ---------------- TMA producer: the tile's contiguous runs -> raw stage
+        const int nruns = 1 << (12 - p.r);
+        const uint32_t run_bytes = 8u << p.r;
+        uint64_t it = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const int r = it % kRaw;
+            mbar_wait(&rempty[r], ((it / kRaw) & 1) ^ 1);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[r])),
+                             "r"(kRawBytes)
+                             : "memory");
+            __syncwarp();
+            const float2* src = p.amps + tile_base(tile);
+            const uint32_t dst = su32(raw + (size_t)r * 4096);
+            for (int u = lane; u < nruns; u += 32)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dst + u * run_bytes),
+                    "l"(src + offr[u]), "r"(run_bytes), "r"(su32(&rfull[r]))
+                    : "memory");
+        }
+    } else if (warp < kLoadWarps) {
+        // ---------------- converters: thread = column j, target octets `to` and `to + 4`
+        const int lt = threadIdx.x;           // 0..255
+        const int j = lt & 63;
+        const int to = lt >> 6;               // 0..3
+        const int sj = sofj[j];
+        uint64_t it = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const int r = it % kRaw;
+            mbar_wait(&rfull[r], (it / kRaw) & 1);
+            const float2* rb = raw + (size_t)r * 4096;
+            float2 b[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) b[i] = rb[soft[8 * (to + 4 * (i >> 3)) + (i & 7)] | sj];
+            mbar_arrive(&rempty[r]);
+            // tile max |x|: thread -> warp -> CTA (named barrier over the 8 converter warps)
+            float mx = 0.f;
+#pragma unroll
+            for (int i = 0; i < 16; i++) mx = fmaxf(mx, fmaxf(fabsf(b[i].x), fabsf(b[i].y)));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            int* wm = wmax + 8 * (it & 1);
+            if (lane == 0) wm[warp] = __float_as_int(mx);
+            asm volatile("bar.sync 2, 256;" ::: "memory");
+            int mi = wm[0];
+#pragma unroll
+            for (int w = 1; w < 8; w++) mi = max(mi, wm[w]);   // non-negative floats order as ints
+            const int e = mi > 0 ? ((mi >> 23) & 0xff) - 127 : 0;
+            const float sc = __int_as_float((127 + 14 - e) << 23);   // 2^(14 - e)
+            const int s = it % kStages;
+            mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+            if (lt == 0) texp[s] = e;
+            uint8_t* bhi = stages + s * kStageBytes;
+            uint8_t* blo = bhi + kBBytes;
+#pragma unroll
+            for (int g = 0; g < 2; g++) {
+                uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+                for (int e2 = 0; e2 < 4; e2++) {
+                    float xr[2], xi[2], hr[2], hi2[2];
+#pragma unroll
+                    for (int u = 0; u < 2; u++) {
+                        const float2 v = b[8 * g + 2 * e2 + u];
+                        xr[u] = v.x * sc;
+                        xi[u] = v.y * sc;
+                        hr[u] = __half2float(__float2half_rn(xr[u]));
+                        hi2[u] = __half2float(__float2half_rn(xi[u]));
+                    }
+                    rh[e2] = pack_h2(hr[0], hr[1]);
+                    rl[e2] = pack_h2(xr[0] - hr[0], xr[1] - hr[1]);
+                    ih[e2] = pack_h2(hi2[0], hi2[1]);
+                    il[e2] = pack_h2(xi[0] - hi2[0], xi[1] - hi2[1]);
+                }
+                const int c = to + 4 * g;                 // t octet -> K chunk (re); +8 (im)
+                const uint32_t ore = bchunk(j, c), oim = bchunk(j, c + 8);
+                *reinterpret_cast<uint4*>(bhi + ore) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
+                *reinterpret_cast<uint4*>(bhi + oim) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
+                *reinterpret_cast<uint4*>(blo + ore) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+                *reinterpret_cast<uint4*>(blo + oim) = make_uint4(il[0], il[1], il[2], il[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&full[s]);
+        }
+    } else if (warp == kMmaWarp) {
+        // ---------------- MMA issuer
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        uint64_t it = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const int s = it % kStages, d = it & 1;
+            mbar_wait(&full[s], (it / kStages) & 1);
+            mbar_wait(&tempty[d], ((it >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                meta[d] = texp[s];
+                mbar_arrive(&mfull[d]);
+                const uint32_t sb = su32(stages + s * kStageBytes);
+                const uint32_t d0 = tmem + 128 + d * kAccCols;
+                // descriptors of K-step ks = base + ks * (256 B >> 4): no carry out of the 14-bit field
+                const uint64_t bh0 = bdesc(sb), bl0 = bdesc(sb + kBBytes);
+                const uint32_t ah = tmem, al = tmem + 64;
+                // cross terms (A_hi B_lo, A_lo B_hi) first, into accumulator 0
+                MMA_F16(d0, ah, bl0, idesc, 0);
+                MMA_F16(d0, al, bh0, idesc, 1);
+#pragma unroll
+                for (int ks = 1; ks < TK / 16; ks++) {
+                    MMA_F16(d0, ah + ks * 8, bl0 + ks * 16, idesc, 1);
+                    MMA_F16(d0, al + ks * 8, bh0 + ks * 16, idesc, 1);
+                }
+                // main term A_hi B_hi: K-steps 0-2 -> acc 0, 3-5 -> acc 1, 6-7 -> acc 2
+#pragma unroll
+                for (int ks = 0; ks < 3; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                MMA_F16(d0 + TN, ah + 3 * 8, bh0 + 3 * 16, idesc, 0);
+#pragma unroll
+                for (int ks = 4; ks < 6; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                MMA_F16(d0 + 2 * TN, ah + 6 * 8, bh0 + 6 * 16, idesc, 0);
+                MMA_F16(d0 + 2 * TN, ah + 7 * 8, bh0 + 7 * 16, idesc, 1);
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&empty[s])));
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&tfull[d])));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+        // ---------------- epilogue
+        const int q = warp - kEpiWarp0;
+        const int et = threadIdx.x - kEpiWarp0 * 32;   // 0..127
+        const int m = q * 32 + lane;                   // D row: t = m/2, re (m even) / im (m odd)
+        const int trow = m >> 1, comp = m & 1;
+        // store phase: thread owns column jj and rows t0 + 2i (i < 32)
+        const int jj = et & 63, t0 = et >> 6;
+        const uint64_t oj8 = offj[jj] * 8;
+        const char* sld = reinterpret_cast<const char*>(staging) + (t0 * kPitchF + 2 * jj) * 4;
+        const char* obase = reinterpret_cast<const char*>(offt + t0);
+        float* st = staging + trow * kPitchF + comp;
+        uint64_t it = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const int d = it & 1;
+            mbar_wait(&mfull[d], (it >> 1) & 1);
+            const int e = meta[d];
+            mbar_wait(&tfull[d], (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float us = __int_as_float((127 + e - 28) << 23);   // 2^(e - 14 - 14)
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + 128 + d * kAccCols;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                uint32_t a0[32], a1[32], a2[32];
+                TMEM_LD32(ta + h * 32, a0);
+                TMEM_LD32(ta + TN + h * 32, a1);
+                TMEM_LD32(ta + 2 * TN + h * 32, a2);
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+                if (h == 1) {
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(&tempty[d]);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; c++)
+                    st[2 * (32 * h + c)] =
+                        ((__uint_as_float(a0[c]) + __uint_as_float(a1[c])) + __uint_as_float(a2[c])) * us;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            char* dst = reinterpret_cast<char*>(p.amps + tile_base(tile)) + oj8;
+#pragma unroll 8
+            for (int i = 0; i < 32; i++) {
+                const float2 v = *reinterpret_cast<const float2*>(sld + i * (2 * kPitchF * 4));
+                const uint64_t ot = *reinterpret_cast<const uint64_t*>(obase + i * 16);   // offt[t0 + 2i]
+                __stcs(reinterpret_cast<float2*>(dst + ot * 8), v);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // staging reused by the next tile
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace
+
+size_t tc_matrix_words() { return 2 * 128 * 64; }
+
+// A = [[U_re, -U_im], [U_im, U_re]] (rows interleaved), scaled by 2^14 and split into fp16
+// hi = fp16(2^14 A), lo = fp16(2^14 A - hi) computed from the fp64 product; packed 2 per word
+// (k even in the low half), [hi rows 0..127][lo rows 0..127], 64 words per row.
+void tc_pack_matrix(const double* u_re_im /* 64x64 complex, row-major interleaved */, uint32_t* out) {
+    auto split = [](double x, uint16_t* h, uint16_t* l) {
+        const double xs = x * 16384.0;
+        const __half hh = __float2half_rn((float)xs);
+        const __half ll = __float2half_rn((float)(xs - (double)__half2float(hh)));
+        *h = __half_as_ushort(hh);
+        *l = __half_as_ushort(ll);
+    };
+    for (int m = 0; m < 128; m++) {
+        const int t = m >> 1, im_row = m & 1;
+        for (int k = 0; k < 128; k += 2) {
+            uint16_t h[2], l[2];
+            for (int u = 0; u < 2; u++) {
+                const int kk = k + u;
+                const int col = kk & 63;
+                const double ur = u_re_im[2 * (t * 64 + col)], ui = u_re_im[2 * (t * 64 + col) + 1];
+                double v;
+                if (!im_row) v = kk < 64 ? ur : -ui;   // row 2t:   [U_re | -U_im]
+                else v = kk < 64 ? ui : ur;            // row 2t+1: [U_im |  U_re]
+                split(v, &h[u], &l[u]);
+            }
+            out[(size_t)m * 64 + k / 2] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+            out[(size_t)128 * 64 + (size_t)m * 64 + k / 2] = (uint32_t)l[0] | ((uint32_t)l[1] << 16);
+        }
+    }
+}
+
+cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st) {
+    if (nl < 12) return cudaErrorInvalidValue;
+    TcArgs p{};
+    p.amps = amps;
+    p.a = d_a;
+    p.ntiles = 1ull << (nl - 12);
+    uint64_t tmask = 0;
+    for (int i = 0; i < 6; i++) {
+        p.pos[i] = pos[i];
+        tmask |= 1ull << pos[i];
+    }
+    int nj = 0;
+    for (int b = 0; b < nl && nj < 6; b++)
+        if (!((tmask >> b) & 1)) p.jpos[nj++] = b;
+    if (nj != 6) return cudaErrorInvalidValue;
+    // sub-cube bits = targets U column bits, ascending
+    int all[12], na = 0;
+    for (int b = 0; b < nl && na < 12; b++) {
+        bool in = (tmask >> b) & 1;
+        for (int i = 0; i < 6; i++) in = in || p.jpos[i] == b;
+        if (in) all[na++] = b;
+    }
+    if (na != 12) return cudaErrorInvalidValue;
+    for (int i = 0; i < 12; i++) p.sub[i] = all[i];
+    p.r = 0;
+    while (p.r < 12 && p.sub[p.r] == p.r) p.r++;   // >= 6: the 6 lowest non-targets are in the cube
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_pass_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const uint64_t grid = p.ntiles < (uint64_t)num_sms ? p.ntiles : (uint64_t)num_sms;
+    count_launch();
+    k_pass_tc<<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace dev
+}  // namespace rcs

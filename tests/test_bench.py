@@ -14,7 +14,7 @@ def test_plan_pass_table_matches_planner():
     build.build()
     for cfg in CONFIGS:
         c = Circuit.from_qasm(config_qasm(cfg))
-        for k in (3, 4, 5):
+        for k in (3, 4, 5, 6):
             assert bench.PLAN_PASSES[cfg][k] == Plan(c, k, 0).n_passes, (cfg, k)
 
 

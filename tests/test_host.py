@@ -79,7 +79,7 @@ def test_parser_errors_match_oracle(rcs, text):
 
 def test_block_matrices_unitary_and_cover_all_gates(rcs):
     c = rcs.Circuit.from_qasm(config_qasm("c2"))
-    for k in (2, 3, 4, 5):
+    for k in (2, 3, 4, 5, 6):
         p = rcs.Plan(c, k, 0)
         items = p.items()
         tot = 0
@@ -93,9 +93,9 @@ def test_block_matrices_unitary_and_cover_all_gates(rcs):
 
 
 @pytest.mark.parametrize("seed", range(12))
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 6])
 def test_plan_executor_matches_oracle_random(rcs, seed, k):
-    n = 4 + seed % 6
+    n = 4 + seed % 6 if k < 6 else 12 + seed % 3
     text = random_qasm(n, 60, 1000 + seed)
     ref = oracle.build_state(text)
     c = rcs.Circuit.from_qasm(text)
@@ -114,7 +114,7 @@ def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
     text = emit_qasm(generate(rows, cols, cyc, pat, seed=g))
     ref = oracle.build_state(text)
     c = rcs.Circuit.from_qasm(text)
-    p = rcs.Plan(c, 4, g)
+    p = rcs.Plan(c, 6 if n - g >= 12 else 4, g)
     items = p.items()
     nl = n - g
     for it in items:
@@ -125,7 +125,7 @@ def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
         else:
             assert all(3 <= a < nl and 3 <= b < nl for a, b in zip(it["a"], it["b"]))
     # the fusion is independent of the number of global qubits (P-invariance)
-    p0 = rcs.Plan(c, 4, 0)
+    p0 = rcs.Plan(c, 6 if n - g >= 12 else 4, 0)
     b0 = [i for i in p0.items() if i["type"] == "pass"]
     bg = [i for i in items if i["type"] == "pass"]
     assert len(b0) == len(bg)
@@ -138,7 +138,7 @@ def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
 def test_plan_rejects_bad_arguments(rcs):
     c = rcs.Circuit.from_qasm(config_qasm("c1"))
     with pytest.raises(rcs.RcsError):
-        rcs.Plan(c, 6, 0)
+        rcs.Plan(c, 7, 0)
     with pytest.raises(rcs.RcsError):
         rcs.Plan(c, 4, 9)   # 12 - 9 - 3 < 4 movable local qubits
 
