@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -531,10 +532,26 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         for (auto& e : ev) BUILD_TRY(cudaEventCreate(&e));
     }
     // tensor-core passes: A_hi/A_lo of every 6-qubit block, one H2D copy per build
+    // 5-qubit blocks run there too, padded to 6 with the identity on one more local qubit as
+    // the highest matrix bit (same arithmetic for every choice of that qubit)
     std::vector<int> tc_slot(P.items.size(), -1);
+    std::vector<std::array<int, 6>> tc_pos(P.items.size());
     int n_tc = 0;
-    for (size_t ii = 0; ii < P.items.size(); ii++)
-        if (P.items[ii].type == RCS_ITEM_PASS && P.items[ii].k == 6) tc_slot[ii] = n_tc++;
+    for (size_t ii = 0; ii < P.items.size(); ii++) {
+        const Item& it = P.items[ii];
+        if (it.type != RCS_ITEM_PASS || nl < kTcMinLocal || it.k < 5) continue;
+        for (int i = 0; i < it.k; i++) tc_pos[ii][i] = it.pos[i];
+        if (it.k == 5) {
+            int pad = -1;
+            for (int b = 6; b < nl && pad < 0; b++) {
+                bool used = false;
+                for (int i = 0; i < 5; i++) used = used || it.pos[i] == b;
+                if (!used) pad = b;
+            }
+            tc_pos[ii][5] = pad;
+        }
+        tc_slot[ii] = n_tc++;
+    }
     const size_t tc_words_each = dev::tc_matrix_words();
     const size_t tc_floats = (size_t)n_tc * tc_words_each;
     if (n_tc > 0) {
@@ -549,10 +566,19 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             ctx->tc_cap = tc_floats;
         }
         BUILD_TRY(cudaStreamSynchronize(stream));   // previous build may still read h_tc
-        for (size_t ii = 0; ii < P.items.size(); ii++)
-            if (tc_slot[ii] >= 0)
-                dev::tc_pack_matrix(reinterpret_cast<const double*>(P.blocks[P.items[ii].block].matrix.data()),
-                                    ctx->h_tc + (size_t)tc_slot[ii] * tc_words_each);
+        std::vector<cplx> padded(64 * 64);
+        for (size_t ii = 0; ii < P.items.size(); ii++) {
+            if (tc_slot[ii] < 0) continue;
+            const Block& B = P.blocks[P.items[ii].block];
+            const cplx* m = B.matrix.data();
+            if (P.items[ii].k == 5) {   // U (x) I with the pad qubit as matrix bit 5
+                for (int r = 0; r < 64; r++)
+                    for (int c = 0; c < 64; c++)
+                        padded[r * 64 + c] = ((r ^ c) & 32) ? cplx{0.0, 0.0} : B.matrix[(r & 31) * 32 + (c & 31)];
+                m = padded.data();
+            }
+            dev::tc_pack_matrix(reinterpret_cast<const double*>(m), ctx->h_tc + (size_t)tc_slot[ii] * tc_words_each);
+        }
     }
     BUILD_TRY(cudaEventRecord(eb0, stream));
     if (n_tc > 0)
@@ -564,7 +590,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         const Item& it = P.items[ii];
         if (o.timing) BUILD_TRY(cudaEventRecord(ev[2 * ii], stream));
         if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
-            BUILD_TRY(dev::gate_pass_tc(s->amps, nl, it.pos, ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
+            BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tc_pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
                                         ctx->num_sms, stream));
             pass_bytes += 16ull * n_amps;
         } else if (it.type == RCS_ITEM_PASS) {

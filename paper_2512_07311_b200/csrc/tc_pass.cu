@@ -18,8 +18,10 @@
 // Tile = 64 columns x 64 target combinations = 4096 amplitudes (32 KB), a 12-bit sub-cube of
 // the index: the 6 target bits plus the 6 lowest non-target bits, so every tile is a set of
 // 2^(12-r) contiguous runs of 2^r >= 64 amplitudes.  Persistent kernel, one CTA per SM:
-//   warp  13   producer: cp.async.bulk (TMA) of the tile's runs into raw stage r (4 stages,
-//                         up to 128 KB in flight per SM, no registers) -> rfull[r] (complete_tx)
+//   warp  13   producer: cp.async.bulk (TMA) of a PAIR of adjacent tiles (tile index bit 0 is
+//                         index bit r, right above every run, so each copy covers both tiles'
+//                         runs: >= 1 KB per copy) into a raw pair slot (2 slots = 128 KB, no
+//                         registers) -> rfull[slot] (complete_tx)
 //   warps 0-7  converters: raw smem -> tile max exponent (named barrier) -> hi/lo split ->
 //                         STS into B stage (K-major, interleaved core matrices) -> full[s]
 //   warp  12   MMA     : 8 K-steps x 3 terms = 24 tcgen05.mma kind::f16 (M=128, N=64, K=16,
@@ -67,6 +69,7 @@ struct TcArgs {
     int jpos[6];             // the 6 lowest non-target positions (column bits, ascending)
     int sub[12];             // all 12 sub-cube positions, ascending (for the tile base deposit)
     int r;                   // sub[0..r) == 0..r-1: runs of 2^r contiguous amplitudes
+    int pair;                // 2: tiles processed in adjacent pairs (ntiles >= 2), else 1
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -134,7 +137,7 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant__ TcArgs p) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    float2* raw = reinterpret_cast<float2*>(smem);                                   // [kRaw][4096]
+    float2* raw = reinterpret_cast<float2*>(smem);                                   // [2 pair slots][8192]
     uint8_t* stages = smem + kRaw * kRawBytes;                                       // [kStages][hi|lo]
     float* staging = reinterpret_cast<float*>(stages + kStages * kStageBytes);       // run-padded tile
     uint8_t* ctl = reinterpret_cast<uint8_t*>(staging) + kStagingBytes;
@@ -143,9 +146,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
     uint64_t* tfull = empty + kStages;                    // [2]
     uint64_t* tempty = tfull + 2;                         // [2]
     uint64_t* mfull = tempty + 2;                         // [2]
-    uint64_t* rfull = mfull + 2;                          // [kRaw]
-    uint64_t* rempty = rfull + kRaw;                      // [kRaw]
-    uint64_t* offt = rempty + kRaw;                       // [64] target-combination offsets (global)
+    uint64_t* rfull = mfull + 2;                          // [2] raw pair slots
+    uint64_t* rempty = rfull + 2;                         // [2]
+    uint64_t* offt = rempty + 2;                          // [64] target-combination offsets (global)
     uint64_t* offj = offt + 64;                           // [64] column offsets (global)
     uint64_t* offr = offj + 64;                           // [64] run offsets (global)
     int* wmax = reinterpret_cast<int*>(offr + 64);        // [2][8] per-warp max |x| (float bits)
@@ -170,9 +173,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             mbar_init(&tempty[d], 128);
             mbar_init(&mfull[d], 1);
         }
-        for (int r = 0; r < kRaw; r++) {
+        for (int r = 0; r < 2; r++) {
             mbar_init(&rfull[r], 1);
-            mbar_init(&rempty[r], kLoadWarps * 32);
+            mbar_init(&rempty[r], 2 * kLoadWarps * 32);   // both tiles of the pair consumed
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
@@ -198,8 +201,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         offt[x] = ot;
         offj[x] = oj;
         offr[x] = orr;
-        soft[x] = (uint16_t)st;
-        sofj[x] = (uint16_t)sj;
+        // raw pair layout: element index = s with a zero inserted at bit r (bit r = pair half)
+        const int lowm = (1 << p.r) - 1;
+        soft[x] = (uint16_t)(((st & ~lowm) << 1) | (st & lowm));
+        sofj[x] = (uint16_t)(((sj & ~lowm) << 1) | (sj & lowm));
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -237,28 +242,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         for (int i = 0; i < 12; i++) b = ins0(b, p.sub[i]);
         return b;
     };
+    // every role walks the same tile sequence: pairs (2i, 2i+1), i = blockIdx.x + k gridDim.x
+    const uint64_t first_tile = (uint64_t)blockIdx.x * p.pair;
+    auto next_tile = [&](uint64_t t) -> uint64_t {
+        if (p.pair == 2 && !(t & 1)) return t + 1;
+        return t - (p.pair == 2 ? 1 : 0) + (uint64_t)gridDim.x * p.pair;
+    };
 
     if (warp == kProdWarp) {
-        // ---------------- TMA producer: the tile's contiguous runs -> raw stage
+        // ---------------- TMA producer: both tiles of a pair, runs of 2 x 2^r amplitudes
         const int nruns = 1 << (12 - p.r);
-        const uint32_t run_bytes = 8u << p.r;
+        const uint32_t copy_bytes = (8u << p.r) * (uint32_t)p.pair;   // one run of each tile of the pair
+        const uint32_t dst_stride = (8u << p.r) * 2;                  // same layout when pair == 1
         uint64_t it = 0;
-        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
-            const int r = it % kRaw;
-            mbar_wait(&rempty[r], ((it / kRaw) & 1) ^ 1);
+        for (uint64_t tile = first_tile; tile < ntiles; it++) {
+            if (p.pair == 2 && (tile & 1)) { tile = next_tile(tile); continue; }   // odd half: copied with its pair
+            const int slot = (it >> (p.pair - 1)) & 1;
+            const uint64_t use = it >> (p.pair);                   // uses of this slot before
+            mbar_wait(&rempty[slot], (use & 1) ^ 1);
             if (lane == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[r])),
-                             "r"(kRawBytes)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[slot])),
+                             "r"(kRawBytes * p.pair)
                              : "memory");
             __syncwarp();
             const float2* src = p.amps + tile_base(tile);
-            const uint32_t dst = su32(raw + (size_t)r * 4096);
+            const uint32_t dst = su32(raw + (size_t)slot * 8192);
             for (int u = lane; u < nruns; u += 32)
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        dst + u * run_bytes),
-                    "l"(src + offr[u]), "r"(run_bytes), "r"(su32(&rfull[r]))
+                        dst + u * dst_stride),
+                    "l"(src + offr[u]), "r"(copy_bytes), "r"(su32(&rfull[slot]))
                     : "memory");
+            tile = next_tile(tile);
         }
     } else if (warp < kLoadWarps) {
         // ---------------- converters: thread = column j, target octets `to` and `to + 4`
@@ -267,14 +282,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         const int to = lt >> 6;               // 0..3
         const int sj = sofj[j];
         uint64_t it = 0;
-        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
-            const int r = it % kRaw;
-            mbar_wait(&rfull[r], (it / kRaw) & 1);
-            const float2* rb = raw + (size_t)r * 4096;
+        for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
+            const int slot = (it >> (p.pair - 1)) & 1;
+            const uint64_t use = it >> (p.pair);
+            mbar_wait(&rfull[slot], use & 1);
+            const float2* rb = raw + (size_t)slot * 8192 + ((p.pair == 2 && (tile & 1)) ? (1 << p.r) : 0);
             float2 b[16];
 #pragma unroll
             for (int i = 0; i < 16; i++) b[i] = rb[soft[8 * (to + 4 * (i >> 3)) + (i & 7)] | sj];
-            mbar_arrive(&rempty[r]);
+            mbar_arrive(&rempty[slot]);
+            if (p.pair == 1) mbar_arrive(&rempty[slot]);   // count is for two tiles
             // tile max |x|: thread -> warp -> CTA (named barrier over the 8 converter warps)
             float mx = 0.f;
 #pragma unroll
@@ -327,7 +344,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         // ---------------- MMA issuer
         const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         uint64_t it = 0;
-        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
             const int s = it % kStages, d = it & 1;
             mbar_wait(&full[s], (it / kStages) & 1);
             mbar_wait(&tempty[d], ((it >> 1) & 1) ^ 1);
@@ -376,7 +393,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         const char* obase = reinterpret_cast<const char*>(offt + t0);
         float* st = staging + trow * kPitchF + comp;
         uint64_t it = 0;
-        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
             const int d = it & 1;
             mbar_wait(&mfull[d], (it >> 1) & 1);
             const int e = meta[d];
@@ -477,13 +494,15 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
     for (int i = 0; i < 12; i++) p.sub[i] = all[i];
     p.r = 0;
     while (p.r < 12 && p.sub[p.r] == p.r) p.r++;   // >= 6: the 6 lowest non-targets are in the cube
+    p.pair = p.ntiles >= 2 ? 2 : 1;                // tile bit 0 = index bit r (first non-cube bit)
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_pass_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const uint64_t grid = p.ntiles < (uint64_t)num_sms ? p.ntiles : (uint64_t)num_sms;
+    const uint64_t units = p.ntiles / p.pair;
+    const uint64_t grid = units < (uint64_t)num_sms ? units : (uint64_t)num_sms;
     count_launch();
     k_pass_tc<<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
     return cudaGetLastError();

@@ -26,4 +26,4 @@ for it, ms in zip(passes, t):
     rows.append((it["k"], sorted(it["pos"]), float(ms), gbs, it["n_gates"]))
     print(f"k={it['k']} pos={sorted(it['pos'])!s:28s} gates={it['n_gates']:3d} {ms:8.3f} ms {gbs:7.0f} GB/s")
 print("build_ms", st.report["build_ms"], "sum pass ms", float(t.sum()))
-json.dump(rows, open(f"gpurun_out/pass_report_{cfg}_k{k}.json", "w"))
+json.dump([[a, b, float(c), float(d), e] for a, b, c, d, e in rows], open(f"gpurun_out/pass_report_{cfg}_k{k}.json", "w"))
