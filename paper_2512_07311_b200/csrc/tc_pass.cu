@@ -44,7 +44,9 @@ namespace rcs {
 namespace dev {
 namespace {
 
-constexpr int kLoadWarps = 8, kEpiWarp0 = 8, kMmaWarp = 12, kProdWarp = 13, kWarps = 14, kThreadsTC = kWarps * 32;
+constexpr int kLoadWarps = 8, kEpiWarp0 = 8, kEpiWarps = 4, kMmaWarp = 12, kProdWarp = 13, kWarps = 14;
+constexpr int kThreadsTC = kWarps * 32;
+constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int TN = 64;                       // columns per tile (MMA N)
 constexpr int TK = 128;                      // real K
 constexpr int kStages = 2;                   // B stages
@@ -57,7 +59,7 @@ constexpr int kPitchF = 130;                 // staging row pitch in floats (520
 constexpr uint32_t kStagingBytes = 64 * kPitchF * 4;
 constexpr uint32_t kCtlBytes = 2560;   // barriers + offset tables; total <= 227 KB
 // control block: 18 mbarriers + 3 x 64 offsets (8 B) + 24 ints + 2 x 64 uint16
-static_assert(18 * 8 + 3 * 64 * 8 + 24 * 4 + 2 * 64 * 2 <= 2048, "control block overflow");
+static_assert(18 * 8 + 3 * 64 * 8 + 24 * 4 + 2 * 64 * 2 <= 2560, "control block overflow");
 constexpr uint32_t kSmemBytes = kRaw * kRawBytes + kStages * kStageBytes + kStagingBytes + kCtlBytes;
 constexpr int kAccCols = 3 * TN;             // one D buffer
 
@@ -70,6 +72,8 @@ struct TcArgs {
     int sub[12];             // all 12 sub-cube positions, ascending (for the tile base deposit)
     int r;                   // sub[0..r) == 0..r-1: runs of 2^r contiguous amplitudes
     int pair;                // 2: tiles processed in adjacent pairs (ntiles >= 2), else 1
+    int sso[32];             // staging offset (floats) of sub-cube index 128 i
+    uint64_t sgo[32];        // global offset (amplitudes) of sub-cube index 128 i
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -109,6 +113,20 @@ __device__ __forceinline__ uint32_t bchunk(int n, int c) {
     return (uint32_t)((n >> 3) * kSBO + c * 128 + (n & 7) * 16);
 }
 
+// out half k = in half (k - rho) & 7 for a packed octet of fp16 (4 words); rho lane-dependent,
+// so it is done with selects and byte permutes (no dynamic register indexing)
+__device__ __forceinline__ void rot_h8(uint32_t (&w)[4], int rho) {
+    uint32_t a[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) a[i] = (rho & 2) ? w[(i + 3) & 3] : w[i];   // 1 word = 2 halves
+#pragma unroll
+    for (int i = 0; i < 4; i++) w[i] = (rho & 4) ? a[(i + 2) & 3] : a[i];   // 2 words
+#pragma unroll
+    for (int i = 0; i < 4; i++) a[i] = __byte_perm(w[(i + 3) & 3], w[i], 0x5432);   // 1 half
+#pragma unroll
+    for (int i = 0; i < 4; i++) w[i] = (rho & 1) ? a[i] : w[i];
+}
+
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
     return (uint32_t)__half_as_ushort(__float2half_rn(a)) | ((uint32_t)__half_as_ushort(__float2half_rn(b)) << 16);
 }
@@ -135,6 +153,10 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
     asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, " #acc ";" ::"r"(d), "r"(a), "l"(b), \
                  "r"(idesc))
 
+// ROT: when >= 2 target bits are among the 4 lowest sub-cube bits, the converters' shared-memory
+// reads of one element index across lanes hit the same banks; lane l then walks its target octet
+// starting at element (l & 7) and rotates the packed fp16 octet back before storing it.
+template <bool ROT>
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant__ TcArgs p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     float2* raw = reinterpret_cast<float2*>(smem);                                   // [2 pair slots][8192]
@@ -170,7 +192,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         }
         for (int d = 0; d < 2; d++) {
             mbar_init(&tfull[d], 1);
-            mbar_init(&tempty[d], 128);
+            mbar_init(&tempty[d], kEpiThreads);
             mbar_init(&mfull[d], 1);
         }
         for (int r = 0; r < 2; r++) {
@@ -206,6 +228,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         soft[x] = (uint16_t)(((st & ~lowm) << 1) | (st & lowm));
         sofj[x] = (uint16_t)(((sj & ~lowm) << 1) | (sj & lowm));
     }
+    // sub-cube index s -> (target combo t, column j, global offset); bit b of s is sub[b]
+    auto decomp = [&](int sidx, int& t, int& jj, uint64_t& go) {
+        t = 0;
+        jj = 0;
+        go = 0;
+        for (int b = 0; b < 12; b++) {
+            if (!((sidx >> b) & 1)) continue;
+            go |= 1ull << p.sub[b];
+            for (int i = 0; i < 6; i++) {
+                if (p.pos[i] == p.sub[b]) t |= 1 << i;
+                if (p.jpos[i] == p.sub[b]) jj |= 1 << i;
+            }
+        }
+    };
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -281,6 +317,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         const int j = lt & 63;
         const int to = lt >> 6;               // 0..3
         const int sj = sofj[j];
+        const int rho = ROT ? (lane & 7) : 0;
         uint64_t it = 0;
         for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
             const int slot = (it >> (p.pair - 1)) & 1;
@@ -289,7 +326,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             const float2* rb = raw + (size_t)slot * 8192 + ((p.pair == 2 && (tile & 1)) ? (1 << p.r) : 0);
             float2 b[16];
 #pragma unroll
-            for (int i = 0; i < 16; i++) b[i] = rb[soft[8 * (to + 4 * (i >> 3)) + (i & 7)] | sj];
+            for (int i = 0; i < 16; i++) b[i] = rb[soft[8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj];
             mbar_arrive(&rempty[slot]);
             if (p.pair == 1) mbar_arrive(&rempty[slot]);   // count is for two tiles
             // tile max |x|: thread -> warp -> CTA (named barrier over the 8 converter warps)
@@ -329,6 +366,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                     rl[e2] = pack_h2(xr[0] - hr[0], xr[1] - hr[1]);
                     ih[e2] = pack_h2(hi2[0], hi2[1]);
                     il[e2] = pack_h2(xi[0] - hi2[0], xi[1] - hi2[1]);
+                }
+                if (ROT) {
+                    rot_h8(rh, rho);
+                    rot_h8(rl, rho);
+                    rot_h8(ih, rho);
+                    rot_h8(il, rho);
                 }
                 const int c = to + 4 * g;                 // t octet -> K chunk (re); +8 (im)
                 const uint32_t ore = bchunk(j, c), oim = bchunk(j, c + 8);
@@ -380,17 +423,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             }
             __syncwarp();
         }
-    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-        // ---------------- epilogue
-        const int q = warp - kEpiWarp0;
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
+        // ---------------- epilogue: warp q reads TMEM lane quarter q (rows 32q .. 32q+31)
+        const int q = warp & 3;
         const int et = threadIdx.x - kEpiWarp0 * 32;   // 0..127
         const int m = q * 32 + lane;                   // D row: t = m/2, re (m even) / im (m odd)
         const int trow = m >> 1, comp = m & 1;
-        // store phase: thread owns column jj and rows t0 + 2i (i < 32)
-        const int jj = et & 63, t0 = et >> 6;
-        const uint64_t oj8 = offj[jj] * 8;
-        const char* sld = reinterpret_cast<const char*>(staging) + (t0 * kPitchF + 2 * jj) * 4;
-        const char* obase = reinterpret_cast<const char*>(offt + t0);
+        // store phase in memory order: thread handles sub-cube indices et + 128 i (i < 32), so
+        // consecutive lanes write consecutive addresses for every target layout
+        int tb, jb;
+        uint64_t gb;
+        decomp(et, tb, jb, gb);
+        const float* sld = staging + tb * kPitchF + 2 * jb;
         float* st = staging + trow * kPitchF + comp;
         uint64_t it = 0;
         for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
@@ -404,26 +448,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 uint32_t a0[32], a1[32], a2[32];
-                TMEM_LD32(ta + h * 32, a0);
-                TMEM_LD32(ta + TN + h * 32, a1);
-                TMEM_LD32(ta + 2 * TN + h * 32, a2);
+                TMEM_LD32(ta + 32 * h, a0);
+                TMEM_LD32(ta + TN + 32 * h, a1);
+                TMEM_LD32(ta + 2 * TN + 32 * h, a2);
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
                 if (h == 1) {
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     mbar_arrive(&tempty[d]);
                 }
 #pragma unroll
-                for (int c = 0; c < 32; c++)
-                    st[2 * (32 * h + c)] =
-                        ((__uint_as_float(a0[c]) + __uint_as_float(a1[c])) + __uint_as_float(a2[c])) * us;
+                for (int c = 0; c < 32; c += 2) {
+                    float o0, o1;   // ((acc0 + acc1) + acc2) * 2^(e-28), two columns per packed op
+                    asm("{\n.reg .b64 x, y, z, u;\n"
+                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 z, {%6, %7};\nmov.b64 u, {%8, %8};\n"
+                        "add.rn.f32x2 x, x, y;\nadd.rn.f32x2 x, x, z;\nmul.rn.f32x2 x, x, u;\n"
+                        "mov.b64 {%0, %1}, x;\n}"
+                        : "=f"(o0), "=f"(o1)
+                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "r"(a2[c]), "r"(a2[c + 1]),
+                          "f"(us));
+                    st[2 * (32 * h + c)] = o0;
+                    st[2 * (32 * h + c) + 2] = o1;
+                }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            char* dst = reinterpret_cast<char*>(p.amps + tile_base(tile)) + oj8;
+            float2* dst = p.amps + (tile_base(tile) | gb);
 #pragma unroll 8
             for (int i = 0; i < 32; i++) {
-                const float2 v = *reinterpret_cast<const float2*>(sld + i * (2 * kPitchF * 4));
-                const uint64_t ot = *reinterpret_cast<const uint64_t*>(obase + i * 16);   // offt[t0 + 2i]
-                __stcs(reinterpret_cast<float2*>(dst + ot * 8), v);
+                const float2 v = *reinterpret_cast<const float2*>(sld + p.sso[i]);
+                __stcs(dst + p.sgo[i], v);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");   // staging reused by the next tile
         }
@@ -495,16 +547,39 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
     p.r = 0;
     while (p.r < 12 && p.sub[p.r] == p.r) p.r++;   // >= 6: the 6 lowest non-targets are in the cube
     p.pair = p.ntiles >= 2 ? 2 : 1;                // tile bit 0 = index bit r (first non-cube bit)
+    for (int i = 0; i < 32; i++) {                 // epilogue store offsets of sub-cube index 128 i
+        const int sidx = 128 * i;
+        int t = 0, jj = 0;
+        uint64_t go = 0;
+        for (int b = 0; b < 12; b++) {
+            if (!((sidx >> b) & 1)) continue;
+            go |= 1ull << p.sub[b];
+            for (int k = 0; k < 6; k++) {
+                if (p.pos[k] == p.sub[b]) t |= 1 << k;
+                if (p.jpos[k] == p.sub[b]) jj |= 1 << k;
+            }
+        }
+        p.sso[i] = t * kPitchF + 2 * jj;
+        p.sgo[i] = go;
+    }
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(k_pass_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_pass_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    // bank conflicts of the converters' reads: target bits among the 4 lowest sub-cube bits
+    int low_targets = 0;
+    for (int i = 0; i < 4; i++) low_targets += (int)((tmask >> p.sub[i]) & 1);
     const uint64_t units = p.ntiles / p.pair;
     const uint64_t grid = units < (uint64_t)num_sms ? units : (uint64_t)num_sms;
     count_launch();
-    k_pass_tc<<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
+    if (low_targets >= 2)
+        k_pass_tc<true><<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
+    else
+        k_pass_tc<false><<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
     return cudaGetLastError();
 }
 
