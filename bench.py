@@ -314,7 +314,8 @@ def run_ours(args):
             "xeb": X["F"], "xeb_sigma": X["sigma"], "fstar": X["fstar"], "norm": R["norm"],
             "n_passes": R["n_passes"], "n_remaps": R["n_remaps"], "n_swaps": R["n_swaps"],
             "pass_gbs": {"min": gbs[0], "median": gbs[len(gbs) // 2], "max": gbs[-1]},
-            "pass_ms_total": R["pass_ms"], "remap_ms_total": R["remap_ms"], "blocksum_ms": R["blocksum_ms"],
+            "pass_ms_total": R["pass_ms"], "remap_ms_total": R["remap_ms"], "swap_ms_total": R["swap_ms"],
+            "blocksum_ms": R["blocksum_ms"], "n_tc_passes": R["n_tc_passes"],
             "remap_gbs": (R["remap_bytes"] / (R["remap_ms"] / 1e3) / 1e9) if R["remap_ms"] > 0 else None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config, world),

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -26,6 +27,13 @@ struct rcs_context {
     uint32_t* d_tc = nullptr;
     uint32_t* h_tc = nullptr;
     size_t tc_cap = 0;   // words
+    // remaps over NVLink: CUDA-IPC mappings of the peers' shards (re-checked every build)
+    bool p2p = false;                 // every peer mappable
+    char* d_xchg = nullptr;           // device buffer for the handle all-gather
+    cudaIpcMemHandle_t peer_handle[8];
+    uint64_t peer_off[8] = {0};
+    void* peer_map[8] = {nullptr};
+    float* d_bar = nullptr;           // 1-float all-reduce used as a stream-ordered barrier
 };
 
 struct rcs_state {
@@ -165,6 +173,118 @@ rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs
         *bytes_sent += e * 8ull * np;
     }
     return RCS_OK;
+}
+
+// --- NVLink peer mapping -----------------------------------------------------------------
+typedef int (*PFN_getAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+rcs_status setup_peers(rcs_context* c, void* amps, rcs_error* err) {
+    c->p2p = false;
+    if (getenv("RCS_REMAP_NCCL")) return RCS_OK;   // force the NCCL send/recv path
+    for (int r = 0; r < c->world; r++) {
+        if (r == c->rank) continue;
+        int can = 0;
+        if (cudaDeviceCanAccessPeer(&can, c->device, r) != cudaSuccess || !can) {
+            cudaGetLastError();
+            return RCS_OK;   // ranks are not one-GPU-per-device-index on this box: NCCL path
+        }
+    }
+    static PFN_getAddressRange get_range = nullptr;
+    if (!get_range) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return RCS_OK;
+        get_range = (PFN_getAddressRange)fn;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (unsigned long long)amps) != 0) return RCS_OK;
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        uint64_t off;
+        int ok;
+    } mine{};
+    mine.off = (uint64_t)amps - base;
+    mine.ok = cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess;
+    if (!mine.ok) cudaGetLastError();
+    const size_t rec = (sizeof(Rec) + 15) / 16 * 16;
+    if (!c->d_xchg) CUDA_TRY(cudaMalloc(&c->d_xchg, rec * (c->world + 1)));
+    if (!c->d_bar) CUDA_TRY(cudaMalloc(&c->d_bar, 16));
+    CUDA_TRY(cudaMemcpyAsync(c->d_xchg, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(ncclAllGather(c->d_xchg, c->d_xchg + rec, rec, ncclChar, c->comm, c->stream));
+    std::vector<char> all(rec * c->world);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), c->d_xchg + rec, rec * c->world, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    bool ok = true;
+    for (int r = 0; r < c->world; r++) ok = ok && reinterpret_cast<Rec*>(all.data() + rec * r)->ok;
+    if (!ok) return RCS_OK;
+    for (int r = 0; r < c->world; r++) {
+        if (r == c->rank) continue;
+        const Rec* pr = reinterpret_cast<const Rec*>(all.data() + rec * r);
+        if (c->peer_map[r] && std::memcmp(&c->peer_handle[r], &pr->h, sizeof pr->h) == 0) {
+            c->peer_off[r] = pr->off;
+            continue;
+        }
+        if (c->peer_map[r]) cudaIpcCloseMemHandle(c->peer_map[r]);
+        c->peer_map[r] = nullptr;
+        void* mp = nullptr;
+        if (cudaIpcOpenMemHandle(&mp, pr->h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return RCS_OK;
+        }
+        c->peer_map[r] = mp;
+        c->peer_handle[r] = pr->h;
+        c->peer_off[r] = pr->off;
+    }
+    c->p2p = true;
+    return RCS_OK;
+}
+
+// stream-ordered barrier over all ranks (no rank proceeds past it before every rank reached it)
+rcs_status stream_barrier(rcs_context* c, rcs_error* err) {
+    NCCL_TRY(ncclAllReduce(c->d_bar, c->d_bar, 1, ncclFloat, ncclSum, c->comm, c->stream));
+    return RCS_OK;
+}
+
+// Remap over NVLink: swap the exchanged halves in place, local <-> peer (CUDA-IPC mapping);
+// every unordered rank pair splits its element pairs in two halves, one per rank.
+rcs_status do_remap_p2p(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_error* err) {
+    rcs_context* c = s->ctx;
+    const int j = it.k, nl = s->nl;
+    dev::PeerSwapArgs A{};
+    A.local = s->amps;
+    A.j = j;
+    int lpos[8];
+    for (int i = 0; i < j; i++) lpos[i] = it.b[i];
+    std::sort(lpos, lpos + j);
+    for (int i = 0; i < j; i++) A.lpos[i] = lpos[i];
+    int my_code = 0;
+    for (int i = 0; i < j; i++) my_code |= ((c->rank >> (it.a[i] - nl)) & 1) << i;
+    for (int i = 0; i < j; i++)
+        if ((my_code >> i) & 1) A.my_mask |= 1ull << it.b[i];
+    const uint64_t count = 1ull << (nl - j);
+    for (int code = 0; code < (1 << j); code++) {
+        if (code == my_code) continue;
+        int peer = c->rank;
+        uint64_t mask = 0;
+        for (int i = 0; i < j; i++) {
+            const int gb = it.a[i] - nl;
+            peer = (peer & ~(1 << gb)) | (((code >> i) & 1) << gb);
+            if ((code >> i) & 1) mask |= 1ull << it.b[i];
+        }
+        const int pc = A.npeers++;
+        A.peer[pc] = reinterpret_cast<float2*>(static_cast<char*>(c->peer_map[peer]) + c->peer_off[peer]);
+        A.mask[pc] = mask;
+        const uint64_t half = count / 2;
+        A.m_begin[pc] = c->rank < peer ? 0 : half;
+        A.m_count[pc] = c->rank < peer ? half : count - half;
+        *bytes_sent += count * 8ull;
+    }
+    rcs_status st = stream_barrier(c, err);
+    if (st) return st;
+    CUDA_TRY(dev::peer_swap(A, c->stream));
+    return stream_barrier(c, err);
 }
 
 // block sums + scan + shard totals (collective); fills s->T_*, E_r, sum_sq, ownership
@@ -437,6 +557,10 @@ rcs_status rcs_context_create(int device, int rank, int world, const void* nccl_
 void rcs_context_free(rcs_context* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    for (int r = 0; r < 8; r++)
+        if (c->peer_map[r]) cudaIpcCloseMemHandle(c->peer_map[r]);
+    if (c->d_xchg) cudaFree(c->d_xchg);
+    if (c->d_bar) cudaFree(c->d_bar);
     if (c->d_tc) cudaFree(c->d_tc);
     if (c->h_tc) cudaFreeHost(c->h_tc);
     if (c->comm) ncclCommDestroy(c->comm);
@@ -580,6 +704,10 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             dev::tc_pack_matrix(reinterpret_cast<const double*>(m), ctx->h_tc + (size_t)tc_slot[ii] * tc_words_each);
         }
     }
+    if (ctx->world > 1 && P.n_remaps > 0) {
+        rcs_status r = setup_peers(ctx, s->amps, err);
+        if (r) return fail(r);
+    }
     BUILD_TRY(cudaEventRecord(eb0, stream));
     if (n_tc > 0)
         BUILD_TRY(cudaMemcpyAsync(ctx->d_tc, ctx->h_tc, tc_floats * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
@@ -608,7 +736,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             if (ctx->world == 1) {
                 BUILD_TRY(dev::bit_swap(s->amps, nl, it.k, it.a, it.b, stream));
             } else {
-                rcs_status r = do_remap_nccl(s, it, &remap_bytes, err);
+                rcs_status r = ctx->p2p ? do_remap_p2p(s, it, &remap_bytes, err)
+                                        : do_remap_nccl(s, it, &remap_bytes, err);
                 if (r) return fail(r);
             }
         }
@@ -644,6 +773,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
                 R.pass_ms_min = std::min(R.pass_ms_min, (double)t);
                 R.pass_ms_max = std::max(R.pass_ms_max, (double)t);
                 s->pass_ms.push_back(t);
+            } else if (P.items[ii].type == RCS_ITEM_SWAP) {
+                R.swap_ms += t;
             } else {
                 R.remap_ms += t;
             }

@@ -227,6 +227,40 @@ __global__ void __launch_bounds__(kThreads) k_pack(float2* __restrict__ amps, fl
     }
 }
 
+// peer swap (remap over NVLink): each thread moves U 16-B vectors each way, loads first
+constexpr int kSwapU = 4;
+__global__ void __launch_bounds__(kThreads) k_peer_swap(const __grid_constant__ PeerSwapArgs a) {
+    const int pc = blockIdx.y;
+    const uint64_t nvec = a.m_count[pc] >> 1;   // 16-B vectors (2 amplitudes)
+    float4* loc = reinterpret_cast<float4*>(a.local);
+    float4* rem = reinterpret_cast<float4*>(a.peer[pc]);
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads * kSwapU;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * kThreads * kSwapU + threadIdx.x; v0 < nvec; v0 += stride) {
+        uint64_t li[kSwapU], ri[kSwapU];
+        float4 lv[kSwapU], rv[kSwapU];
+        bool ok[kSwapU];
+#pragma unroll
+        for (int u = 0; u < kSwapU; u++) {
+            const uint64_t v = v0 + (uint64_t)u * kThreads;
+            ok[u] = v < nvec;
+            uint64_t m = a.m_begin[pc] + 2 * v;
+            for (int i = 0; i < a.j; i++) m = insert_zero(m, a.lpos[i]);
+            li[u] = (m | a.mask[pc]) >> 1;
+            ri[u] = (m | a.my_mask) >> 1;
+            if (ok[u]) {
+                lv[u] = loc[li[u]];
+                rv[u] = rem[ri[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kSwapU; u++)
+            if (ok[u]) {
+                loc[li[u]] = rv[u];
+                rem[ri[u]] = lv[u];
+            }
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // K5: block sums; K6: scan; reductions
 // ------------------------------------------------------------------------------------
@@ -535,6 +569,17 @@ cudaError_t unpack(float2* amps, const float2* buf, int j, const int* lpos, uint
                    uint64_t count, cudaStream_t st) {
     note_launch();
     k_pack<false><<<grid_for(count), kThreads, 0, st>>>(amps, const_cast<float2*>(buf), make_pack(j, lpos, codemask, m0, count));
+    return cudaGetLastError();
+}
+
+cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st) {
+    uint64_t maxv = 0;
+    for (int i = 0; i < a.npeers; i++) maxv = a.m_count[i] / 2 > maxv ? a.m_count[i] / 2 : maxv;
+    if (maxv == 0) return cudaSuccess;
+    uint64_t gx = (maxv + (uint64_t)kThreads * kSwapU - 1) / ((uint64_t)kThreads * kSwapU);
+    if (gx > 148u * 8u) gx = 148u * 8u;
+    note_launch();
+    k_peer_swap<<<dim3((unsigned)gx, (unsigned)a.npeers), kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

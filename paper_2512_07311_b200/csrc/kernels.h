@@ -36,6 +36,22 @@ cudaError_t pack(const float2* amps, float2* buf, int j, const int* lpos_sorted,
 cudaError_t unpack(float2* amps, const float2* buf, int j, const int* lpos_sorted, uint64_t codemask,
                    uint64_t m0, uint64_t count, cudaStream_t st);
 
+// a7 (K10-lite): in-place remap over NVLink.  For every peer c: swap local[l] <-> peer_c[l'] with
+// l = ins(m) | mask_c, l' = ins(m) | my_mask (ins = insert zeros at the sorted local swap
+// positions), for m in this rank's share [m_begin_c, m_begin_c + m_count_c) (m even, pairs of
+// amplitudes moved as 16-B vectors).  Peer pointers are CUDA-IPC mappings of the peers' shards.
+struct PeerSwapArgs {
+    float2* local;
+    float2* peer[7];
+    int npeers;
+    int j;
+    int lpos[8];
+    uint64_t mask[7];
+    uint64_t my_mask;
+    uint64_t m_begin[7], m_count[7];
+};
+cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st);
+
 // a9 (K5): bsum[blk] = sum_{x in blk} |a_x|^2 (fp64) for blocks of 2^b amps; part[c] = per-CTA
 // partial sum of p^2 (fixed grid => deterministic).  Returns the number of partials used.
 int block_sums_grid();

@@ -21,15 +21,18 @@ def ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_sharded_build_sample_xeb(world, tmp_path, cuda_ok):
+def test_sharded_build_sample_xeb(world, mode, tmp_path, cuda_ok):
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     from paper_2512_07311_b200 import build
     build.build()
     env = dict(os.environ, MGPU_OUT=str(tmp_path))
+    if mode == "nccl":
+        env["RCS_REMAP_NCCL"] = "1"   # grouped send/recv remaps instead of NVLink peer swaps
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-                        "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
+                        "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if mode == "nccl" else 0)),
                         os.path.join(ROOT, "tests", "mgpu_worker.py")], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
