@@ -39,13 +39,13 @@ METRIC = "fused gate-pass HBM GB/s (whole RCS step: state build + shots + XEB)"
 # Fused passes per config and fuse_k of the library's planner (P-independent).  The reference
 # arm converts oracle time into the same unit with this table instead of calling our engine;
 # tests/test_bench.py keeps it equal to rcs_plan_create's output.
-PLAN_PASSES = {'c1': {3: 32, 4: 20, 5: 15, 6: 11},
-               'c2': {3: 102, 4: 50, 5: 40, 6: 29},
-               'c3': {3: 101, 4: 65, 5: 47, 6: 37},
-               'c4': {3: 154, 4: 84, 5: 61, 6: 42},
-               'c5': {3: 163, 4: 91, 5: 66, 6: 47},
-               'w33': {3: 119, 4: 77, 5: 56, 6: 42},
-               'w35': {3: 161, 4: 86, 5: 60, 6: 49}}
+PLAN_PASSES = {'c1': {3: 32, 4: 20, 5: 15, 6: 10},
+               'c2': {3: 97, 4: 48, 5: 39, 6: 29},
+               'c3': {3: 99, 4: 60, 5: 44, 6: 34},
+               'c4': {3: 144, 4: 78, 5: 57, 6: 40},
+               'c5': {3: 154, 4: 85, 5: 62, 6: 42},
+               'w33': {3: 115, 4: 74, 5: 54, 6: 42},
+               'w35': {3: 140, 4: 84, 5: 57, 6: 46}}
 
 
 def parse_args():

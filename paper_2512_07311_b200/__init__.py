@@ -51,7 +51,10 @@ class Circuit:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().rcs_circuit_free(h)
+            try:
+                lib().rcs_circuit_free(h)
+            except Exception:   # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     def stats(self) -> dict:
@@ -91,7 +94,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().rcs_plan_free(h)
+            try:
+                lib().rcs_plan_free(h)
+            except Exception:   # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     def items(self) -> list:
@@ -156,7 +162,10 @@ class Context:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().rcs_context_free(h)
+            try:
+                lib().rcs_context_free(h)
+            except Exception:   # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
 
@@ -198,7 +207,10 @@ class State:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().rcs_state_free(h)
+            try:
+                lib().rcs_state_free(h)
+            except Exception:   # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     def free(self):

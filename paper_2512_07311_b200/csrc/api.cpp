@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -25,8 +26,10 @@ struct rcs_context {
     ncclComm_t comm = nullptr;
     // device plan buffer for the tensor-core passes' A matrices (+ pinned host staging)
     uint32_t* d_tc = nullptr;
-    uint32_t* h_tc = nullptr;
     size_t tc_cap = 0;   // words
+    uint64_t tc_uid = 0;                          // circuit / pack whose matrices d_tc holds
+    const rcs::TcPack* tc_pack = nullptr;
+    std::shared_ptr<const rcs::TcPack> tc_hold;   // keeps that pack alive
     // remaps over NVLink: CUDA-IPC mappings of the peers' shards (re-checked every build)
     bool p2p = false;                 // every peer mappable
     char* d_xchg = nullptr;           // device buffer for the handle all-gather
@@ -34,6 +37,11 @@ struct rcs_context {
     uint64_t peer_off[8] = {0};
     void* peer_map[8] = {nullptr};
     float* d_bar = nullptr;           // 1-float all-reduce used as a stream-ordered barrier
+    // sampling / XEB chunk buffers, shared by every state of this context
+    unsigned long long* xbuf = nullptr;
+    double* dbuf = nullptr;
+    double* xeb_part = nullptr;
+    int* bad = nullptr;
 };
 
 struct rcs_state {
@@ -50,7 +58,7 @@ struct rcs_state {
     double* misc = nullptr;         // small device results
     float2* staging = nullptr;
     uint64_t staging_elems = 0;
-    // library-owned device buffers
+    // the context's chunk buffers (set by ensure_buffers)
     unsigned long long* xbuf = nullptr;  // shot / bitstring chunk
     double* dbuf = nullptr;              // uniforms / probabilities chunk
     double* xeb_part = nullptr;
@@ -173,6 +181,44 @@ rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs
         *bytes_sent += e * 8ull * np;
     }
     return RCS_OK;
+}
+
+// Tensor-core items of a plan (6-qubit blocks; 5-qubit blocks padded to 6 with the identity on
+// one more local qubit as the highest matrix bit: same arithmetic for every choice of it).
+void make_tc_pack(const Plan& P, int nl, TcPack& out) {
+    out.slot.assign(P.items.size(), -1);
+    out.pos.assign(P.items.size(), std::array<int, 6>{});
+    out.n_tc = 0;
+    for (size_t ii = 0; ii < P.items.size(); ii++) {
+        const Item& it = P.items[ii];
+        if (it.type != RCS_ITEM_PASS || nl < kTcMinLocal || it.k < 5) continue;
+        for (int i = 0; i < it.k; i++) out.pos[ii][i] = it.pos[i];
+        if (it.k == 5) {   // pad qubit: lowest of the pinned qubits 0..5 not in the block
+            int pad = -1;
+            for (int b = 0; b < kPinnedLow && pad < 0; b++) {
+                bool used = false;
+                for (int i = 0; i < 5; i++) used = used || it.pos[i] == b;
+                if (!used) pad = b;
+            }
+            out.pos[ii][5] = pad;
+        }
+        out.slot[ii] = out.n_tc++;
+    }
+    const size_t each = dev::tc_matrix_words();
+    out.words.assign((size_t)out.n_tc * each, 0u);
+    std::vector<cplx> padded(64 * 64);
+    for (size_t ii = 0; ii < P.items.size(); ii++) {
+        if (out.slot[ii] < 0) continue;
+        const Block& B = P.blocks[P.items[ii].block];
+        const cplx* m = B.matrix.data();
+        if (P.items[ii].k == 5) {
+            for (int r = 0; r < 64; r++)
+                for (int c = 0; c < 64; c++)
+                    padded[r * 64 + c] = ((r ^ c) & 32) ? cplx{0.0, 0.0} : B.matrix[(r & 31) * 32 + (c & 31)];
+            m = padded.data();
+        }
+        dev::tc_pack_matrix(reinterpret_cast<const double*>(m), out.words.data() + (size_t)out.slot[ii] * each);
+    }
 }
 
 // --- NVLink peer mapping -----------------------------------------------------------------
@@ -325,11 +371,18 @@ rcs_status compute_cdf(rcs_state* s, rcs_error* err) {
 
 rcs_status ensure_buffers(rcs_state* s, rcs_error* err) {
     if (s->xbuf) return RCS_OK;
+    rcs_context* c = s->ctx;
+    if (!c->xbuf) {   // allocated once per context: cudaMalloc/cudaFree per state would sync
+        CUDA_TRY(cudaMalloc(&c->xbuf, kChunkShots * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMalloc(&c->dbuf, kChunkShots * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&c->xeb_part, (size_t)dev::xeb_grid() * 3 * sizeof(double) + 64));
+        CUDA_TRY(cudaMalloc(&c->bad, sizeof(int)));
+    }
     s->chunk = kChunkShots;
-    CUDA_TRY(cudaMalloc(&s->xbuf, s->chunk * sizeof(unsigned long long)));
-    CUDA_TRY(cudaMalloc(&s->dbuf, s->chunk * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&s->xeb_part, (size_t)dev::xeb_grid() * 3 * sizeof(double) + 64));
-    CUDA_TRY(cudaMalloc(&s->bad, sizeof(int)));
+    s->xbuf = c->xbuf;
+    s->dbuf = c->dbuf;
+    s->xeb_part = c->xeb_part;
+    s->bad = c->bad;
     return RCS_OK;
 }
 
@@ -426,6 +479,8 @@ rcs_status rcs_circuit_load_qasm(const char* text, size_t len, rcs_circuit** out
     if (!c) { set_error(err, RCS_ERR_MEMORY, "out of host memory"); return RCS_ERR_MEMORY; }
     rcs_status st = parse_qasm(text, len, c->c, err);
     if (st != RCS_OK) { delete c; return st; }
+    static std::atomic<uint64_t> next_uid{1};
+    c->uid = next_uid.fetch_add(1);
     *out = c;
     return RCS_OK;
 }
@@ -561,8 +616,11 @@ void rcs_context_free(rcs_context* c) {
         if (c->peer_map[r]) cudaIpcCloseMemHandle(c->peer_map[r]);
     if (c->d_xchg) cudaFree(c->d_xchg);
     if (c->d_bar) cudaFree(c->d_bar);
+    if (c->xbuf) cudaFree(c->xbuf);
+    if (c->dbuf) cudaFree(c->dbuf);
+    if (c->xeb_part) cudaFree(c->xeb_part);
+    if (c->bad) cudaFree(c->bad);
     if (c->d_tc) cudaFree(c->d_tc);
-    if (c->h_tc) cudaFreeHost(c->h_tc);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -609,9 +667,24 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     CUDA_TRY(cudaSetDevice(ctx->device));
 
     auto t0 = std::chrono::steady_clock::now();
-    Plan P;
-    rcs_status st = build_plan(circ->c, o.fuse_k, plan_g, P, err);
-    if (st) return st;
+    std::shared_ptr<const Plan> plan_ptr;
+    {
+        rcs_circuit* cc = const_cast<rcs_circuit*>(circ);
+        std::lock_guard<std::mutex> lk(cc->mu);
+        auto key = std::make_pair(o.fuse_k, plan_g);
+        auto f = cc->plans.find(key);
+        if (f != cc->plans.end()) {
+            plan_ptr = f->second;
+        } else {
+            auto np = std::make_shared<Plan>();
+            rcs_status pst = build_plan(circ->c, o.fuse_k, plan_g, *np, err);
+            if (pst) return pst;
+            plan_ptr = np;
+            cc->plans[key] = plan_ptr;
+        }
+    }
+    const Plan& P = *plan_ptr;
+    rcs_status st = RCS_OK;
     auto t1 = std::chrono::steady_clock::now();
 
     rcs_state* s = new (std::nothrow) rcs_state();
@@ -655,62 +728,47 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         ev.resize(2 * P.items.size());
         for (auto& e : ev) BUILD_TRY(cudaEventCreate(&e));
     }
-    // tensor-core passes: A_hi/A_lo of every 6-qubit block, one H2D copy per build
-    // 5-qubit blocks run there too, padded to 6 with the identity on one more local qubit as
-    // the highest matrix bit (same arithmetic for every choice of that qubit)
-    std::vector<int> tc_slot(P.items.size(), -1);
-    std::vector<std::array<int, 6>> tc_pos(P.items.size());
-    int n_tc = 0;
-    for (size_t ii = 0; ii < P.items.size(); ii++) {
-        const Item& it = P.items[ii];
-        if (it.type != RCS_ITEM_PASS || nl < kTcMinLocal || it.k < 5) continue;
-        for (int i = 0; i < it.k; i++) tc_pos[ii][i] = it.pos[i];
-        if (it.k == 5) {
-            int pad = -1;
-            for (int b = 6; b < nl && pad < 0; b++) {
-                bool used = false;
-                for (int i = 0; i < 5; i++) used = used || it.pos[i] == b;
-                if (!used) pad = b;
-            }
-            tc_pos[ii][5] = pad;
+    // tensor-core passes: packed operands cached per (circuit, plan, n_local); the device copy
+    // lives in the context and is re-uploaded only when the circuit or plan changes
+    std::shared_ptr<const TcPack> tcp;
+    {
+        rcs_circuit* cc = const_cast<rcs_circuit*>(circ);
+        std::lock_guard<std::mutex> lk(cc->mu);
+        auto key = std::make_tuple(o.fuse_k, plan_g, nl);
+        auto f = cc->packs.find(key);
+        if (f != cc->packs.end()) {
+            tcp = f->second;
+        } else {
+            auto np = std::make_shared<TcPack>();
+            make_tc_pack(P, nl, *np);
+            tcp = np;
+            cc->packs[key] = tcp;
         }
-        tc_slot[ii] = n_tc++;
     }
+    const std::vector<int>& tc_slot = tcp->slot;
+    const int n_tc = tcp->n_tc;
     const size_t tc_words_each = dev::tc_matrix_words();
-    const size_t tc_floats = (size_t)n_tc * tc_words_each;
-    if (n_tc > 0) {
-        if (ctx->tc_cap < tc_floats) {
-            if (ctx->d_tc) cudaFree(ctx->d_tc);
-            if (ctx->h_tc) cudaFreeHost(ctx->h_tc);
-            ctx->d_tc = nullptr;
-            ctx->h_tc = nullptr;
-            ctx->tc_cap = 0;
-            BUILD_TRY(cudaMalloc(&ctx->d_tc, tc_floats * sizeof(uint32_t)));
-            BUILD_TRY(cudaMallocHost(&ctx->h_tc, tc_floats * sizeof(uint32_t)));
-            ctx->tc_cap = tc_floats;
-        }
-        BUILD_TRY(cudaStreamSynchronize(stream));   // previous build may still read h_tc
-        std::vector<cplx> padded(64 * 64);
-        for (size_t ii = 0; ii < P.items.size(); ii++) {
-            if (tc_slot[ii] < 0) continue;
-            const Block& B = P.blocks[P.items[ii].block];
-            const cplx* m = B.matrix.data();
-            if (P.items[ii].k == 5) {   // U (x) I with the pad qubit as matrix bit 5
-                for (int r = 0; r < 64; r++)
-                    for (int c = 0; c < 64; c++)
-                        padded[r * 64 + c] = ((r ^ c) & 32) ? cplx{0.0, 0.0} : B.matrix[(r & 31) * 32 + (c & 31)];
-                m = padded.data();
-            }
-            dev::tc_pack_matrix(reinterpret_cast<const double*>(m), ctx->h_tc + (size_t)tc_slot[ii] * tc_words_each);
-        }
+    const size_t tc_words = (size_t)n_tc * tc_words_each;
+    const bool tc_upload = n_tc > 0 && !(ctx->tc_uid == circ->uid && ctx->tc_pack == tcp.get());
+    if (tc_upload && ctx->tc_cap < tc_words) {
+        if (ctx->d_tc) cudaFree(ctx->d_tc);
+        ctx->d_tc = nullptr;
+        ctx->tc_cap = 0;
+        BUILD_TRY(cudaMalloc(&ctx->d_tc, tc_words * sizeof(uint32_t)));
+        ctx->tc_cap = tc_words;
     }
     if (ctx->world > 1 && P.n_remaps > 0) {
         rcs_status r = setup_peers(ctx, s->amps, err);
         if (r) return fail(r);
     }
     BUILD_TRY(cudaEventRecord(eb0, stream));
-    if (n_tc > 0)
-        BUILD_TRY(cudaMemcpyAsync(ctx->d_tc, ctx->h_tc, tc_floats * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    if (tc_upload) {
+        BUILD_TRY(cudaMemcpyAsync(ctx->d_tc, tcp->words.data(), tc_words * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                  stream));
+        ctx->tc_uid = circ->uid;
+        ctx->tc_pack = tcp.get();
+        ctx->tc_hold = tcp;
+    }
     BUILD_TRY(dev::init_basis(s->amps, n_amps, ctx->rank == 0, stream));
     uint64_t pass_bytes = 0, remap_bytes = 0;
     std::vector<float> mbuf;
@@ -718,7 +776,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         const Item& it = P.items[ii];
         if (o.timing) BUILD_TRY(cudaEventRecord(ev[2 * ii], stream));
         if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
-            BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tc_pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
+            BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tcp->pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
                                         ctx->num_sms, stream));
             pass_bytes += 16ull * n_amps;
         } else if (it.type == RCS_ITEM_PASS) {
@@ -916,10 +974,7 @@ rcs_status rcs_xeb(const rcs_state* s_, const uint64_t* x, uint64_t count, rcs_x
 void rcs_state_free(rcs_state* s) {
     if (!s) return;
     if (s->ctx) cudaSetDevice(s->ctx->device);
-    if (s->xbuf) cudaFree(s->xbuf);
-    if (s->dbuf) cudaFree(s->dbuf);
-    if (s->xeb_part) cudaFree(s->xeb_part);
-    if (s->bad) cudaFree(s->bad);
+    // chunk buffers belong to the context
     delete s;
 }
 

@@ -1,7 +1,12 @@
 // internal.h -- host-side data structures shared by the library's translation units.
 #pragma once
 
+#include <array>
 #include <cstdint>
+#include <map>
+#include <tuple>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -53,11 +58,17 @@ struct Plan {
     int n_passes = 0, n_remaps = 0, n_swaps = 0;
 };
 
-// low physical positions never moved by remaps (keeps qubit 0 at bit 0 for the
-// 128-bit pair loads of the gate-pass kernel and keeps short runs contiguous)
-constexpr int kPinnedLow = 3;
+// low physical positions never moved by remaps: keeps qubit 0 at bit 0 (the CUDA-core pass
+// moves amplitude pairs along bit 0) and makes qubits 0..5 always local, so a 5-qubit block
+// can be padded onto the tensor-core pass with one of them whatever the sharding (the
+// padded arithmetic depends on which qubit pads it: the choice must be layout-independent)
+constexpr int kPinnedLow = 6;
 // the tensor-core pass tiles 6 target + 6 column bits
 constexpr int kTcMinLocal = 12;
+// fuser: ready gates tried as block seeds besides the earliest unassigned one
+constexpr int kFuseSeeds = 4;
+// fuser: pick among the seeds by the block count of a greedy completion (rollout)
+constexpr bool kFuseLookahead = true;
 
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err);
 
@@ -65,8 +76,24 @@ void set_error(rcs_error* err, int code, const char* fmt, ...);
 
 }  // namespace rcs
 
+namespace rcs {
+// tensor-core pass operands of a plan: which items run on K9, their 6 positions (5-qubit blocks
+// padded with one more local qubit) and the packed fp16 hi/lo matrices (host copy)
+struct TcPack {
+    std::vector<int> slot;                 // per item, -1 if not a tensor-core pass
+    std::vector<std::array<int, 6>> pos;
+    std::vector<uint32_t> words;           // n_tc * tc_matrix_words()
+    int n_tc = 0;
+};
+}  // namespace rcs
+
 struct rcs_circuit {
     rcs::Circuit c;
+    uint64_t uid = 0;   // unique per parsed circuit (device-side caches key on it)
+    // plans are a pure function of (circuit, fuse_k, n_global): cached, shared read-only
+    std::mutex mu;
+    std::map<std::pair<int, int>, std::shared_ptr<const rcs::Plan>> plans;
+    std::map<std::tuple<int, int, int>, std::shared_ptr<const rcs::TcPack>> packs;
 };
 
 struct rcs_plan {

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -36,6 +37,8 @@ struct Fuser {
     std::vector<std::vector<int>> per_q;   // gate ids per qubit, source order
     std::vector<int> head;                 // first unassigned position in per_q[q]
     std::vector<char> assigned;
+
+    int seeds = 0;
 
     Fuser(const Circuit& c, int k_) : C(c), k(k_) {
         per_q.assign(c.n, {});
@@ -88,15 +91,12 @@ struct Fuser {
         return r;
     }
 
-    bool next_block(Block& B) {
-        int g0 = -1;
-        for (int i = 0; i < (int)assigned.size(); i++)
-            if (!assigned[i]) { g0 = i; break; }
-        if (g0 < 0) return false;
-        std::vector<int> S;
+    // greedy growth of a block seeded by ready gate g0 (qubit set S, absorbed gates cur)
+    void grow(int g0, std::vector<int>& S, std::vector<int>& cur) const {
+        S.clear();
         for (int j = 0; j < nq(g0); j++) S.push_back(qb(g0, j));
         std::sort(S.begin(), S.end());
-        std::vector<int> cur = closure(S);
+        cur = closure(S);
         while ((int)S.size() < k) {
             // candidate extensions: qubits of gates at the heads reachable after the closure
             std::map<int, int> h;
@@ -156,6 +156,66 @@ struct Fuser {
             S = merged(S, best_ext);
             cur = best_cl;
         }
+    }
+
+    bool ready(int g) const {
+        for (int j = 0; j < nq(g); j++) {
+            const int q = qb(g, j);
+            if (head[q] >= (int)per_q[q].size() || per_q[q][head[q]] != g) return false;
+        }
+        return true;
+    }
+
+    void commit(const std::vector<int>& cur) {
+        for (int g : cur) {
+            assigned[g] = 1;
+            for (int j = 0; j < nq(g); j++) head[qb(g, j)]++;
+        }
+    }
+
+    // number of blocks the plain greedy (earliest-gate seed) needs from the current state
+    int rollout() const {
+        Fuser f = *this;
+        f.seeds = 0;
+        f.lookahead = false;
+        int n = 0;
+        Block b;
+        while (f.next_block(b)) n++;
+        return n;
+    }
+
+    bool lookahead = false;
+
+    // next block: grow from the earliest unassigned gate and from up to `seeds` other ready
+    // gates; keep the block absorbing the most gate-qubits (2q gates count double), or with
+    // `lookahead`, the one whose greedy completion needs the fewest blocks
+    bool next_block(Block& B) {
+        int g0 = -1;
+        for (int i = 0; i < (int)assigned.size(); i++)
+            if (!assigned[i]) { g0 = i; break; }
+        if (g0 < 0) return false;
+        std::vector<int> cand{g0};
+        for (int i = g0 + 1; i < (int)assigned.size() && (int)cand.size() < 1 + seeds; i++)
+            if (!assigned[i] && ready(i)) cand.push_back(i);
+        std::vector<int> S, cur, bS, bcur;
+        long best = LONG_MIN;
+        for (int g : cand) {
+            grow(g, S, cur);
+            long score = 0;
+            for (int x : cur) score += nq(x);
+            if (lookahead && cand.size() > 1) {
+                Fuser f = *this;
+                f.commit(cur);
+                score = -1000L * f.rollout() + score;   // fewest remaining blocks, then most gates now
+            }
+            if (score > best) {
+                best = score;
+                bS = S;
+                bcur = cur;
+            }
+        }
+        S = bS;
+        cur = bcur;
         // commit
         B.qubits = S;
         B.gate_ids = cur;
@@ -233,6 +293,8 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
 
     // ---- 1. fusion
     Fuser F(c, k);
+    F.seeds = getenv("RCS_FUSE_SEEDS") ? atoi(getenv("RCS_FUSE_SEEDS")) : kFuseSeeds;
+    F.lookahead = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
     Block B;
     while (F.next_block(B)) {
         const int kb = (int)B.qubits.size();

@@ -105,12 +105,12 @@ def test_plan_executor_matches_oracle_random(rcs, seed, k):
 
 
 @pytest.mark.parametrize("g", [1, 2, 3])
-@pytest.mark.parametrize("grid", [(3, 4, 14, "EFGH"), (2, 5, 20, "ABCDCDAB"), (3, 3, 12, "ABCD")])
+@pytest.mark.parametrize("grid", [(3, 4, 14, "EFGH"), (2, 6, 20, "ABCDCDAB"), (3, 5, 12, "ABCD")])
 def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
     rows, cols, cyc, pat = grid
     n = rows * cols
-    if n - g - 3 < 4:
-        pytest.skip("too few local qubits")
+    if n - g - 6 < 4:
+        pytest.skip("too few movable local qubits (positions 0..5 are pinned)")
     text = emit_qasm(generate(rows, cols, cyc, pat, seed=g))
     ref = oracle.build_state(text)
     c = rcs.Circuit.from_qasm(text)
@@ -121,9 +121,9 @@ def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
         if it["type"] == "pass":
             assert max(it["pos"]) < nl                          # blocks only touch local bits
         elif it["type"] == "remap":
-            assert all(a >= nl for a in it["a"]) and all(3 <= b < nl for b in it["b"])
+            assert all(a >= nl for a in it["a"]) and all(6 <= b < nl for b in it["b"])
         else:
-            assert all(3 <= a < nl and 3 <= b < nl for a, b in zip(it["a"], it["b"]))
+            assert all(6 <= a < nl and 6 <= b < nl for a, b in zip(it["a"], it["b"]))
     # the fusion is independent of the number of global qubits (P-invariance)
     p0 = rcs.Plan(c, 6 if n - g >= 12 else 4, 0)
     b0 = [i for i in p0.items() if i["type"] == "pass"]
@@ -140,7 +140,7 @@ def test_plan_rejects_bad_arguments(rcs):
     with pytest.raises(rcs.RcsError):
         rcs.Plan(c, 7, 0)
     with pytest.raises(rcs.RcsError):
-        rcs.Plan(c, 4, 9)   # 12 - 9 - 3 < 4 movable local qubits
+        rcs.Plan(c, 4, 3)   # 12 - 3 - 6 < 4 movable local qubits
 
 
 def test_pass_counts_reported(rcs):
