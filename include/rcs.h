@@ -91,13 +91,18 @@ typedef struct {
     double build_ms;         /* device: init .. final norm, CUDA events on the context stream    */
     double pass_ms;          /* timing=1: sum of gate-pass kernel times                          */
     double pass_ms_min, pass_ms_max;
-    double remap_ms;         /* timing=1: sum of remap times (NVLink peer swap, or NCCL fallback)  */
+    double remap_ms;         /* timing=1: sum of remap times (NVLink peer swap, or NCCL fallback);
+                                for pipelined remaps the time not hidden behind pass chunks    */
     double blocksum_ms;      /* timing=1: block-sum + scan (sampling CDF) time                   */
     uint64_t pass_bytes;     /* algorithmic bytes of all gate passes on this rank (16 B/amp/pass) */
     uint64_t remap_bytes;    /* bytes this rank sent over NCCL                                   */
     double norm;             /* sum |psi|^2 over all ranks                                       */
     int n_tc_passes;         /* of n_passes, 6-qubit passes run on the tensor cores (K9)          */
     double swap_ms;          /* timing=1: sum of local bit-swap (layout restore) pass times       */
+    int n_pipelined;         /* remaps run as chunked NVLink swaps overlapped with the adjacent
+                                tensor-core passes; env RCS_OVERLAP=0 disables,
+                                RCS_OVERLAP_CHUNKS = log2 chunks (default 2), RCS_OVERLAP_SMS =
+                                SMs left to the swaps (default 16)                              */
 } rcs_build_report;
 
 typedef struct {

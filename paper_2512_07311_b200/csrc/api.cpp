@@ -37,6 +37,9 @@ struct rcs_context {
     uint64_t peer_off[8] = {0};
     void* peer_map[8] = {nullptr};
     float* d_bar = nullptr;           // 1-float all-reduce used as a stream-ordered barrier
+    // pipelined remaps (f1): a second stream for the chunked peer swaps + per-chunk events
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t ev_a[16] = {}, ev_s[16] = {};
     // sampling / XEB chunk buffers, shared by every state of this context
     unsigned long long* xbuf = nullptr;
     double* dbuf = nullptr;
@@ -288,28 +291,32 @@ rcs_status setup_peers(rcs_context* c, void* amps, rcs_error* err) {
 }
 
 // stream-ordered barrier over all ranks (no rank proceeds past it before every rank reached it)
-rcs_status stream_barrier(rcs_context* c, rcs_error* err) {
-    NCCL_TRY(ncclAllReduce(c->d_bar, c->d_bar, 1, ncclFloat, ncclSum, c->comm, c->stream));
+rcs_status stream_barrier(rcs_context* c, cudaStream_t st, rcs_error* err) {
+    NCCL_TRY(ncclAllReduce(c->d_bar, c->d_bar, 1, ncclFloat, ncclSum, c->comm, st));
     return RCS_OK;
 }
 
-// Remap over NVLink: swap the exchanged halves in place, local <-> peer (CUDA-IPC mapping);
-// every unordered rank pair splits its element pairs in two halves, one per rank.
-rcs_status do_remap_p2p(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_error* err) {
+// Peer-swap arguments for one REMAP item: every unordered rank pair splits its element pairs
+// in two halves, one per rank.  fix/nfix/fixval restrict it to one chunk of the index space.
+void make_swap_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint64_t fixval, dev::PeerSwapArgs& A,
+                    uint64_t* bytes_sent) {
     rcs_context* c = s->ctx;
     const int j = it.k, nl = s->nl;
-    dev::PeerSwapArgs A{};
+    A = dev::PeerSwapArgs{};
     A.local = s->amps;
     A.j = j;
     int lpos[8];
     for (int i = 0; i < j; i++) lpos[i] = it.b[i];
     std::sort(lpos, lpos + j);
     for (int i = 0; i < j; i++) A.lpos[i] = lpos[i];
+    A.nfix = nfix;
+    for (int i = 0; i < nfix; i++) A.fix[i] = fix[i];
+    A.fixval = fixval;
     int my_code = 0;
     for (int i = 0; i < j; i++) my_code |= ((c->rank >> (it.a[i] - nl)) & 1) << i;
     for (int i = 0; i < j; i++)
         if ((my_code >> i) & 1) A.my_mask |= 1ull << it.b[i];
-    const uint64_t count = 1ull << (nl - j);
+    const uint64_t count = 1ull << (nl - j - nfix);
     for (int code = 0; code < (1 << j); code++) {
         if (code == my_code) continue;
         int peer = c->rank;
@@ -327,10 +334,108 @@ rcs_status do_remap_p2p(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_
         A.m_count[pc] = c->rank < peer ? half : count - half;
         *bytes_sent += count * 8ull;
     }
-    rcs_status st = stream_barrier(c, err);
+}
+
+// Remap over NVLink: swap the exchanged halves in place, local <-> peer (CUDA-IPC mapping).
+rcs_status do_remap_p2p(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_error* err) {
+    rcs_context* c = s->ctx;
+    dev::PeerSwapArgs A;
+    make_swap_args(s, it, nullptr, 0, 0, A, bytes_sent);
+    rcs_status st = stream_barrier(c, c->stream, err);
     if (st) return st;
     CUDA_TRY(dev::peer_swap(A, c->stream));
-    return stream_barrier(c, err);
+    return stream_barrier(c, c->stream, err);
+}
+
+// Pipelined remap: [pass A] -> REMAP -> [pass B] in 2^cb chunks of the index
+// space (cb fixed "chunk" bits, untouched by A, the remap and B).  Pass chunks run on the
+// context stream on (num_sms - reserve) SMs; the peer swap of chunk c runs on xstream as soon
+// as every rank finished A on chunk c (barrier), and B on chunk c starts once every rank
+// finished swapping it (barrier).  Arithmetic per amplitude is unchanged (bitwise equal).
+struct PassRef {
+    const int* pos;
+    const uint32_t* d_a;
+};
+struct Span {   // timing: item time += sign * elapsed(a, b)
+    size_t item;
+    cudaEvent_t a, b;
+    int sign;
+};
+
+rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, const PassRef* pb, const int* fix,
+                              int cb, int reserve, uint64_t* bytes_sent, uint64_t* pass_bytes, size_t ia, size_t ir,
+                              size_t ib, std::vector<Span>* spans, std::vector<cudaEvent_t>* owned, rcs_error* err) {
+    rcs_context* c = s->ctx;
+    const int nch = 1 << cb;
+    if (!c->xstream) CUDA_TRY(cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
+    for (int i = 0; i < nch; i++) {
+        if (!c->ev_a[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_a[i], cudaEventDisableTiming));
+        if (!c->ev_s[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_s[i], cudaEventDisableTiming));
+    }
+    auto tev = [&](cudaStream_t st) -> cudaEvent_t {   // timing event (only when spans requested)
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        owned->push_back(e);
+        cudaEventRecord(e, st);
+        return e;
+    };
+    auto fixval = [&](int ch) {
+        uint64_t v = 0;
+        for (int i = 0; i < cb; i++)
+            if ((ch >> i) & 1) v |= 1ull << fix[i];
+        return v;
+    };
+    const int sms = std::max(1, c->num_sms - reserve);
+    cudaEvent_t t0 = spans ? tev(c->stream) : nullptr;
+    // A: all chunks, in order, on the main stream
+    for (int ch = 0; ch < nch; ch++) {
+        if (pa) {
+            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch)));
+        }
+        CUDA_TRY(cudaEventRecord(c->ev_a[ch], c->stream));
+    }
+    if (pa) *pass_bytes += 16ull * s->n_amps;
+    cudaEvent_t tA = spans ? tev(c->stream) : nullptr;
+    if (spans && pa) spans->push_back({ia, t0, tA, 1});
+    // swaps: chunk by chunk on xstream
+    for (int ch = 0; ch < nch; ch++) {
+        dev::PeerSwapArgs A;
+        make_swap_args(s, it, fix, cb, fixval(ch), A, bytes_sent);
+        A.max_grid = reserve * 8;
+        CUDA_TRY(cudaStreamWaitEvent(c->xstream, c->ev_a[ch], 0));
+        rcs_status st = stream_barrier(c, c->xstream, err);
+        if (st) return st;
+        CUDA_TRY(dev::peer_swap(A, c->xstream));
+        st = stream_barrier(c, c->xstream, err);
+        if (st) return st;
+        CUDA_TRY(cudaEventRecord(c->ev_s[ch], c->xstream));
+    }
+    // B: chunk c after every rank swapped chunk c
+    for (int ch = 0; ch < nch; ch++) {
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
+        if (pb) {
+            cudaEvent_t w = spans ? tev(c->stream) : nullptr;
+            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pb->pos, pb->d_a, sms, c->stream, fix, cb, fixval(ch)));
+            if (spans) {
+                cudaEvent_t d = tev(c->stream);
+                spans->push_back({ib, w, d, 1});
+                spans->push_back({ir, w, d, -1});
+            }
+        }
+    }
+    if (pb) *pass_bytes += 16ull * s->n_amps;
+    if (spans) spans->push_back({ir, tA, tev(c->stream), 1});
+    return RCS_OK;
+}
+
+// chunk bits for a pipelined remap: the highest positions outside `excl`; false if too few
+bool choose_chunk_bits(int nl, uint64_t excl, int cb, int* fix) {
+    int got = 0;
+    for (int b = nl - 1; b >= kPinnedLow && got < cb; b--)
+        if (!((excl >> b) & 1)) fix[got++] = b;
+    if (got < cb) return false;
+    std::sort(fix, fix + cb);
+    return true;
 }
 
 // block sums + scan + shard totals (collective); fills s->T_*, E_r, sum_sq, ownership
@@ -621,6 +726,11 @@ void rcs_context_free(rcs_context* c) {
     if (c->xeb_part) cudaFree(c->xeb_part);
     if (c->bad) cudaFree(c->bad);
     if (c->d_tc) cudaFree(c->d_tc);
+    for (int i = 0; i < 16; i++) {
+        if (c->ev_a[i]) cudaEventDestroy(c->ev_a[i]);
+        if (c->ev_s[i]) cudaEventDestroy(c->ev_s[i]);
+    }
+    if (c->xstream) cudaStreamDestroy(c->xstream);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -723,11 +833,6 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     BUILD_TRY(cudaEventCreate(&eb0));
     BUILD_TRY(cudaEventCreate(&eb1));
     BUILD_TRY(cudaEventCreate(&ec0));
-    std::vector<cudaEvent_t> ev;
-    if (o.timing) {
-        ev.resize(2 * P.items.size());
-        for (auto& e : ev) BUILD_TRY(cudaEventCreate(&e));
-    }
     // tensor-core passes: packed operands cached per (circuit, plan, n_local); the device copy
     // lives in the context and is re-uploaded only when the circuit or plan changes
     std::shared_ptr<const TcPack> tcp;
@@ -771,10 +876,50 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     }
     BUILD_TRY(dev::init_basis(s->amps, n_amps, ctx->rank == 0, stream));
     uint64_t pass_bytes = 0, remap_bytes = 0;
+    int n_pipelined = 0;
     std::vector<float> mbuf;
+    std::vector<Span> spans;
+    std::vector<cudaEvent_t> owned;
+    // pipelined remaps (f1): on unless RCS_OVERLAP=0; 2^cb chunks, `reserve` SMs left to the swaps
+    static const int ov_on = getenv("RCS_OVERLAP") ? atoi(getenv("RCS_OVERLAP")) : 1;
+    static const int ov_cb = getenv("RCS_OVERLAP_CHUNKS") ? atoi(getenv("RCS_OVERLAP_CHUNKS")) : 2;
+    static const int ov_res = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 16;
+    auto is_tc = [&](size_t i) { return i < P.items.size() && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
+    auto tc_ref = [&](size_t i) {
+        return PassRef{tcp->pos[i].data(), ctx->d_tc + (size_t)tc_slot[i] * tc_words_each};
+    };
     for (size_t ii = 0; ii < P.items.size(); ii++) {
         const Item& it = P.items[ii];
-        if (o.timing) BUILD_TRY(cudaEventRecord(ev[2 * ii], stream));
+        // [TC pass] -> REMAP -> [TC pass] pipelined over NVLink
+        if (ov_on && ctx->world > 1 && ctx->p2p && ov_cb >= 1 && ov_cb <= 4) {
+            size_t ir = (it.type == RCS_ITEM_REMAP) ? ii : (is_tc(ii) && ii + 1 < P.items.size() &&
+                                                            P.items[ii + 1].type == RCS_ITEM_REMAP) ? ii + 1 : SIZE_MAX;
+            if (ir != SIZE_MAX) {
+                const Item& rm = P.items[ir];
+                const bool has_a = ir != ii, has_b = is_tc(ir + 1);
+                uint64_t excl = 0;
+                for (int i = 0; i < rm.k; i++) excl |= 1ull << rm.b[i];
+                if (has_a) excl |= dev::tc_reserved_mask(nl, tcp->pos[ii].data());
+                if (has_b) excl |= dev::tc_reserved_mask(nl, tcp->pos[ir + 1].data());
+                int fix[4];
+                if ((has_a || has_b) && choose_chunk_bits(nl, excl, ov_cb, fix)) {
+                    PassRef ra = has_a ? tc_ref(ii) : PassRef{}, rb = has_b ? tc_ref(ir + 1) : PassRef{};
+                    rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, has_b ? &rb : nullptr, fix, ov_cb,
+                                                      ov_res, &remap_bytes, &pass_bytes, ii, ir, ir + 1,
+                                                      o.timing ? &spans : nullptr, &owned, err);
+                    if (r) return fail(r);
+                    n_pipelined++;
+                    ii = has_b ? ir + 1 : ir;
+                    continue;
+                }
+            }
+        }
+        cudaEvent_t e0 = nullptr;
+        if (o.timing) {
+            BUILD_TRY(cudaEventCreate(&e0));
+            owned.push_back(e0);
+            BUILD_TRY(cudaEventRecord(e0, stream));
+        }
         if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
             BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tcp->pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
                                         ctx->num_sms, stream));
@@ -799,7 +944,13 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
                 if (r) return fail(r);
             }
         }
-        if (o.timing) BUILD_TRY(cudaEventRecord(ev[2 * ii + 1], stream));
+        if (o.timing) {
+            cudaEvent_t e1;
+            BUILD_TRY(cudaEventCreate(&e1));
+            owned.push_back(e1);
+            BUILD_TRY(cudaEventRecord(e1, stream));
+            spans.push_back({ii, e0, e1, 1});
+        }
     }
     BUILD_TRY(cudaEventRecord(ec0, stream));
     st = compute_cdf(s, err);
@@ -823,22 +974,27 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     s->pass_ms.clear();
     if (o.timing) {
         R.blocksum_ms = cdf_ms;
-        for (size_t ii = 0; ii < P.items.size(); ii++) {
+        std::vector<double> item_ms(P.items.size(), 0.0);
+        for (const Span& sp : spans) {
             float t = 0.f;
-            cudaEventElapsedTime(&t, ev[2 * ii], ev[2 * ii + 1]);
+            if (sp.a && sp.b) cudaEventElapsedTime(&t, sp.a, sp.b);
+            item_ms[sp.item] += sp.sign * (double)t;
+        }
+        for (size_t ii = 0; ii < P.items.size(); ii++) {
+            const double t = item_ms[ii];
             if (P.items[ii].type == RCS_ITEM_PASS) {
                 R.pass_ms += t;
-                R.pass_ms_min = std::min(R.pass_ms_min, (double)t);
-                R.pass_ms_max = std::max(R.pass_ms_max, (double)t);
-                s->pass_ms.push_back(t);
+                R.pass_ms_min = std::min(R.pass_ms_min, t);
+                R.pass_ms_max = std::max(R.pass_ms_max, t);
+                s->pass_ms.push_back((float)t);
             } else if (P.items[ii].type == RCS_ITEM_SWAP) {
                 R.swap_ms += t;
             } else {
                 R.remap_ms += t;
             }
         }
-        for (auto& e : ev) cudaEventDestroy(e);
     }
+    for (auto& e : owned) cudaEventDestroy(e);
     if (R.pass_ms_min > R.pass_ms_max) R.pass_ms_min = 0;
     cudaEventDestroy(eb0);
     cudaEventDestroy(eb1);
@@ -847,6 +1003,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     R.remap_bytes = remap_bytes;
     R.norm = s->T_total;
     R.n_tc_passes = n_tc;
+    R.n_pipelined = n_pipelined;
     if (rep) *rep = R;
     *out = s;
     return RCS_OK;

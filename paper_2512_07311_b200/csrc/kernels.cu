@@ -244,7 +244,11 @@ __global__ void __launch_bounds__(kThreads) k_peer_swap(const __grid_constant__ 
             const uint64_t v = v0 + (uint64_t)u * kThreads;
             ok[u] = v < nvec;
             uint64_t m = a.m_begin[pc] + 2 * v;
-            for (int i = 0; i < a.j; i++) m = insert_zero(m, a.lpos[i]);
+            for (int i = 0, f = 0; i < a.j || f < a.nfix;) {   // lpos and fix merged, ascending
+                if (f >= a.nfix || (i < a.j && a.lpos[i] < a.fix[f])) m = insert_zero(m, a.lpos[i++]);
+                else m = insert_zero(m, a.fix[f++]);
+            }
+            m |= a.fixval;
             li[u] = (m | a.mask[pc]) >> 1;
             ri[u] = (m | a.my_mask) >> 1;
             if (ok[u]) {
@@ -577,7 +581,8 @@ cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st) {
     for (int i = 0; i < a.npeers; i++) maxv = a.m_count[i] / 2 > maxv ? a.m_count[i] / 2 : maxv;
     if (maxv == 0) return cudaSuccess;
     uint64_t gx = (maxv + (uint64_t)kThreads * kSwapU - 1) / ((uint64_t)kThreads * kSwapU);
-    if (gx > 148u * 8u) gx = 148u * 8u;
+    const uint64_t cap = a.max_grid > 0 ? (uint64_t)a.max_grid : 148u * 8u;
+    if (gx > cap) gx = cap;
     note_launch();
     k_peer_swap<<<dim3((unsigned)gx, (unsigned)a.npeers), kThreads, 0, st>>>(a);
     return cudaGetLastError();

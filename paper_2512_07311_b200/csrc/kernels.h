@@ -17,8 +17,13 @@ void count_launch();
 // embedding, scaled by 2^14).
 size_t tc_matrix_words();
 void tc_pack_matrix(const double* u_re_im, uint32_t* out);
+// Optional chunking (pipelined remaps): fix[0..nfix) are extra positions held at the bits of
+// fixval, so the launch covers one 2^-nfix slice of the index space.  Fixed positions must lie
+// outside tc_reserved_mask(pos); the grid is min(num_sms, tiles).
 cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const uint32_t* d_a, int num_sms,
-                         cudaStream_t st);
+                         cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0);
+// positions a chunk bit must avoid for this pass: the 12-bit tile sub-cube and the bit above its run
+uint64_t tc_reserved_mask(int n_local_bits, const int* pos);
 
 // a6 (K1) fused dense gate pass: amps <- M (x) over every group of 2^k amplitudes that
 // differ only in the physical bits pos[0..k) (matrix bit i <-> pos[i]); M is 2^k x 2^k
@@ -48,7 +53,11 @@ struct PeerSwapArgs {
     int lpos[8];
     uint64_t mask[7];
     uint64_t my_mask;
-    uint64_t m_begin[7], m_count[7];
+    uint64_t m_begin[7], m_count[7];   // element-pair range of this rank, per peer
+    int nfix;                          // chunking: extra fixed positions (ascending) ...
+    int fix[4];
+    uint64_t fixval;                   // ... and their bits
+    int max_grid;                      // 0: default
 };
 cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st);
 

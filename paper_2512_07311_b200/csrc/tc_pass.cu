@@ -77,6 +77,11 @@ struct TcArgs {
     int pair;                // 2: tiles processed in adjacent pairs (ntiles >= 2), else 1
     int sso[32];             // staging offset (floats) of sub-cube index 128 i
     uint64_t sgo[32];        // global offset (amplitudes) of sub-cube index 128 i
+    int nins;                // 12 + number of fixed (chunk) bits
+    int ins[16];             // sub-cube and fixed positions, ascending (tile base deposit)
+    uint64_t fixval;         // value of the fixed bits (one chunk of the index space)
+    uint64_t fmask;          // positions the tile index is deposited into (below n_local)
+    uint64_t dstride;        // deposit of the per-CTA tile-pair stride (gridDim.x * pair)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -130,8 +135,22 @@ __device__ __forceinline__ void rot_h8(uint32_t (&w)[4], int rho) {
     for (int i = 0; i < 4; i++) w[i] = (rho & 1) ? a[i] : w[i];
 }
 
-__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
-    return (uint32_t)__half_as_ushort(__float2half_rn(a)) | ((uint32_t)__half_as_ushort(__float2half_rn(b)) << 16);
+// (x0, x1) -> hi = fp16x2(x0, x1) (x0 in the low half), lo = fp16x2(x - f32(hi)): one packed
+// convert each, two widening converts and two FADDs (x0, x1 already scaled)
+__device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
+    const __half2 h = *reinterpret_cast<const __half2*>(&hi);
+    const float r0 = x0 - __low2float(h), r1 = x1 - __high2float(h);
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r1), "f"(r0));
+}
+
+__device__ __forceinline__ float2 f2mul(float2 v, float s) {   // packed f32x2 multiply
+    float2 o;
+    asm("{\n.reg .b64 x, y;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%4, %4};\nmul.rn.f32x2 x, x, y;\n"
+        "mov.b64 {%0, %1}, x;\n}"
+        : "=f"(o.x), "=f"(o.y)
+        : "f"(v.x), "f"(v.y), "f"(s));
+    return o;
 }
 
 #define TMEM_ST32(addr, R)                                                                                       \
@@ -274,27 +293,37 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
     asm volatile("tcgen05.fence::after_thread_sync;");
 
     const uint64_t ntiles = p.ntiles;
+    // tile base = deposit of the tile index into the free positions, | the fixed bits.  Each role
+    // walks pairs (2i, 2i+1), i = blockIdx.x + k gridDim.x, and advances the deposited base of the
+    // pair's even tile incrementally: pdep(x + y) = ((pdep(x) | ~M) + pdep(y)) & M.
     auto tile_base = [&](uint64_t tile) {
         uint64_t b = tile;
 #pragma unroll
-        for (int i = 0; i < 12; i++) b = ins0(b, p.sub[i]);
+        for (int i = 0; i < 16; i++)
+            if (i < p.nins) b = ins0(b, p.ins[i]);
         return b;
     };
-    // every role walks the same tile sequence: pairs (2i, 2i+1), i = blockIdx.x + k gridDim.x
     const uint64_t first_tile = (uint64_t)blockIdx.x * p.pair;
-    auto next_tile = [&](uint64_t t) -> uint64_t {
-        if (p.pair == 2 && !(t & 1)) return t + 1;
-        return t - (p.pair == 2 ? 1 : 0) + (uint64_t)gridDim.x * p.pair;
+    const uint64_t first_base = tile_base(first_tile);
+    const uint64_t rbit = 1ull << p.r;   // tile index bit 0 -> position r (first free position)
+    auto next_tile = [&](uint64_t& t, uint64_t& bp) {
+        if (p.pair == 2 && !(t & 1)) {
+            t += 1;
+            return;
+        }
+        t = t - (p.pair == 2 ? 1 : 0) + (uint64_t)gridDim.x * p.pair;
+        bp = ((bp | ~p.fmask) + p.dstride) & p.fmask;
     };
+    auto base_of = [&](uint64_t t, uint64_t bp) { return bp | ((p.pair == 2 && (t & 1)) ? rbit : 0) | p.fixval; };
 
     if (warp == kProdWarp) {
         // ---------------- TMA producer: both tiles of a pair, runs of 2 x 2^r amplitudes
         const int nruns = 1 << (12 - p.r);
         const uint32_t copy_bytes = (8u << p.r) * (uint32_t)p.pair;   // one run of each tile of the pair
         const uint32_t dst_stride = (8u << p.r) * 2;                  // same layout when pair == 1
-        uint64_t it = 0;
+        uint64_t it = 0, bp = first_base;
         for (uint64_t tile = first_tile; tile < ntiles; it++) {
-            if (p.pair == 2 && (tile & 1)) { tile = next_tile(tile); continue; }   // odd half: copied with its pair
+            if (p.pair == 2 && (tile & 1)) { next_tile(tile, bp); continue; }   // odd half: copied with its pair
             const int slot = (it >> (p.pair - 1)) & 1;
             const uint64_t use = it >> (p.pair);                   // uses of this slot before
             mbar_wait(&rempty[slot], (use & 1) ^ 1);
@@ -303,7 +332,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                              "r"(kRawBytes * p.pair)
                              : "memory");
             __syncwarp();
-            const float2* src = p.amps + tile_base(tile);
+            const float2* src = p.amps + base_of(tile, bp);
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
             for (int u = lane; u < nruns; u += 32)
                 asm volatile(
@@ -311,7 +340,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                         dst + u * dst_stride),
                     "l"(src + offr[u]), "r"(copy_bytes), "r"(su32(&rfull[slot]))
                     : "memory");
-            tile = next_tile(tile);
+            next_tile(tile, bp);
         }
     } else if (warp < kLoadWarps) {
         // ---------------- converters: thread = column j, target octets `to` and `to + 4`
@@ -320,18 +349,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         const int to = lt >> 6;               // 0..3
         const int sj = sofj[j];
         const int rho = ROT ? (lane & 7) : 0;
-        uint64_t it = 0;
-        for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
+        int boff[16];   // raw-slot element offsets of this thread's 16 amplitudes (tile-invariant)
+#pragma unroll
+        for (int i = 0; i < 16; i++) boff[i] = soft[8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj;
+        uint64_t it = 0, bp = first_base;
+        for (uint64_t tile = first_tile; tile < ntiles; next_tile(tile, bp), it++) {
             const int slot = (it >> (p.pair - 1)) & 1;
             const uint64_t use = it >> (p.pair);
             mbar_wait(&rfull[slot], use & 1);
             const float2* rb = raw + (size_t)slot * 8192 + ((p.pair == 2 && (tile & 1)) ? (1 << p.r) : 0);
             float2 b[16];
 #pragma unroll
-            for (int i = 0; i < 16; i++) b[i] = rb[soft[8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj];
+            for (int i = 0; i < 16; i++) b[i] = f2mul(rb[boff[i]], 32768.f);   // x 2^15 (fixed scale)
             mbar_arrive(&rempty[slot]);
             if (p.pair == 1) mbar_arrive(&rempty[slot]);   // count is for two tiles
-            const float sc = 32768.f;   // 2^15
             const int s = it % kStages;
             mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
             uint8_t* bhi = stages + s * kStageBytes;
@@ -341,19 +372,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                 uint32_t rh[4], rl[4], ih[4], il[4];
 #pragma unroll
                 for (int e2 = 0; e2 < 4; e2++) {
-                    float xr[2], xi[2], hr[2], hi2[2];
-#pragma unroll
-                    for (int u = 0; u < 2; u++) {
-                        const float2 v = b[8 * g + 2 * e2 + u];
-                        xr[u] = v.x * sc;
-                        xi[u] = v.y * sc;
-                        hr[u] = __half2float(__float2half_rn(xr[u]));
-                        hi2[u] = __half2float(__float2half_rn(xi[u]));
-                    }
-                    rh[e2] = pack_h2(hr[0], hr[1]);
-                    rl[e2] = pack_h2(xr[0] - hr[0], xr[1] - hr[1]);
-                    ih[e2] = pack_h2(hi2[0], hi2[1]);
-                    il[e2] = pack_h2(xi[0] - hi2[0], xi[1] - hi2[1]);
+                    const float2 v0 = b[8 * g + 2 * e2], v1 = b[8 * g + 2 * e2 + 1];
+                    split_h2(v0.x, v1.x, rh[e2], rl[e2]);
+                    split_h2(v0.y, v1.y, ih[e2], il[e2]);
                 }
                 if (ROT) {
                     rot_h8(rh, rho);
@@ -374,8 +395,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
     } else if (warp == kMmaWarp) {
         // ---------------- MMA issuer
         const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        uint64_t it = 0;
-        for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
+        uint64_t it = 0, bp = first_base;
+        for (uint64_t tile = first_tile; tile < ntiles; next_tile(tile, bp), it++) {
             const int s = it % kStages, d = it & 1;
             mbar_wait(&full[s], (it / kStages) & 1);
             mbar_wait(&tempty[d], ((it >> 1) & 1) ^ 1);
@@ -422,8 +443,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         decomp(et, tb, jb, gb);
         const float* sld = staging + tb * kPitchF + 2 * jb;
         float* st = staging + trow * kPitchF + comp;
-        uint64_t it = 0;
-        for (uint64_t tile = first_tile; tile < ntiles; tile = next_tile(tile), it++) {
+        uint64_t it = 0, bp = first_base;
+        for (uint64_t tile = first_tile; tile < ntiles; next_tile(tile, bp), it++) {
             const int d = it & 1;
             mbar_wait(&tfull[d], (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -455,7 +476,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            float2* dst = p.amps + (tile_base(tile) | gb);
+            float2* dst = p.amps + (base_of(tile, bp) | gb);
 #pragma unroll 8
             for (int i = 0; i < 32; i++) {
                 const float2 v = *reinterpret_cast<const float2*>(sld + p.sso[i]);
@@ -504,12 +525,28 @@ void tc_pack_matrix(const double* u_re_im /* 64x64 complex, row-major interleave
     }
 }
 
-cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st) {
-    if (nl < 12) return cudaErrorInvalidValue;
+uint64_t tc_reserved_mask(int nl, const int* pos) {
+    uint64_t tmask = 0;
+    for (int i = 0; i < 6; i++) tmask |= 1ull << pos[i];
+    uint64_t m = tmask;
+    int nj = 0, r = -1;
+    for (int b = 0; b < nl; b++) {
+        if ((tmask >> b) & 1) continue;
+        if (nj < 6) { m |= 1ull << b; nj++; continue; }
+        r = b;
+        break;
+    }
+    if (r >= 0) m |= 1ull << r;
+    return m;
+}
+
+cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
+                         const int* fix, int nfix, uint64_t fixval) {
+    if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
     p.amps = amps;
     p.a = d_a;
-    p.ntiles = 1ull << (nl - 12);
+    p.ntiles = 1ull << (nl - 12 - nfix);
     uint64_t tmask = 0;
     for (int i = 0; i < 6; i++) {
         p.pos[i] = pos[i];
@@ -530,6 +567,19 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
     for (int i = 0; i < 12; i++) p.sub[i] = all[i];
     p.r = 0;
     while (p.r < 12 && p.sub[p.r] == p.r) p.r++;   // >= 6: the 6 lowest non-targets are in the cube
+    // fixed (chunk) bits: outside the sub-cube and not the first non-cube bit (tile pairs)
+    uint64_t insmask = 0, fixmask = 0;
+    for (int i = 0; i < 12; i++) insmask |= 1ull << p.sub[i];
+    for (int i = 0; i < nfix; i++) {
+        if (fix[i] < 0 || fix[i] >= nl || fix[i] == p.r || ((insmask >> fix[i]) & 1)) return cudaErrorInvalidValue;
+        insmask |= 1ull << fix[i];
+        fixmask |= 1ull << fix[i];
+    }
+    if (fixval & ~fixmask) return cudaErrorInvalidValue;
+    p.fixval = fixval;
+    p.nins = 0;
+    for (int b = 0; b < nl; b++)
+        if ((insmask >> b) & 1) p.ins[p.nins++] = b;
     p.pair = p.ntiles >= 2 ? 2 : 1;                // tile bit 0 = index bit r (first non-cube bit)
     static const bool no_pair = getenv("RCS_TC_NOPAIR") != nullptr, no_rot = getenv("RCS_TC_NOROT") != nullptr;
     if (no_pair) p.pair = 1;
@@ -561,6 +611,17 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
     for (int i = 0; i < 4; i++) low_targets += (int)((tmask >> p.sub[i]) & 1);
     const uint64_t units = p.ntiles / p.pair;
     const uint64_t grid = units < (uint64_t)num_sms ? units : (uint64_t)num_sms;
+    if (grid == 0) return cudaSuccess;
+    p.fmask = ~insmask & ((nl >= 64) ? ~0ull : ((1ull << nl) - 1));
+    {   // pdep(grid * pair, fmask)
+        uint64_t v = grid * (uint64_t)p.pair, d = 0;
+        for (int b = 0; b < 64 && v; b++)
+            if ((p.fmask >> b) & 1) {
+                if (v & 1) d |= 1ull << b;
+                v >>= 1;
+            }
+        p.dstride = d;
+    }
     count_launch();
     if (low_targets >= 2 && !no_rot)
         k_pass_tc<true><<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);

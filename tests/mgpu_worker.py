@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     import paper_2512_07311_b200 as rcs
-    from rcs_workload import SHOT_SEED, config_qasm, emit_qasm, generate
+    from rcs_workload import SHOT_SEED
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -26,15 +26,11 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = rcs.Context.from_process_group(local)
     results = {}
-    cases = {
-        "c1": config_qasm("c1"),
-        "grid20": emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=3)),
-        "c2": config_qasm("c2"),
-    }
-    for name, text in cases.items():
+    from tests.test_multigpu import CASES
+    for name, (text, k) in CASES.items():
         c = rcs.Circuit.from_qasm(text)
         n = c.n_qubits
-        st = rcs.State.build(ctx, c, fuse_k=4, timing=True, staging_bytes=1 << 20)
+        st = rcs.State.build(ctx, c, fuse_k=k, timing=True, staging_bytes=1 << 20)
         shard = torch.from_numpy(st.copy_out().view(np.float32).copy()).cuda()
         parts = [torch.empty_like(shard) for _ in range(world)] if True else None
         dist.all_gather(parts, shard)

@@ -16,12 +16,24 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+# name -> (qasm, fuse_k): k = 4 runs the CUDA-core passes with sequential remaps; k = 6 the
+# tensor-core passes with remaps pipelined between them (n_pipelined > 0 in p2p modes)
+CASES = {
+    "c1": (config_qasm("c1"), 4),
+    "grid20": (emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=3)), 4),
+    "c2": (config_qasm("c2"), 4),
+    "grid20_k6": (emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=3)), 6),
+    "c2_k6": (config_qasm("c2"), 6),
+    "grid26_k6": (emit_qasm(generate(2, 13, 14, "ABCD", seed=5)), 6),
+}
+
+
 def ngpus():
     import torch
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+@pytest.mark.parametrize("mode", ["p2p", "p2p_seq", "p2p_c8", "nccl"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_build_sample_xeb(world, mode, tmp_path, cuda_ok):
     if ngpus() < world:
@@ -31,25 +43,32 @@ def test_sharded_build_sample_xeb(world, mode, tmp_path, cuda_ok):
     env = dict(os.environ, MGPU_OUT=str(tmp_path))
     if mode == "nccl":
         env["RCS_REMAP_NCCL"] = "1"   # grouped send/recv remaps instead of NVLink peer swaps
+    elif mode == "p2p_seq":
+        env["RCS_OVERLAP"] = "0"      # peer swaps not pipelined with the neighbouring passes
+    elif mode == "p2p_c8":
+        env["RCS_OVERLAP_CHUNKS"] = "3"   # 8 pipeline chunks
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-                        "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + (10 if mode == "nccl" else 0)),
+                        "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + 10 * ["p2p", "p2p_seq", "p2p_c8", "nccl"].index(mode)),
                         os.path.join(ROOT, "tests", "mgpu_worker.py")], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.load(open(tmp_path / "results.json"))
     import paper_2512_07311_b200 as rcs
     ctx = rcs.Context(0)
-    texts = {"c1": config_qasm("c1"), "grid20": emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=3)),
-             "c2": config_qasm("c2")}
-    for name, text in texts.items():
+    for name, (text, k) in CASES.items():
         full = np.load(tmp_path / f"{name}_state.npy")
-        single = rcs.State.build(ctx, rcs.Circuit.from_qasm(text), fuse_k=4)
+        single = rcs.State.build(ctx, rcs.Circuit.from_qasm(text), fuse_k=k)
         ref1 = single.copy_out()
         assert np.array_equal(full, ref1), name            # bitwise P-invariance
         ref = oracle.build_state(text)
         d = full.astype(np.complex128) - ref
         assert np.abs(d).max() <= 1e-5 and np.linalg.norm(d) <= 1e-5
-        assert res[name]["report"]["n_remaps"] > 0 or world == 1
+        rep = res[name]["report"]
+        assert rep["n_remaps"] > 0 or world == 1
+        if k == 6 and mode in ("p2p", "p2p_c8"):
+            assert rep["n_pipelined"] > 0, rep
+        if mode in ("p2p_seq", "nccl") or k == 4:
+            assert rep["n_pipelined"] == 0, rep
         x = np.load(tmp_path / f"{name}_x.npy")
         xs = single.sample(20000, seed=SHOT_SEED)
         u = oracle.uniforms(SHOT_SEED, 20000)
