@@ -49,7 +49,10 @@ typedef enum {
     RCS_ERR_SIZE = 7,           /* bitstring >= 2^n                              */
     RCS_ERR_ARG = 8,            /* invalid argument / unsupported configuration               */
     RCS_ERR_CUDA = 9,           /* CUDA runtime error (message has cudaGetErrorString)        */
-    RCS_ERR_NCCL = 10           /* NCCL error (message has ncclGetErrorString)                */
+    RCS_ERR_NCCL = 10,          /* NCCL error (message has ncclGetErrorString)                */
+    RCS_ERR_IO = 11,            /* file open/read/write/rename failed, or an existing output  */
+    RCS_ERR_FORMAT = 12,        /* snapshot: bad magic, version, header or truncated payload  */
+    RCS_ERR_DIGEST = 13         /* snapshot: payload SHA-256 differs from the header's digest */
 } rcs_status;
 
 typedef struct {
@@ -199,6 +202,43 @@ rcs_status rcs_sample_uniforms(rcs_state *s, const double *u, uint64_t shots, ui
 /* Linear XEB of bitstrings x (host or device) against this state. */
 rcs_status rcs_xeb(const rcs_state *s, const uint64_t *x, uint64_t count, rcs_xeb_report *out, rcs_error *err);
 void rcs_state_free(rcs_state *s);   /* frees the handle and its device plan/staging buffers */
+
+/* ---- paper stages 2-3: state snapshot and independent sampler jobs -------
+ * PAPER §3.2 l.37: "The generated quantum state ... is written to a shared file system in an
+ * internal format optimized for fast read access"; l.38: "N CPU-only jobs, each of which
+ * rebuilds the quantum state from the persisted state and performs 2.5x10^6/N measurement
+ * shots ... Each job stores its output in a job-specific file".  File format = SPEC
+ * snapshot-store (reading F3-1): 52-byte header {"RCSS", u32 version 1,
+ * u32 n_qubits, u64 payload_bytes = 16 2^n, 32-byte SHA-256(payload)} then the amplitudes in
+ * index order as little-endian float64 (re, im).  Single-rank states only (world == 1): the
+ * paper's jobs are independent processes (RCS_ERR_ARG otherwise). */
+/* SHA-256 (FIPS 180-4) of a host buffer; host-only, no device needed. */
+rcs_status rcs_sha256(const void *data, uint64_t bytes, uint8_t digest[32]);
+/* Write the state to `path` atomically (temp file + rename; an existing `path` is replaced,
+ * the temp file is never left behind on error); complex64 amplitudes are widened exactly to
+ * float64.  digest (may be NULL) receives SHA-256(payload).  RCS_ERR_IO on I/O failure. */
+rcs_status rcs_snapshot_save(const rcs_state *s, const char *path, uint8_t digest[32], rcs_error *err);
+/* Header-only read (never loads the payload). RCS_ERR_IO / RCS_ERR_FORMAT. */
+rcs_status rcs_snapshot_info(const char *path, int *n_qubits, uint64_t *payload_bytes, uint8_t digest[32],
+                             rcs_error *err);
+/* Device scratch for rcs_snapshot_load of an n-qubit file (block CDF), block_bits as in
+ * rcs_build_opts (0 -> 6). */
+rcs_status rcs_snapshot_scratch_bytes(const rcs_context *ctx, int n_qubits, int block_bits, uint64_t *bytes);
+/* Load `path` into the caller's device buffer (2^n complex64, rounded from float64), verifying
+ * the digest while streaming (RCS_ERR_DIGEST; the buffer content is then unspecified) and the
+ * norm (|T - 1| <= 1e-5, RCS_ERR_NORM); returns a sample-ready state (same calls as a built
+ * one).  The file is opened read-only.  RCS_ERR_IO / RCS_ERR_FORMAT / RCS_ERR_MEMORY. */
+rcs_status rcs_snapshot_load(rcs_context *ctx, const char *path, int block_bits, void *d_amps, uint64_t amps_bytes,
+                             void *d_scratch, uint64_t scratch_bytes, rcs_state **out, rcs_error *err);
+/* PAPER l.38 "2.5x10^6/N measurement shots": counts[j] = total / n_jobs, the
+ * first total mod n_jobs jobs get one more.  RCS_ERR_ARG if n_jobs < 1. */
+rcs_status rcs_shard_shots(uint64_t total, int n_jobs, uint64_t *counts);
+/* Per-job shot seed (reading F3-2): SplitMix64 finalizer of base_seed + 0x9E3779B97F4A7C15 (job_id + 1). */
+uint64_t rcs_job_seed(uint64_t base_seed, uint64_t job_id);
+/* XEB from already-known ideal probabilities p[0..count) of the sampled bitstrings (the
+ * aggregation of the jobs' result files): F, sigma, mean_p as rcs_xeb; fstar = NaN.
+ * Host fp64, no device needed. */
+rcs_status rcs_xeb_from_probs(int n_qubits, const double *p, uint64_t count, rcs_xeb_report *out);
 
 #ifdef __cplusplus
 }

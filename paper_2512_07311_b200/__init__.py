@@ -21,7 +21,8 @@ import numpy as np
 from ._lib import (RcsError, check, lib, rcs_build_opts, rcs_build_report, rcs_circuit_counts, rcs_error,
                    rcs_plan_item, rcs_sample_report, rcs_xeb_report)
 
-__all__ = ["Circuit", "Plan", "Context", "State", "RcsError", "lib"]
+__all__ = ["Circuit", "Plan", "Context", "State", "RcsError", "lib", "sha256", "snapshot_info", "shard_shots",
+           "job_seed", "xeb_from_probs"]
 
 KIND_NAMES = {0: "sx", 1: "sy", 2: "sw", 3: "rz", 4: "fsim"}
 ITEM_NAMES = {0: "pass", 1: "remap", 2: "swap"}
@@ -269,6 +270,40 @@ class State:
               "rcs_sample_uniforms")
         return out
 
+    # ---- paper stage 2: snapshot file (include/rcs.h rcs_snapshot_*)
+    def save_snapshot(self, path: str) -> bytes:
+        """Write the state atomically in the RCSS format; returns SHA-256(payload)."""
+        dg = C.create_string_buffer(32)
+        err = rcs_error()
+        check(lib().rcs_snapshot_save(self._h, path.encode(), dg, C.byref(err)), err, "rcs_snapshot_save")
+        return dg.raw
+
+    @classmethod
+    def load_snapshot(cls, ctx: "Context", path: str, block_bits: int = 0, amps=None, scratch=None) -> "State":
+        """Digest-verified load of an RCSS file into a sample-ready single-GPU state."""
+        import torch
+        n = snapshot_info(path)["n_qubits"]
+        sb = C.c_uint64()
+        check(lib().rcs_snapshot_scratch_bytes(ctx._h, n, block_bits, C.byref(sb)), None,
+              "rcs_snapshot_scratch_bytes")
+        dev = torch.device("cuda", ctx.device)
+        if amps is None:
+            amps = torch.empty(1 << n, dtype=torch.complex64, device=dev)
+        if scratch is None or scratch.numel() < sb.value:
+            scratch = torch.empty(sb.value, dtype=torch.uint8, device=dev)
+        self = cls()
+        self.ctx, self.circuit, self.n, self.g = ctx, None, n, 0
+        self.amps, self.scratch = amps, scratch
+        h = C.c_void_p()
+        err = rcs_error()
+        ctx.stream.wait_stream(torch.cuda.current_stream(dev))
+        check(lib().rcs_snapshot_load(ctx._h, path.encode(), block_bits, _ptr(amps), amps.numel() * 8,
+                                      _ptr(scratch), scratch.numel(), C.byref(h), C.byref(err)), err,
+              "rcs_snapshot_load")
+        self._h = h
+        self.report = {}
+        return self
+
     def xeb(self, x) -> dict:
         if not hasattr(x, "data_ptr"):
             x = np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
@@ -279,3 +314,38 @@ class State:
         err = rcs_error()
         check(lib().rcs_xeb(self._h, _ptr(x), n, C.byref(rep), C.byref(err)), err, "rcs_xeb")
         return {f: getattr(rep, f) for f, _ in rep._fields_}
+
+
+# ---- paper stages 2-4 helpers (host; include/rcs.h) ----------------------------------------
+def sha256(data: bytes) -> bytes:
+    out = C.create_string_buffer(32)
+    check(lib().rcs_sha256(data, len(data), out), None, "rcs_sha256")
+    return out.raw
+
+
+def snapshot_info(path: str) -> dict:
+    n = C.c_int()
+    nb = C.c_uint64()
+    dg = C.create_string_buffer(32)
+    err = rcs_error()
+    check(lib().rcs_snapshot_info(path.encode(), C.byref(n), C.byref(nb), dg, C.byref(err)), err,
+          "rcs_snapshot_info")
+    return {"n_qubits": n.value, "payload_bytes": nb.value, "digest": dg.raw}
+
+
+def shard_shots(total: int, n_jobs: int) -> list:
+    out = (C.c_uint64 * max(1, n_jobs))()
+    check(lib().rcs_shard_shots(total, n_jobs, out), None, "rcs_shard_shots")
+    return list(out)[:n_jobs]
+
+
+def job_seed(base_seed: int, job_id: int) -> int:
+    return int(lib().rcs_job_seed(base_seed, job_id))
+
+
+def xeb_from_probs(n_qubits: int, p) -> dict:
+    p = np.ascontiguousarray(np.asarray(p, dtype=np.float64))
+    rep = rcs_xeb_report()
+    check(lib().rcs_xeb_from_probs(n_qubits, p.ctypes.data_as(C.POINTER(C.c_double)), p.size, C.byref(rep)), None,
+          "rcs_xeb_from_probs")
+    return {f: getattr(rep, f) for f, _ in rep._fields_}

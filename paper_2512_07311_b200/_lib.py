@@ -9,7 +9,8 @@ LIB_PATH = os.path.join(HERE, "librcs.so")
 
 STATUS = {0: "RCS_OK", 1: "RCS_ERR_PARSE", 2: "RCS_ERR_UNKNOWN_GATE", 3: "RCS_ERR_QUBIT_RANGE",
           4: "RCS_ERR_ARITY", 5: "RCS_ERR_MEMORY", 6: "RCS_ERR_NORM", 7: "RCS_ERR_SIZE",
-          8: "RCS_ERR_ARG", 9: "RCS_ERR_CUDA", 10: "RCS_ERR_NCCL"}
+          8: "RCS_ERR_ARG", 9: "RCS_ERR_CUDA", 10: "RCS_ERR_NCCL", 11: "RCS_ERR_IO", 12: "RCS_ERR_FORMAT",
+          13: "RCS_ERR_DIGEST"}
 
 
 class rcs_error(C.Structure):
@@ -83,6 +84,14 @@ SIGNATURES = {
     "rcs_sample_uniforms": (C.c_int, [VP, VP, C.c_uint64, VP, C.POINTER(rcs_sample_report), E]),
     "rcs_xeb": (C.c_int, [VP, VP, C.c_uint64, C.POINTER(rcs_xeb_report), E]),
     "rcs_state_free": (None, [VP]),
+    "rcs_sha256": (C.c_int, [VP, C.c_uint64, VP]),
+    "rcs_snapshot_save": (C.c_int, [VP, C.c_char_p, VP, E]),
+    "rcs_snapshot_info": (C.c_int, [C.c_char_p, IP, U64P, VP, E]),
+    "rcs_snapshot_scratch_bytes": (C.c_int, [VP, C.c_int, C.c_int, U64P]),
+    "rcs_snapshot_load": (C.c_int, [VP, C.c_char_p, C.c_int, VP, C.c_uint64, VP, C.c_uint64, PP, E]),
+    "rcs_shard_shots": (C.c_int, [C.c_uint64, C.c_int, U64P]),
+    "rcs_job_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "rcs_xeb_from_probs": (C.c_int, [C.c_int, DP, C.c_uint64, C.POINTER(rcs_xeb_report)]),
 }
 
 _lib = None

@@ -66,6 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
               "-I", CSRC, "-I", inc] + ARCH
+    common += os.environ.get("RCS_NVCC_FLAGS", "").split()   # experiments, e.g. -DRCS_TC_EPI_WARPS=4
     if verbose:
         common += ["-Xptxas", "-v"]
     objs = []

@@ -12,7 +12,10 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
+
+#include <unistd.h>
 
 #include "internal.h"
 #include "kernels.h"
@@ -573,6 +576,9 @@ const char* rcs_status_string(int s) {
         case RCS_ERR_ARG: return "RCS_ERR_ARG";
         case RCS_ERR_CUDA: return "RCS_ERR_CUDA";
         case RCS_ERR_NCCL: return "RCS_ERR_NCCL";
+        case RCS_ERR_IO: return "RCS_ERR_IO";
+        case RCS_ERR_FORMAT: return "RCS_ERR_FORMAT";
+        case RCS_ERR_DIGEST: return "RCS_ERR_DIGEST";
         default: return "RCS_ERR_UNKNOWN";
     }
 }
@@ -1125,6 +1131,230 @@ rcs_status rcs_xeb(const rcs_state* s_, const uint64_t* x, uint64_t count, rcs_x
     out->F = std::ldexp(mean, s->n) - 1.0;
     out->sigma = std::ldexp(std::sqrt(var), s->n) / std::sqrt(S);
     out->fstar = std::ldexp(s->sum_sq, s->n) - 1.0;
+    return RCS_OK;
+}
+
+// ---- paper stages 2-3: snapshot file + sampler-job helpers -----------------
+rcs_status rcs_sha256(const void* data, uint64_t bytes, uint8_t digest[32]) {
+    if ((!data && bytes) || !digest) return RCS_ERR_ARG;
+    Sha256 h;
+    h.update(data, bytes);
+    h.final(digest);
+    return RCS_OK;
+}
+
+namespace {
+constexpr uint64_t kSnapChunk = 1ull << 22;   // amplitudes per host<->device chunk (32 MB f32)
+
+struct HostBuf {   // pinned staging for the snapshot streams
+    void* p = nullptr;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+}  // namespace
+
+rcs_status rcs_snapshot_save(const rcs_state* s, const char* path, uint8_t digest[32], rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!s || !path) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    rcs_context* c = s->ctx;
+    if (c->world != 1) { set_error(err, RCS_ERR_ARG, "snapshot needs a single-rank state"); return RCS_ERR_ARG; }
+    CUDA_TRY(cudaSetDevice(c->device));
+    HostBuf hb;
+    CUDA_TRY(cudaMallocHost(&hb.p, kSnapChunk * sizeof(float2)));
+    std::vector<double> wide(2 * kSnapChunk);
+    const std::string tmp = std::string(path) + ".tmp." + std::to_string((long long)getpid());
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) { set_error(err, RCS_ERR_IO, "cannot create %s", tmp.c_str()); return RCS_ERR_IO; }
+    auto io_fail = [&](const char* what) {
+        std::fclose(f);
+        std::remove(tmp.c_str());
+        set_error(err, RCS_ERR_IO, "%s %s", what, tmp.c_str());
+        return RCS_ERR_IO;
+    };
+    uint8_t hdr[kSnapHeaderBytes] = {0};
+    if (std::fwrite(hdr, 1, kSnapHeaderBytes, f) != (size_t)kSnapHeaderBytes) return io_fail("write failed:");
+    Sha256 h;
+    for (uint64_t i0 = 0; i0 < s->n_amps; i0 += kSnapChunk) {
+        const uint64_t cnt = std::min(kSnapChunk, s->n_amps - i0);
+        cudaError_t e = cudaMemcpyAsync(hb.p, s->amps + i0, cnt * sizeof(float2), cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) {
+            std::fclose(f);
+            std::remove(tmp.c_str());
+            set_error(err, RCS_ERR_CUDA, "snapshot copy: %s", cudaGetErrorString(e));
+            return RCS_ERR_CUDA;
+        }
+        const float* src = static_cast<const float*>(hb.p);
+        for (uint64_t k = 0; k < 2 * cnt; k++) wide[k] = (double)src[k];   // exact widening
+        h.update(wide.data(), cnt * 16);   // little-endian host (x86-64 / aarch64)
+        if (std::fwrite(wide.data(), 16, cnt, f) != cnt) return io_fail("write failed:");
+    }
+    uint8_t dg[32];
+    h.final(dg);
+    put_snapshot_header(hdr, (uint32_t)s->n, dg);
+    if (std::fseek(f, 0, SEEK_SET) != 0 || std::fwrite(hdr, 1, kSnapHeaderBytes, f) != (size_t)kSnapHeaderBytes)
+        return io_fail("header write failed:");
+    if (std::fflush(f) != 0 || fsync(fileno(f)) != 0) return io_fail("flush failed:");
+    if (std::fclose(f) != 0) {
+        std::remove(tmp.c_str());
+        set_error(err, RCS_ERR_IO, "close failed: %s", tmp.c_str());
+        return RCS_ERR_IO;
+    }
+    if (std::rename(tmp.c_str(), path) != 0) {
+        std::remove(tmp.c_str());
+        set_error(err, RCS_ERR_IO, "rename to %s failed", path);
+        return RCS_ERR_IO;
+    }
+    if (digest) std::memcpy(digest, dg, 32);
+    return RCS_OK;
+}
+
+namespace {
+rcs_status read_header(FILE* f, const char* path, SnapHeader* H, rcs_error* err) {
+    uint8_t hdr[kSnapHeaderBytes];
+    if (std::fread(hdr, 1, kSnapHeaderBytes, f) != (size_t)kSnapHeaderBytes) {
+        set_error(err, RCS_ERR_FORMAT, "%s: truncated header", path);
+        return RCS_ERR_FORMAT;
+    }
+    const char* why = nullptr;
+    if (!get_snapshot_header(hdr, H, &why)) {
+        set_error(err, RCS_ERR_FORMAT, "%s: %s", path, why);
+        return RCS_ERR_FORMAT;
+    }
+    return RCS_OK;
+}
+}  // namespace
+
+rcs_status rcs_snapshot_info(const char* path, int* n_qubits, uint64_t* payload_bytes, uint8_t digest[32],
+                             rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!path) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    FILE* f = std::fopen(path, "rb");
+    if (!f) { set_error(err, RCS_ERR_IO, "cannot open %s", path); return RCS_ERR_IO; }
+    SnapHeader H;
+    rcs_status st = read_header(f, path, &H, err);
+    std::fclose(f);
+    if (st) return st;
+    if (n_qubits) *n_qubits = (int)H.n_qubits;
+    if (payload_bytes) *payload_bytes = H.payload_bytes;
+    if (digest) std::memcpy(digest, H.digest, 32);
+    return RCS_OK;
+}
+
+rcs_status rcs_snapshot_scratch_bytes(const rcs_context* ctx, int n_qubits, int block_bits, uint64_t* bytes) {
+    if (!ctx || !bytes || n_qubits < 1 || ctx->world != 1) return RCS_ERR_ARG;
+    *bytes = scratch_layout(n_qubits, 1, 0, 0, block_bits).total;
+    return RCS_OK;
+}
+
+rcs_status rcs_snapshot_load(rcs_context* ctx, const char* path, int block_bits, void* d_amps, uint64_t amps_bytes,
+                             void* d_scratch, uint64_t scratch_bytes, rcs_state** out, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!ctx || !path || !d_amps || !out) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    if (ctx->world != 1) { set_error(err, RCS_ERR_ARG, "snapshot load needs a single-rank context"); return RCS_ERR_ARG; }
+    FILE* f = std::fopen(path, "rb");
+    if (!f) { set_error(err, RCS_ERR_IO, "cannot open %s", path); return RCS_ERR_IO; }
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    SnapHeader H;
+    rcs_status st = read_header(f, path, &H, err);
+    if (st) return st;
+    const int n = (int)H.n_qubits;
+    if (n < 1) { set_error(err, RCS_ERR_FORMAT, "%s: n_qubits = 0", path); return RCS_ERR_FORMAT; }
+    const uint64_t n_amps = 1ull << n;
+    if (amps_bytes < n_amps * 8) {
+        set_error(err, RCS_ERR_MEMORY, "amplitude buffer too small: need %llu bytes", (unsigned long long)(n_amps * 8));
+        if (err) err->bytes_required = n_amps * 8;
+        return RCS_ERR_MEMORY;
+    }
+    const Layout L = scratch_layout(n, 1, 0, 0, block_bits);
+    if (!d_scratch || scratch_bytes < L.total) {
+        set_error(err, RCS_ERR_MEMORY, "scratch buffer too small: need %llu bytes", (unsigned long long)L.total);
+        if (err) err->bytes_required = L.total;
+        return RCS_ERR_MEMORY;
+    }
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    HostBuf hb;
+    CUDA_TRY(cudaMallocHost(&hb.p, kSnapChunk * sizeof(float2)));
+    std::vector<double> wide(2 * kSnapChunk);
+    float2* amps = reinterpret_cast<float2*>(d_amps);
+    Sha256 h;
+    for (uint64_t i0 = 0; i0 < n_amps; i0 += kSnapChunk) {
+        const uint64_t cnt = std::min(kSnapChunk, n_amps - i0);
+        if (std::fread(wide.data(), 16, cnt, f) != cnt) {
+            set_error(err, RCS_ERR_FORMAT, "%s: truncated payload", path);
+            return RCS_ERR_FORMAT;
+        }
+        h.update(wide.data(), cnt * 16);
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));   // previous chunk's copy done with hb
+        float* dst = static_cast<float*>(hb.p);
+        for (uint64_t k = 0; k < 2 * cnt; k++) dst[k] = (float)wide[k];   // round to nearest
+        CUDA_TRY(cudaMemcpyAsync(amps + i0, hb.p, cnt * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    uint8_t dg[32];
+    h.final(dg);
+    if (std::memcmp(dg, H.digest, 32) != 0) {
+        set_error(err, RCS_ERR_DIGEST, "%s: payload digest mismatch", path);
+        return RCS_ERR_DIGEST;
+    }
+    rcs_state* s = new (std::nothrow) rcs_state();
+    if (!s) return RCS_ERR_MEMORY;
+    s->ctx = ctx;
+    s->n = n;
+    s->g = 0;
+    s->nl = n;
+    s->amps = amps;
+    s->n_amps = n_amps;
+    char* sc = reinterpret_cast<char*>(d_scratch);
+    s->b = L.b;
+    s->nblocks = L.nblocks;
+    s->inc = reinterpret_cast<double*>(sc + L.inc_off);
+    s->scan_tmp = reinterpret_cast<double*>(sc + L.tmp_off);
+    s->part_sq = reinterpret_cast<double*>(sc + L.part_off);
+    s->misc = reinterpret_cast<double*>(sc + L.misc_off);
+    s->staging = reinterpret_cast<float2*>(sc + L.stage_off);
+    s->staging_elems = (L.total - L.stage_off) / sizeof(float2);
+    st = compute_cdf(s, err);
+    if (st) {
+        delete s;
+        return st;
+    }
+    if (!(std::fabs(s->T_total - 1.0) <= 1e-5)) {
+        set_error(err, RCS_ERR_NORM, "%s: norm %.9f", path, s->T_total);
+        delete s;
+        return RCS_ERR_NORM;
+    }
+    *out = s;
+    return RCS_OK;
+}
+
+rcs_status rcs_shard_shots(uint64_t total, int n_jobs, uint64_t* counts) {
+    if (n_jobs < 1 || !counts) return RCS_ERR_ARG;
+    const uint64_t q = total / (uint64_t)n_jobs, r = total % (uint64_t)n_jobs;
+    for (int j = 0; j < n_jobs; j++) counts[j] = q + ((uint64_t)j < r ? 1 : 0);
+    return RCS_OK;
+}
+
+uint64_t rcs_job_seed(uint64_t base_seed, uint64_t job_id) { return job_seed(base_seed, job_id); }
+
+rcs_status rcs_xeb_from_probs(int n_qubits, const double* p, uint64_t count, rcs_xeb_report* out) {
+    if (!out || (!p && count) || n_qubits < 1 || n_qubits > 63 || count == 0) return RCS_ERR_ARG;
+    double sum = 0.0;
+    for (uint64_t i = 0; i < count; i++) sum += p[i];
+    const double S = (double)count, mean = sum / S;
+    double ss = 0.0;
+    for (uint64_t i = 0; i < count; i++) ss += (p[i] - mean) * (p[i] - mean);
+    const double var = count > 1 ? ss / (S - 1.0) : 0.0;
+    out->n_qubits = n_qubits;
+    out->shots = count;
+    out->mean_p = mean;
+    out->F = std::ldexp(mean, n_qubits) - 1.0;
+    out->sigma = std::ldexp(std::sqrt(var), n_qubits) / std::sqrt(S);
+    out->fstar = std::nan("");
     return RCS_OK;
 }
 

@@ -77,6 +77,30 @@ void set_error(rcs_error* err, int code, const char* fmt, ...);
 }  // namespace rcs
 
 namespace rcs {
+// ---- snapshot.cpp: paper stage 2/3 artifacts
+struct Sha256 {   // FIPS 180-4, incremental
+    uint32_t h[8];
+    uint8_t buf[64];
+    size_t fill = 0;
+    uint64_t total = 0;
+    Sha256();
+    void update(const void* data, size_t n);
+    void final(uint8_t out[32]);
+
+private:
+    void block(const uint8_t* p);
+};
+constexpr int kSnapHeaderBytes = 52;
+constexpr uint32_t kSnapVersion = 1;
+struct SnapHeader {
+    uint32_t version, n_qubits;
+    uint64_t payload_bytes;
+    uint8_t digest[32];
+};
+void put_snapshot_header(uint8_t out[kSnapHeaderBytes], uint32_t n_qubits, const uint8_t digest[32]);
+bool get_snapshot_header(const uint8_t in[kSnapHeaderBytes], SnapHeader* h, const char** why);
+uint64_t job_seed(uint64_t base_seed, uint64_t job_id);
+
 // tensor-core pass operands of a plan: which items run on K9, their 6 positions (5-qubit blocks
 // padded with one more local qubit) and the packed fp16 hi/lo matrices (host copy)
 struct TcPack {
