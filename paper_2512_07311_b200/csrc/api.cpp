@@ -889,7 +889,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     // pipelined remaps (f1): on unless RCS_OVERLAP=0; 2^cb chunks, `reserve` SMs left to the swaps
     static const int ov_on = getenv("RCS_OVERLAP") ? atoi(getenv("RCS_OVERLAP")) : 1;
     static const int ov_cb = getenv("RCS_OVERLAP_CHUNKS") ? atoi(getenv("RCS_OVERLAP_CHUNKS")) : 2;
-    static const int ov_res = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 16;
+    static const int ov_res = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 32;
     auto is_tc = [&](size_t i) { return i < P.items.size() && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
     auto tc_ref = [&](size_t i) {
         return PassRef{tcp->pos[i].data(), ctx->d_tc + (size_t)tc_slot[i] * tc_words_each};
