@@ -157,11 +157,18 @@ def oracle_sample(cfg_name: str, cfg: dict, shots: int, budget_s: float, n_small
     text = config_qasm(cfg_name, n_qubits=n_small)
     full_gates = len(oracle.parse(config_qasm(cfg_name)).gates)
     circ = oracle.parse(text)
-    # calibrate G so that the build takes ~budget/2
-    t0 = time.perf_counter()
-    psi = circ.build_state(max_gates=2)
-    t_two = time.perf_counter() - t0
-    G = max(2, min(len(circ.gates), int(2 * (budget_s * 0.5) / max(t_two, 1e-3))))
+    # calibrate G so that the build takes ~budget/2: per-gate cost from the difference of a 2- and
+    # a 6-gate build (the first build_state also allocates and zeroes the 2^n state)
+    def timed(g):
+        t0 = time.perf_counter()
+        circ.build_state(max_gates=g)
+        return time.perf_counter() - t0
+    timed(2)               # first touch of the state's pages
+    t2 = timed(2)
+    t6 = timed(6)
+    per_gate = max((t6 - t2) / 4, 1e-4)
+    fixed = max(0.0, t2 - 2 * per_gate)
+    G = max(6, min(len(circ.gates), int(budget_s * 0.5 / per_gate)))
     t0 = time.perf_counter()
     psi = circ.build_state(max_gates=G)
     t_build = time.perf_counter() - t0
@@ -173,7 +180,7 @@ def oracle_sample(cfg_name: str, cfg: dict, shots: int, budget_s: float, n_small
     t_samp = time.perf_counter() - t0
     n_full = cfg["n_qubits"]
     scale = 2.0 ** (n_full - n_small)
-    proj = t_build / G * full_gates * scale + t_samp * scale
+    proj = max(t_build - fixed, 1e-9) / G * full_gates * scale + t_samp * scale
     desc = (f"oracle fp64, first {G} of {len(circ.gates)} gates of the {cfg_name} circuit at n={n_small} "
             f"({t_build:.2f} s) + sample/XEB of {S} shots ({t_samp:.2f} s); projected linearly in 2^n*gates "
             f"to n={n_full}, {full_gates} gates, {shots} shots: {proj:.1f} s")

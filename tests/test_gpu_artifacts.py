@@ -98,7 +98,9 @@ def test_worker_result_files(rcs, ctx, tmp_path):
     head, x, c, p = jobs.read_result(str(d1 / "result_1.jsonl"))
     assert c.sum() == 2500 and head["shots"] == 2500 and head["n_qubits"] == 12
     assert head["timings"]["sample_s"] > 0 and head["timings"]["load_s"] > 0
-    np.testing.assert_allclose(p, np.abs(ref[x.astype(np.int64)]) ** 2, rtol=0, atol=1e-9)
+    a = np.abs(ref[x.astype(np.int64)])
+    assert (np.abs(p - a ** 2) <= (2 * a + 1e-5) * 1e-5).all()      # amplitude tolerance 1e-5 (G16)
+    np.testing.assert_allclose(p, np.abs(st.copy_out()[x.astype(np.int64)].astype(np.complex128)) ** 2, rtol=1e-6)
     lines = open(d1 / "result_1.jsonl").read().splitlines()
     assert json.loads(lines[1])["bitstring"] == A.bitstring(int(x[0]), 12)
     # the job's draws are the library's sampler with the job seed
