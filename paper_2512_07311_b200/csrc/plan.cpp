@@ -24,6 +24,7 @@
 #include <cstring>
 #include <map>
 #include <set>
+#include <thread>
 
 #include "internal.h"
 
@@ -199,19 +200,40 @@ struct Fuser {
             if (!assigned[i] && ready(i)) cand.push_back(i);
         std::vector<int> S, cur, bS, bcur;
         long best = LONG_MIN;
-        for (int g : cand) {
-            grow(g, S, cur);
-            long score = 0;
-            for (int x : cur) score += nq(x);
-            if (lookahead && cand.size() > 1) {
+        if (lookahead && cand.size() > 1) {
+            // candidates are independent (each grows + rolls out on its own copy): one thread
+            // each, then the same fixed-order choice as the serial loop (deterministic)
+            const size_t nc = cand.size();
+            std::vector<std::vector<int>> cS(nc), ccur(nc);
+            std::vector<long> sc(nc);
+            auto work = [&](size_t i) {
+                grow(cand[i], cS[i], ccur[i]);
+                long score = 0;
+                for (int x : ccur[i]) score += nq(x);
                 Fuser f = *this;
-                f.commit(cur);
-                score = -1000L * f.rollout() + score;   // fewest remaining blocks, then most gates now
-            }
-            if (score > best) {
-                best = score;
-                bS = S;
-                bcur = cur;
+                f.commit(ccur[i]);
+                sc[i] = -1000L * f.rollout() + score;   // fewest remaining blocks, then most gates now
+            };
+            std::vector<std::thread> th;
+            for (size_t i = 1; i < nc; i++) th.emplace_back(work, i);
+            work(0);
+            for (auto& t : th) t.join();
+            for (size_t i = 0; i < nc; i++)
+                if (sc[i] > best) {
+                    best = sc[i];
+                    bS = cS[i];
+                    bcur = ccur[i];
+                }
+        } else {
+            for (int g : cand) {
+                grow(g, S, cur);
+                long score = 0;
+                for (int x : cur) score += nq(x);
+                if (score > best) {
+                    best = score;
+                    bS = S;
+                    bcur = cur;
+                }
             }
         }
         S = bS;

@@ -64,7 +64,11 @@ constexpr uint32_t kCtlBytes = 2560;   // barriers + offset tables; total <= 227
 // control block: 18 mbarriers + 3 x 64 offsets (8 B) + 24 ints + 2 x 64 uint16
 static_assert(18 * 8 + 3 * 64 * 8 + 24 * 4 + 2 * 64 * 2 <= 2560, "control block overflow");
 constexpr uint32_t kSmemBytes = kRaw * kRawBytes + kStages * kStageBytes + kStagingBytes + kCtlBytes;
-constexpr int kAccCols = 3 * TN;             // one D buffer
+#ifndef RCS_TC_ACCS
+#define RCS_TC_ACCS 3                        // accumulators per D buffer (precision / energy trade)
+#endif
+constexpr int kAccs = RCS_TC_ACCS;
+constexpr int kAccCols = kAccs * TN;         // one D buffer
 
 struct TcArgs {
     float2* amps;
@@ -416,13 +420,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                     MMA_F16(d0, al + ks * 8, bh0 + ks * 16, idesc, 1);
                 }
                 // main term A_hi B_hi: K-steps 0-2 -> acc 0, 3-5 -> acc 1, 6-7 -> acc 2
+                if (kAccs == 3) {
 #pragma unroll
-                for (int ks = 0; ks < 3; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                MMA_F16(d0 + TN, ah + 3 * 8, bh0 + 3 * 16, idesc, 0);
+                    for (int ks = 0; ks < 3; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                    MMA_F16(d0 + TN, ah + 3 * 8, bh0 + 3 * 16, idesc, 0);
 #pragma unroll
-                for (int ks = 4; ks < 6; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                MMA_F16(d0 + 2 * TN, ah + 6 * 8, bh0 + 6 * 16, idesc, 0);
-                MMA_F16(d0 + 2 * TN, ah + 7 * 8, bh0 + 7 * 16, idesc, 1);
+                    for (int ks = 4; ks < 6; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                    MMA_F16(d0 + 2 * TN, ah + 6 * 8, bh0 + 6 * 16, idesc, 0);
+                    MMA_F16(d0 + 2 * TN, ah + 7 * 8, bh0 + 7 * 16, idesc, 1);
+                } else if (kAccs == 2) {   // experiment: K-steps 0-3 -> acc 0, 4-7 -> acc 1
+#pragma unroll
+                    for (int ks = 0; ks < 4; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                    MMA_F16(d0 + TN, ah + 4 * 8, bh0 + 4 * 16, idesc, 0);
+#pragma unroll
+                    for (int ks = 5; ks < 8; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                } else {                   // experiment: everything in acc 0
+#pragma unroll
+                    for (int ks = 0; ks < 8; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     su32(&empty[s])));
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -454,8 +469,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             for (int h = 0; h < 2; h++) {
                 uint32_t a0[32], a1[32], a2[32];
                 TMEM_LD32(ta + 32 * h, a0);
-                TMEM_LD32(ta + TN + 32 * h, a1);
-                TMEM_LD32(ta + 2 * TN + 32 * h, a2);
+                if (kAccs > 1) TMEM_LD32(ta + TN + 32 * h, a1);
+                if (kAccs > 2) TMEM_LD32(ta + 2 * TN + 32 * h, a2);
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
                 if (h == 1) {
                     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -464,13 +479,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
 #pragma unroll
                 for (int c = 0; c < 32; c += 2) {
                     float o0, o1;   // ((acc0 + acc1) + acc2) * 2^-29, two columns per packed op
-                    asm("{\n.reg .b64 x, y, z, u;\n"
-                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 z, {%6, %7};\nmov.b64 u, {%8, %8};\n"
-                        "add.rn.f32x2 x, x, y;\nadd.rn.f32x2 x, x, z;\nmul.rn.f32x2 x, x, u;\n"
-                        "mov.b64 {%0, %1}, x;\n}"
-                        : "=f"(o0), "=f"(o1)
-                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "r"(a2[c]), "r"(a2[c + 1]),
-                          "f"(us));
+                    if (kAccs == 3) {
+                        asm("{\n.reg .b64 x, y, z, u;\n"
+                            "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 z, {%6, %7};\nmov.b64 u, {%8, %8};\n"
+                            "add.rn.f32x2 x, x, y;\nadd.rn.f32x2 x, x, z;\nmul.rn.f32x2 x, x, u;\n"
+                            "mov.b64 {%0, %1}, x;\n}"
+                            : "=f"(o0), "=f"(o1)
+                            : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "r"(a2[c]), "r"(a2[c + 1]),
+                              "f"(us));
+                    } else if (kAccs == 2) {
+                        asm("{\n.reg .b64 x, y, u;\n"
+                            "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\n"
+                            "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\n"
+                            "mov.b64 {%0, %1}, x;\n}"
+                            : "=f"(o0), "=f"(o1)
+                            : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(us));
+                    } else {
+                        o0 = __uint_as_float(a0[c]) * us;
+                        o1 = __uint_as_float(a0[c + 1]) * us;
+                    }
                     st[2 * (32 * h + c)] = o0;
                     st[2 * (32 * h + c) + 2] = o1;
                 }
