@@ -69,6 +69,7 @@ constexpr int kTcMinLocal = 12;
 constexpr int kFuseSeeds = 4;
 // fuser: pick among the seeds by the block count of a greedy completion (rollout)
 constexpr bool kFuseLookahead = true;
+constexpr bool kRemapPrefetch = true;   // remaps also bring in soon-needed global qubits
 
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err);
 

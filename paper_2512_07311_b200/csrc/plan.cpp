@@ -375,8 +375,36 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
                 if (na != nb) return na > nb;
                 return pos[a] > pos[b2];
             });
+            // prefetch: also bring in the global qubits needed soonest, while the eviction
+            // candidate is needed later than they are (a (k+1)-bit remap moves 1 - 2^-(k+1) of the
+            // shard, cheaper than a separate 1-bit remap later: 1/2)
+            if (kRemapPrefetch) {
+                std::vector<int> later;
+                for (int q = 0; q < n; q++)
+                    if (pos[q] >= n_local && !std::count(need.begin(), need.end(), q) && next_use(q, bi) < INT_MAX)
+                        later.push_back(q);
+                std::stable_sort(later.begin(), later.end(),
+                                 [&](int a, int b2) { return next_use(a, bi) < next_use(b2, bi); });
+                for (int q : later) {
+                    if ((int)need.size() >= n_global || need.size() >= cand.size()) break;
+                    if (next_use(cand[need.size()], bi) <= next_use(q, bi)) break;
+                    need.push_back(q);
+                }
+            }
+            // evicted canonical-global qubits go to their home global position when it is free
+            std::vector<int> gpos;
+            for (int q : need) gpos.push_back(pos[q]);
+            std::vector<int> ev(cand.begin(), cand.begin() + need.size());
+            std::vector<int> slot(need.size(), -1);
+            std::vector<char> used(need.size(), 0);
+            for (size_t i = 0; i < ev.size(); i++)
+                for (size_t j = 0; j < gpos.size(); j++)
+                    if (!used[j] && gpos[j] == ev[i]) { slot[i] = (int)j; used[j] = 1; break; }
+            for (size_t i = 0; i < ev.size(); i++)
+                for (size_t j = 0; j < gpos.size() && slot[i] < 0; j++)
+                    if (!used[j]) { slot[i] = (int)j; used[j] = 1; }
             std::vector<std::pair<int, int>> pairs;
-            for (size_t i = 0; i < need.size(); i++) pairs.push_back({pos[need[i]], pos[cand[i]]});
+            for (size_t i = 0; i < ev.size(); i++) pairs.push_back({gpos[slot[i]], pos[ev[i]]});
             emit_remap(pairs);
         }
         Item it;
