@@ -59,6 +59,7 @@ def parse_args():
     ap.add_argument("--shots", type=int, default=0, help="override the config's shot count")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="default: --steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--canonical", action="store_true", help="restore the canonical layout after every build")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     return ap.parse_args()
 
@@ -216,7 +217,8 @@ def run_ours(args):
     plan = rcs.Plan(circuit, args.fuse_k, g)
     mat_bytes = sum(8 * (1 << it["k"]) ** 2 for it in plan.items() if it["type"] == "pass")
     amps = torch.empty(1 << (n - g), dtype=torch.complex64, device=dev)
-    st0 = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, amps=amps)   # sizes scratch
+    keep = not args.canonical   # skip the final layout restore: samples/XEB are layout-independent
+    st0 = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, amps=amps, keep_layout=keep)   # sizes scratch
     scratch = st0.scratch
     st0.free()
     x_dev = torch.empty(shots, dtype=torch.int64, device=dev)
@@ -226,7 +228,8 @@ def run_ours(args):
             dist.barrier(device_ids=[local])
 
     def step(timing):
-        st = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, timing=timing, amps=amps, scratch=scratch)
+        st = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, timing=timing, amps=amps, scratch=scratch,
+                             keep_layout=keep)
         rep = rcs_sample_report()
         err = rcs_error()
         import ctypes as C
@@ -277,7 +280,7 @@ def run_ours(args):
     w0 = time.perf_counter()
     for _ in range(e2e_steps):
         c2 = rcs.Circuit.from_qasm(text)                       # host QASM in
-        st = rcs.State.build(ctx, c2, fuse_k=args.fuse_k, amps=amps, scratch=scratch)
+        st = rcs.State.build(ctx, c2, fuse_k=args.fuse_k, amps=amps, scratch=scratch, keep_layout=keep)
         xh = st.sample(shots, seed=SHOT_SEED)                  # bitstrings to host
         xr_h = st.xeb(xh)                                      # XEB from the host array
         st.free()
@@ -321,6 +324,7 @@ def run_ours(args):
             "shots_per_s_incl_blocksum": shots / ((statistics.median(sample_ms) + R["blocksum_ms"]) / 1e3),
             "xeb": X["F"], "xeb_sigma": X["sigma"], "fstar": X["fstar"], "norm": R["norm"],
             "n_passes": R["n_passes"], "n_remaps": R["n_remaps"], "n_swaps": R["n_swaps"],
+            "layout_kept": R["layout_kept"],
             "pass_gbs": {"min": gbs[0], "median": gbs[len(gbs) // 2], "max": gbs[-1]},
             "pass_ms_total": R["pass_ms"], "remap_ms_total": R["remap_ms"], "swap_ms_total": R["swap_ms"],
             "blocksum_ms": R["blocksum_ms"], "n_tc_passes": R["n_tc_passes"],

@@ -83,6 +83,12 @@ typedef struct {
                                 remap as an in-device bit swap (tests the sharded plan on 1 GPU) */
     int timing;              /* 1: record a CUDA-event pair around every pass / remap             */
     uint64_t staging_bytes;  /* bound of the remap staging area (0 -> 256 MiB)                   */
+    int keep_layout;         /* 1: skip the final layout restore (remaps / bit swaps that only
+                                bring the qubits back to canonical positions).  Sampling, XEB and
+                                probabilities work on the kept layout (logical CDF over all
+                                ranks); rcs_state_copy_out / rcs_snapshot_save then need
+                                rcs_state_canonicalize first (RCS_ERR_ARG otherwise).  The
+                                scratch grows to 2 x 8 x 2^(n-6) B when world > 1.           */
 } rcs_build_opts;
 
 typedef struct {
@@ -102,6 +108,7 @@ typedef struct {
     double norm;             /* sum |psi|^2 over all ranks                                       */
     int n_tc_passes;         /* of n_passes, 6-qubit passes run on the tensor cores (K9)          */
     double swap_ms;          /* timing=1: sum of local bit-swap (layout restore) pass times       */
+    int layout_kept;         /* 1: the state is in a permuted (non-canonical) layout            */
     int n_pipelined;         /* remaps run as chunked NVLink swaps overlapped with the adjacent
                                 tensor-core passes; env RCS_OVERLAP=0 disables,
                                 RCS_OVERLAP_CHUNKS = log2 chunks (default 2), RCS_OVERLAP_SMS =
@@ -182,6 +189,8 @@ rcs_status rcs_state_scratch_bytes(const rcs_context *ctx, const rcs_circuit *c,
 rcs_status rcs_state_build(rcs_context *ctx, const rcs_circuit *c, const rcs_build_opts *opts,
                            void *d_amps, uint64_t amps_bytes, void *d_scratch, uint64_t scratch_bytes,
                            rcs_state **out, rcs_build_report *rep, rcs_error *err);
+/* Collective: run the deferred layout restore of a keep_layout build (no-op if canonical). */
+rcs_status rcs_state_canonicalize(rcs_state *s, rcs_error *err);
 /* Per-pass kernel times (ms) of the last build (timing=1), in plan order; *n = count. */
 rcs_status rcs_state_pass_times(const rcs_state *s, float *ms, int cap, int *n);
 rcs_status rcs_state_norm(const rcs_state *s, double *norm);          /* collective */

@@ -178,11 +178,13 @@ class State:
 
     @classmethod
     def build(cls, ctx: Context, circuit: Circuit, fuse_k: int = 0, block_bits: int = 0, virtual_global: int = 0,
-              timing: bool = False, staging_bytes: int = 0, amps=None, scratch=None) -> "State":
+              timing: bool = False, staging_bytes: int = 0, amps=None, scratch=None,
+              keep_layout: bool = False) -> "State":
         import torch
         n = circuit.n_qubits
         g = ctx.world.bit_length() - 1
-        opts = rcs_build_opts(fuse_k, block_bits, virtual_global, 1 if timing else 0, staging_bytes)
+        opts = rcs_build_opts(fuse_k, block_bits, virtual_global, 1 if timing else 0, staging_bytes,
+                              1 if keep_layout else 0)
         sb = C.c_uint64()
         check(lib().rcs_state_scratch_bytes(ctx._h, circuit._h, C.byref(opts), C.byref(sb)), None,
               "rcs_state_scratch_bytes")
@@ -216,6 +218,12 @@ class State:
 
     def free(self):
         self.__del__()
+
+    def canonicalize(self) -> None:
+        """Collective: run the restore deferred by keep_layout=True (copy_out needs it)."""
+        err = rcs_error()
+        check(lib().rcs_state_canonicalize(self._h, C.byref(err)), err, "rcs_state_canonicalize")
+        self.report["layout_kept"] = 0
 
     @property
     def norm(self) -> float:

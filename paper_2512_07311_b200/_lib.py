@@ -25,7 +25,7 @@ class rcs_circuit_counts(C.Structure):
 
 class rcs_build_opts(C.Structure):
     _fields_ = [("fuse_k", C.c_int), ("block_bits", C.c_int), ("virtual_global", C.c_int),
-                ("timing", C.c_int), ("staging_bytes", C.c_uint64)]
+                ("timing", C.c_int), ("staging_bytes", C.c_uint64), ("keep_layout", C.c_int)]
 
 
 class rcs_build_report(C.Structure):
@@ -34,7 +34,7 @@ class rcs_build_report(C.Structure):
                 ("pass_ms_min", C.c_double), ("pass_ms_max", C.c_double), ("remap_ms", C.c_double),
                 ("blocksum_ms", C.c_double), ("pass_bytes", C.c_uint64), ("remap_bytes", C.c_uint64),
                 ("norm", C.c_double), ("n_tc_passes", C.c_int), ("swap_ms", C.c_double),
-                ("n_pipelined", C.c_int)]
+                ("layout_kept", C.c_int), ("n_pipelined", C.c_int)]
 
 
 class rcs_sample_report(C.Structure):
@@ -76,6 +76,7 @@ SIGNATURES = {
     "rcs_state_scratch_bytes": (C.c_int, [VP, VP, C.POINTER(rcs_build_opts), U64P]),
     "rcs_state_build": (C.c_int, [VP, VP, C.POINTER(rcs_build_opts), VP, C.c_uint64, VP, C.c_uint64, PP,
                                   C.POINTER(rcs_build_report), E]),
+    "rcs_state_canonicalize": (C.c_int, [VP, E]),
     "rcs_state_pass_times": (C.c_int, [VP, C.POINTER(C.c_float), C.c_int, IP]),
     "rcs_state_norm": (C.c_int, [VP, DP]),
     "rcs_state_copy_out": (C.c_int, [VP, C.c_uint64, C.c_uint64, VP, E]),

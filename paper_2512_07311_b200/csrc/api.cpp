@@ -74,6 +74,13 @@ struct rcs_state {
     double T_r = 0, T_total = 0, E_r = 0, sum_sq = 0;
     int owns_tail = 0, owns_any = 0;
     std::vector<float> pass_ms;
+    // kept (permuted) layout: final_pos of the plan, deferred restore items
+    std::shared_ptr<const Plan> plan;
+    bool permuted = false;
+    double* gbuf = nullptr;          // all ranks' physical block sums (2^(n-b))
+    uint64_t* ptab = nullptr;        // logical -> physical block byte tables (device)
+    uint64_t nblocks_all = 0;
+    uint64_t last_block = 0;
 };
 
 namespace {
@@ -119,24 +126,37 @@ int log2_exact(int w) {
 struct Layout {
     int b;
     uint64_t nblocks, inc_off, tmp_off, part_off, misc_off, stage_off, total;
+    // kept layout (keep_layout with remaps): logical CDF over all 2^(n-b) blocks
+    bool kept = false;
+    uint64_t nblocks_all = 0, gbuf_off = 0, ptab_off = 0;
+    uint64_t stage_end = 0;
 };
 
-Layout scratch_layout(int nl, int world, int virt, uint64_t staging_bytes, int block_bits) {
+// keep: a kept (permuted) final layout is possible (keep_layout and world > 1 or virtual global)
+Layout scratch_layout(int nl, int world, int virt, uint64_t staging_bytes, int block_bits, bool keep = false) {
     Layout L{};
     int b = block_bits > 0 ? block_bits : 6;
     if (b > 6) b = 6;
     if (b > nl) b = nl;
     L.b = b;
     L.nblocks = 1ull << (nl - b);
+    L.kept = keep && (world > 1 || virt > 0);
+    L.nblocks_all = L.kept ? L.nblocks * (uint64_t)world : L.nblocks;
     L.inc_off = 0;
-    L.tmp_off = align_up(L.inc_off + L.nblocks * 8);
-    L.part_off = align_up(L.tmp_off + dev::scan_tmp_doubles(L.nblocks) * 8);
+    L.tmp_off = align_up(L.inc_off + L.nblocks_all * 8);
+    L.part_off = align_up(L.tmp_off + dev::scan_tmp_doubles(L.nblocks_all) * 8);
     L.misc_off = align_up(L.part_off + (uint64_t)dev::block_sums_grid() * 8);
     L.stage_off = align_up(L.misc_off + 64 * 8);
     uint64_t st = 0;
     if (world > 1) st = staging_bytes ? staging_bytes : (256ull << 20);
-    (void)virt;
-    L.total = align_up(L.stage_off + st);
+    uint64_t end = align_up(L.stage_off + st);
+    L.stage_end = end;
+    if (L.kept) {
+        L.gbuf_off = end;
+        L.ptab_off = align_up(L.gbuf_off + L.nblocks_all * 8);
+        end = align_up(L.ptab_off + (uint64_t)dev::kPermTables * 256 * 8);
+    }
+    L.total = end;
     return L;
 }
 
@@ -477,6 +497,40 @@ rcs_status compute_cdf(rcs_state* s, rcs_error* err) {
     return RCS_OK;
 }
 
+// kept (permuted) layout: every rank builds the logical-order block CDF of the whole state
+// (all-gather of the physical block sums, permutation into logical order, one global scan)
+rcs_status compute_cdf_kept(rcs_state* s, rcs_error* err) {
+    rcs_context* c = s->ctx;
+    const uint64_t nbl = s->nblocks;
+    double* mine = s->gbuf + (uint64_t)c->rank * nbl;
+    CUDA_TRY(dev::block_sums(s->amps, nbl, s->b, mine, s->part_sq, c->stream));
+    if (c->world > 1) NCCL_TRY(ncclAllGather(mine, s->gbuf, nbl, ncclDouble, c->comm, c->stream));
+    CUDA_TRY(dev::perm_blocks(s->gbuf, s->inc, s->nblocks_all, s->ptab, c->stream));
+    CUDA_TRY(dev::scan_inclusive(s->inc, s->nblocks_all, s->scan_tmp, c->stream));
+    CUDA_TRY(dev::reduce_sum(s->part_sq, dev::block_sums_grid(), s->misc + 1, c->stream));
+    if (c->world > 1) NCCL_TRY(ncclAllReduce(s->misc + 1, s->misc + 1, 1, ncclDouble, ncclSum, c->comm, c->stream));
+    unsigned long long* last = reinterpret_cast<unsigned long long*>(s->misc + 40);
+    CUDA_TRY(dev::last_nonzero(s->inc, s->nblocks_all, last, c->stream));
+    double T = 0.0, sq = 0.0;
+    unsigned long long lb = 0;
+    CUDA_TRY(cudaMemcpyAsync(&T, s->inc + (s->nblocks_all - 1), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&sq, s->misc + 1, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&lb, last, sizeof lb, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    s->T_total = T;
+    s->sum_sq = sq;
+    s->last_block = lb;
+    s->E_r = 0.0;
+    s->T_r = T;
+    s->owns_any = 1;
+    s->owns_tail = 1;
+    return RCS_OK;
+}
+
+dev::Locator locator(const rcs_state* s) {
+    return dev::Locator{s->nl, (uint64_t)s->ctx->rank, s->b, s->permuted ? s->ptab : nullptr};
+}
+
 rcs_status ensure_buffers(rcs_state* s, rcs_error* err) {
     if (s->xbuf) return RCS_OK;
     rcs_context* c = s->ctx;
@@ -538,6 +592,13 @@ rcs_status sample_impl(rcs_state* s, uint64_t shots, uint64_t seed, uint64_t off
         }
         A.base_index = (uint64_t)c->rank << s->nl;
         A.x_out = xo;
+        A.nl = s->nl;
+        A.rank = (uint64_t)c->rank;
+        if (s->permuted) {   // logical CDF over all ranks' blocks
+            A.ptab = s->ptab;
+            A.nblocks = s->nblocks_all;
+            A.last_block = s->last_block;
+        }
         CUDA_TRY(dev::sample(A, c->stream));
         if (c->world > 1)
             NCCL_TRY(ncclAllReduce(xo, xo, cnt, ncclUint64, ncclSum, c->comm, c->stream));
@@ -748,7 +809,7 @@ rcs_status rcs_state_scratch_bytes(const rcs_context* ctx, const rcs_circuit* c,
     if (opts) o = *opts;
     const int nl = c->c.n - ctx->g;
     if (nl < 1) return RCS_ERR_ARG;
-    *bytes = scratch_layout(nl, ctx->world, o.virtual_global, o.staging_bytes, o.block_bits).total;
+    *bytes = scratch_layout(nl, ctx->world, o.virtual_global, o.staging_bytes, o.block_bits, o.keep_layout != 0).total;
     return RCS_OK;
 }
 
@@ -774,7 +835,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         if (err) err->bytes_required = n_amps * 8;
         return RCS_ERR_MEMORY;
     }
-    const Layout L = scratch_layout(nl, ctx->world, o.virtual_global, o.staging_bytes, o.block_bits);
+    const Layout L = scratch_layout(nl, ctx->world, o.virtual_global, o.staging_bytes, o.block_bits, o.keep_layout != 0);
     if (!d_scratch || scratch_bytes < L.total) {
         set_error(err, RCS_ERR_MEMORY, "scratch buffer too small: need %llu bytes", (unsigned long long)L.total);
         if (err) err->bytes_required = L.total;
@@ -819,7 +880,36 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     s->part_sq = reinterpret_cast<double*>(sc + L.part_off);
     s->misc = reinterpret_cast<double*>(sc + L.misc_off);
     s->staging = reinterpret_cast<float2*>(sc + L.stage_off);
-    s->staging_elems = (L.total - L.stage_off) / sizeof(float2);
+    s->staging_elems = (L.stage_end - L.stage_off) / sizeof(float2);
+    s->plan = plan_ptr;
+    // keep_layout: skip the restore items when the final layout is not canonical
+    bool keep = false;
+    if (L.kept) {
+        for (int q = L.b; q < n && !keep; q++) keep = P.final_pos[q] != q;
+    }
+    const size_t n_exec = keep ? (size_t)P.restore_begin : P.items.size();
+    std::vector<uint64_t> ptab_host;
+    if (keep) {
+        s->gbuf = reinterpret_cast<double*>(sc + L.gbuf_off);
+        s->ptab = reinterpret_cast<uint64_t*>(sc + L.ptab_off);
+        s->nblocks_all = L.nblocks_all;
+        ptab_host.assign((size_t)dev::kPermTables * 256, 0);
+        const int nlb = n - L.b;   // logical block bits
+        if (nlb > 8 * dev::kPermTables) {
+            set_error(err, RCS_ERR_ARG, "keep_layout supports n - block_bits <= %d", 8 * dev::kPermTables);
+            delete s;
+            return RCS_ERR_ARG;
+        }
+        for (int c = 0; c < dev::kPermTables; c++)
+            for (int v = 0; v < 256; v++) {
+                uint64_t o = 0;
+                for (int i = 0; i < 8; i++) {
+                    const int bit = 8 * c + i;
+                    if (bit < nlb && ((v >> i) & 1)) o |= 1ull << (P.final_pos[bit + L.b] - L.b);
+                }
+                ptab_host[(size_t)c * 256 + v] = o;
+            }
+    }
 
     auto fail = [&](rcs_status code) {
         delete s;
@@ -881,6 +971,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         ctx->tc_hold = tcp;
     }
     BUILD_TRY(dev::init_basis(s->amps, n_amps, ctx->rank == 0, stream));
+    if (keep)
+        BUILD_TRY(cudaMemcpyAsync(s->ptab, ptab_host.data(), ptab_host.size() * 8, cudaMemcpyHostToDevice, stream));
     uint64_t pass_bytes = 0, remap_bytes = 0;
     int n_pipelined = 0;
     std::vector<float> mbuf;
@@ -890,15 +982,15 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     static const int ov_on = getenv("RCS_OVERLAP") ? atoi(getenv("RCS_OVERLAP")) : 1;
     static const int ov_cb = getenv("RCS_OVERLAP_CHUNKS") ? atoi(getenv("RCS_OVERLAP_CHUNKS")) : 2;
     static const int ov_res = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 32;
-    auto is_tc = [&](size_t i) { return i < P.items.size() && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
+    auto is_tc = [&](size_t i) { return i < n_exec && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
     auto tc_ref = [&](size_t i) {
         return PassRef{tcp->pos[i].data(), ctx->d_tc + (size_t)tc_slot[i] * tc_words_each};
     };
-    for (size_t ii = 0; ii < P.items.size(); ii++) {
+    for (size_t ii = 0; ii < n_exec; ii++) {
         const Item& it = P.items[ii];
         // [TC pass] -> REMAP -> [TC pass] pipelined over NVLink
         if (ov_on && ctx->world > 1 && ctx->p2p && ov_cb >= 1 && ov_cb <= 4) {
-            size_t ir = (it.type == RCS_ITEM_REMAP) ? ii : (is_tc(ii) && ii + 1 < P.items.size() &&
+            size_t ir = (it.type == RCS_ITEM_REMAP) ? ii : (is_tc(ii) && ii + 1 < n_exec &&
                                                             P.items[ii + 1].type == RCS_ITEM_REMAP) ? ii + 1 : SIZE_MAX;
             if (ir != SIZE_MAX) {
                 const Item& rm = P.items[ir];
@@ -959,15 +1051,21 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         }
     }
     BUILD_TRY(cudaEventRecord(ec0, stream));
-    st = compute_cdf(s, err);
+    s->permuted = keep;
+    st = keep ? compute_cdf_kept(s, err) : compute_cdf(s, err);
     if (st) return fail(st);
     BUILD_TRY(cudaEventRecord(eb1, stream));
     BUILD_TRY(cudaStreamSynchronize(stream));
 
     rcs_build_report R{};
     R.n_passes = P.n_passes;
-    R.n_remaps = P.n_remaps;
-    R.n_swaps = P.n_swaps;
+    R.n_remaps = 0;
+    R.n_swaps = 0;
+    for (size_t ii = 0; ii < n_exec; ii++) {   // executed items (a kept layout skips the restore)
+        R.n_remaps += P.items[ii].type == RCS_ITEM_REMAP;
+        R.n_swaps += P.items[ii].type == RCS_ITEM_SWAP;
+    }
+    R.layout_kept = keep ? 1 : 0;
     R.fuse_k = P.fuse_k;
     R.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     float ms = 0.f;
@@ -980,13 +1078,13 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     s->pass_ms.clear();
     if (o.timing) {
         R.blocksum_ms = cdf_ms;
-        std::vector<double> item_ms(P.items.size(), 0.0);
+        std::vector<double> item_ms(n_exec, 0.0);
         for (const Span& sp : spans) {
             float t = 0.f;
             if (sp.a && sp.b) cudaEventElapsedTime(&t, sp.a, sp.b);
             item_ms[sp.item] += sp.sign * (double)t;
         }
-        for (size_t ii = 0; ii < P.items.size(); ii++) {
+        for (size_t ii = 0; ii < n_exec; ii++) {
             const double t = item_ms[ii];
             if (P.items[ii].type == RCS_ITEM_PASS) {
                 R.pass_ms += t;
@@ -1016,6 +1114,31 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
 #undef BUILD_TRY
 }
 
+rcs_status rcs_state_canonicalize(rcs_state* s, rcs_error* err) {
+    if (err) std::memset(err, 0, sizeof *err);
+    if (!s) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    if (!s->permuted) return RCS_OK;
+    rcs_context* c = s->ctx;
+    CUDA_TRY(cudaSetDevice(c->device));
+    const Plan& P = *s->plan;
+    if (c->world > 1) {   // the peer mappings may belong to another state's buffer by now
+        rcs_status r = setup_peers(c, s->amps, err);
+        if (r) return r;
+    }
+    uint64_t bytes = 0;
+    for (size_t ii = (size_t)P.restore_begin; ii < P.items.size(); ii++) {
+        const Item& it = P.items[ii];
+        if (it.type == RCS_ITEM_REMAP && c->world > 1) {
+            rcs_status r = c->p2p ? do_remap_p2p(s, it, &bytes, err) : do_remap_nccl(s, it, &bytes, err);
+            if (r) return r;
+        } else {
+            CUDA_TRY(dev::bit_swap(s->amps, s->nl, it.k, it.a, it.b, c->stream));
+        }
+    }
+    s->permuted = false;
+    return compute_cdf(s, err);
+}
+
 rcs_status rcs_state_pass_times(const rcs_state* s, float* ms, int cap, int* n) {
     if (!s) return RCS_ERR_ARG;
     const int k = (int)s->pass_ms.size();
@@ -1034,6 +1157,10 @@ rcs_status rcs_state_norm(const rcs_state* s, double* norm) {
 rcs_status rcs_state_copy_out(const rcs_state* s, uint64_t first, uint64_t count, void* dst, rcs_error* err) {
     if (err) std::memset(err, 0, sizeof *err);
     if (!s || (!dst && count)) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
+    if (s->permuted) {
+        set_error(err, RCS_ERR_ARG, "state kept in a permuted layout: call rcs_state_canonicalize first");
+        return RCS_ERR_ARG;
+    }
     const uint64_t base = (uint64_t)s->ctx->rank << s->nl;
     if (first < base || first + count > base + s->n_amps || first + count < first) {
         set_error(err, RCS_ERR_ARG, "range [%llu, +%llu) not on this rank", (unsigned long long)first,
@@ -1064,7 +1191,7 @@ rcs_status rcs_probabilities(const rcs_state* s_, const uint64_t* x, uint64_t co
             xi = s->xbuf;
         }
         double* po = pd ? p_out + i0 : s->dbuf;
-        CUDA_TRY(dev::gather_prob(s->amps, xi, cnt, s->nl, (uint64_t)c->rank, s->n, po, s->bad, c->stream));
+        CUDA_TRY(dev::gather_prob(s->amps, xi, cnt, locator(s), s->n, po, s->bad, c->stream));
         if (c->world > 1) NCCL_TRY(ncclAllReduce(po, po, cnt, ncclDouble, ncclSum, c->comm, c->stream));
         if (!pd) CUDA_TRY(cudaMemcpyAsync(p_out + i0, po, cnt * 8, cudaMemcpyDeviceToHost, c->stream));
     }
@@ -1109,7 +1236,7 @@ rcs_status rcs_xeb(const rcs_state* s_, const uint64_t* x, uint64_t count, rcs_x
             CUDA_TRY(cudaMemcpyAsync(s->xbuf, x + i0, cnt * 8, cudaMemcpyHostToDevice, c->stream));
             xi = s->xbuf;
         }
-        CUDA_TRY(dev::xeb_partials(s->amps, xi, cnt, s->nl, (uint64_t)c->rank, s->n, s->xeb_part, s->bad, c->stream));
+        CUDA_TRY(dev::xeb_partials(s->amps, xi, cnt, locator(s), s->n, s->xeb_part, s->bad, c->stream));
         CUDA_TRY(dev::xeb_finalize(s->xeb_part, grid, acc, c->stream));
         if (c->world > 1) NCCL_TRY(ncclAllReduce(acc, acc, 3, ncclDouble, ncclSum, c->comm, c->stream));
         double part[3];
@@ -1159,6 +1286,10 @@ rcs_status rcs_snapshot_save(const rcs_state* s, const char* path, uint8_t diges
     if (!s || !path) { set_error(err, RCS_ERR_ARG, "null argument"); return RCS_ERR_ARG; }
     rcs_context* c = s->ctx;
     if (c->world != 1) { set_error(err, RCS_ERR_ARG, "snapshot needs a single-rank state"); return RCS_ERR_ARG; }
+    if (s->permuted) {
+        set_error(err, RCS_ERR_ARG, "state kept in a permuted layout: call rcs_state_canonicalize first");
+        return RCS_ERR_ARG;
+    }
     CUDA_TRY(cudaSetDevice(c->device));
     HostBuf hb;
     CUDA_TRY(cudaMallocHost(&hb.p, kSnapChunk * sizeof(float2)));
@@ -1317,7 +1448,7 @@ rcs_status rcs_snapshot_load(rcs_context* ctx, const char* path, int block_bits,
     s->part_sq = reinterpret_cast<double*>(sc + L.part_off);
     s->misc = reinterpret_cast<double*>(sc + L.misc_off);
     s->staging = reinterpret_cast<float2*>(sc + L.stage_off);
-    s->staging_elems = (L.total - L.stage_off) / sizeof(float2);
+    s->staging_elems = (L.stage_end - L.stage_off) / sizeof(float2);
     st = compute_cdf(s, err);
     if (st) {
         delete s;

@@ -56,6 +56,10 @@ struct Plan {
     std::vector<Block> blocks;
     std::vector<Item> items;
     int n_passes = 0, n_remaps = 0, n_swaps = 0;
+    // items [restore_begin, end) only bring the layout back to canonical; final_pos[q] is the
+    // physical position of qubit q before them (>= n - n_global: a rank bit)
+    int restore_begin = 0;
+    std::vector<int> final_pos;
 };
 
 // low physical positions never moved by remaps: keeps qubit 0 at bit 0 (the CUDA-core pass

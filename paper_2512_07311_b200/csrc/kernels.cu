@@ -381,8 +381,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample(const __grid_const
                                 : (double)(splitmix_out(A.seed, A.shot0 + s + 1) >> 11) * (1.0 / 9007199254740992.0);
         t = u * A.T_total;
     }
-    const bool owned = valid && A.owns_any && t >= A.E_r && (A.owns_tail || t < A.E_r + A.T_r);
-    const double tl = t - A.E_r;
+    const bool perm = A.ptab != nullptr;
+    bool owned = perm ? valid : (valid && A.owns_any && t >= A.E_r && (A.owns_tail || t < A.E_r + A.T_r));
+    const double tl = perm ? t : t - A.E_r;
     uint64_t j = A.nblocks;
     if (owned) {
         uint64_t lo = 0, hi = A.nblocks;
@@ -392,6 +393,21 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample(const __grid_const
         }
         j = lo;
     }
+    // kept layout: resolve the tail here, then keep only the shots whose block this rank holds
+    bool ptail = false;
+    uint64_t lblk = 0;   // local block index of logical block j (kept layout)
+    if (perm && owned) {
+        if (j >= A.nblocks) {
+            j = A.last_block;
+            ptail = true;
+        }
+        uint64_t pb = 0;
+#pragma unroll
+        for (int c = 0; c < kPermTables; c++) pb |= __ldg(A.ptab + 256 * c + ((j >> (8 * c)) & 255));
+        const int lbits = A.nl - A.b;
+        owned = (pb >> lbits) == A.rank;
+        lblk = pb & ((1ull << lbits) - 1);
+    }
     const uint64_t B = 1ull << A.b;
     unsigned long long result = 0;
     for (int i = 0; i < 32; i++) {
@@ -399,8 +415,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample(const __grid_const
         if (!own_i) continue;
         uint64_t jj = __shfl_sync(0xffffffffu, j, i);
         double tt = __shfl_sync(0xffffffffu, tl, i);
-        bool tail = false;
-        if (jj >= A.nblocks) {
+        bool tail = __shfl_sync(0xffffffffu, ptail, i);
+        const uint64_t lb = __shfl_sync(0xffffffffu, lblk, i);
+        if (!perm && jj >= A.nblocks) {
             // rounding past this rank's total: last block with non-zero mass, last non-zero amp
             tail = true;
             uint64_t hiblk = A.nblocks;
@@ -420,7 +437,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample(const __grid_const
         }
         const double prev = jj > 0 ? A.inc[jj - 1] : 0.0;
         const double tp = tt - prev;
-        const float2* blk = A.amps + jj * B;
+        const float2* blk = A.amps + (perm ? lb : jj) * B;
         double p0 = 0.0, p1 = 0.0;
         if (B == 64) {
             const float4 v = reinterpret_cast<const float4*>(blk)[lane];
@@ -452,7 +469,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample(const __grid_const
             const bool second = __shfl_sync(0xffffffffu, p1 > 0.0, L);
             amp = 2 * L + (second ? 1 : 0);
         }
-        if (lane == i) result = A.base_index + jj * B + (uint64_t)amp;
+        if (lane == i) result = (perm ? 0 : A.base_index) + jj * B + (uint64_t)amp;
     }
     if (valid) A.x_out[s] = owned ? result : 0ull;
 }
@@ -462,15 +479,56 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_sample(const __grid_const
 // ------------------------------------------------------------------------------------
 constexpr int kXebGrid = 148 * 2;
 
+// logical index x -> (owning rank, local offset).  Canonical layout: rank = x >> nl.  Kept
+// (permuted) layout: the logical block x >> b maps to the physical global block through the
+// byte tables ptab[c][256] (bit permutation, positions < b fixed).
+__device__ __forceinline__ uint64_t perm_block(const uint64_t* __restrict__ ptab, uint64_t lb) {
+    uint64_t r = 0;
+#pragma unroll
+    for (int c = 0; c < kPermTables; c++) r |= __ldg(ptab + 256 * c + ((lb >> (8 * c)) & 255));
+    return r;
+}
+__device__ __forceinline__ bool locate(const Locator& L, uint64_t x, uint64_t* off) {
+    if (!L.ptab) {
+        *off = x & ((1ull << L.nl) - 1);
+        return (x >> L.nl) == L.rank;
+    }
+    const uint64_t pb = perm_block(L.ptab, x >> L.b);
+    *off = ((pb & ((1ull << (L.nl - L.b)) - 1)) << L.b) | (x & ((1ull << L.b) - 1));
+    return (pb >> (L.nl - L.b)) == L.rank;
+}
+
+__global__ void __launch_bounds__(kThreads) k_perm_blocks(const double* __restrict__ in, double* __restrict__ out,
+                                                          uint64_t n, const uint64_t* __restrict__ ptab) {
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kThreads)
+        out[i] = in[perm_block(ptab, i)];
+}
+
+// index of the last block with non-zero mass (inc strictly increasing there), or 0
+__global__ void __launch_bounds__(kThreads) k_last_nonzero(const double* __restrict__ inc, uint64_t n,
+                                                           unsigned long long* __restrict__ out) {
+    unsigned long long best = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kThreads) {
+        const double prev = i > 0 ? inc[i - 1] : 0.0;
+        if (inc[i] > prev && i > best) best = i;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y > best ? y : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
 __global__ void __launch_bounds__(kThreads) k_xeb(const float2* __restrict__ a, const unsigned long long* __restrict__ x,
-                                                  uint64_t count, int nl, uint64_t rank, int nbits,
+                                                  uint64_t count, const Locator L, int nbits,
                                                   double* __restrict__ part, int* __restrict__ bad) {
     double s = 0.0, s2 = 0.0, c = 0.0;
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < count; i += (uint64_t)gridDim.x * kThreads) {
         const uint64_t xi = x[i];
         if (nbits < 64 && (xi >> nbits) != 0) { atomicOr(bad, 1); continue; }
-        if ((xi >> nl) != rank) continue;
-        const float2 v = a[xi & ((1ull << nl) - 1)];
+        uint64_t off;
+        if (!locate(L, xi, &off)) continue;
+        const float2 v = a[off];
         const double p = (double)v.x * v.x + (double)v.y * v.y;
         s += p;
         s2 += p * p;
@@ -499,15 +557,16 @@ __global__ void k_xeb_final(const double* __restrict__ part, int grid, double* _
 }
 
 __global__ void __launch_bounds__(kThreads) k_gather_prob(const float2* __restrict__ a, const unsigned long long* __restrict__ x,
-                                                          uint64_t count, int nl, uint64_t rank, int nbits,
+                                                          uint64_t count, const Locator L, int nbits,
                                                           double* __restrict__ p, int* __restrict__ bad) {
     for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < count; i += (uint64_t)gridDim.x * kThreads) {
         const uint64_t xi = x[i];
         double r = 0.0;
+        uint64_t off;
         if (nbits < 64 && (xi >> nbits) != 0) {
             atomicOr(bad, 1);
-        } else if ((xi >> nl) == rank) {
-            const float2 v = a[xi & ((1ull << nl) - 1)];
+        } else if (locate(L, xi, &off)) {
+            const float2 v = a[off];
             r = (double)v.x * v.x + (double)v.y * v.y;
         }
         p[i] = r;
@@ -639,10 +698,10 @@ cudaError_t sample(const SampleArgs& a, cudaStream_t st) {
 
 int xeb_grid() { return kXebGrid; }
 
-cudaError_t xeb_partials(const float2* amps, const unsigned long long* x, uint64_t count, int nl, uint64_t rank,
+cudaError_t xeb_partials(const float2* amps, const unsigned long long* x, uint64_t count, const Locator& L,
                          int nbits, double* part, int* bad, cudaStream_t st) {
     note_launch();
-    k_xeb<<<kXebGrid, kThreads, 0, st>>>(amps, x, count, nl, rank, nbits, part, bad);
+    k_xeb<<<kXebGrid, kThreads, 0, st>>>(amps, x, count, L, nbits, part, bad);
     return cudaGetLastError();
 }
 
@@ -652,11 +711,25 @@ cudaError_t xeb_finalize(const double* part, int grid, double* out3, cudaStream_
     return cudaGetLastError();
 }
 
-cudaError_t gather_prob(const float2* amps, const unsigned long long* x, uint64_t count, int nl, uint64_t rank,
+cudaError_t gather_prob(const float2* amps, const unsigned long long* x, uint64_t count, const Locator& L,
                         int nbits, double* p, int* bad, cudaStream_t st) {
     if (count == 0) return cudaSuccess;
     note_launch();
-    k_gather_prob<<<grid_for(count), kThreads, 0, st>>>(amps, x, count, nl, rank, nbits, p, bad);
+    k_gather_prob<<<grid_for(count), kThreads, 0, st>>>(amps, x, count, L, nbits, p, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t perm_blocks(const double* in, double* out, uint64_t n, const uint64_t* ptab, cudaStream_t st) {
+    note_launch();
+    k_perm_blocks<<<grid_for(n, 148u * 64u), kThreads, 0, st>>>(in, out, n, ptab);
+    return cudaGetLastError();
+}
+
+cudaError_t last_nonzero(const double* inc, uint64_t n, unsigned long long* out, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    k_last_nonzero<<<grid_for(n, 148u * 16u), kThreads, 0, st>>>(inc, n, out);
     return cudaGetLastError();
 }
 

@@ -87,6 +87,12 @@ struct SampleArgs {
     const double* u_in;     // optional caller uniforms (chunk-local), else SplitMix64
     uint64_t base_index;    // rank * 2^n_local
     unsigned long long* x_out;  // chunk-local, 0 for shots owned by other ranks
+    // kept permuted layout: inc is the GLOBAL logical block prefix (nblocks = 2^(n-b)), every
+    // rank searches every shot, the owner of the found block (per ptab) does the in-block scan
+    const uint64_t* ptab;   // nullptr: canonical layout
+    int nl;                 // local index bits
+    uint64_t rank;
+    uint64_t last_block;    // last logical block with non-zero mass (tail fallback)
 };
 // a11 (K7): per-shot binary search over block prefixes + warp-cooperative in-block scan
 cudaError_t sample(const SampleArgs& a, cudaStream_t st);
@@ -94,13 +100,26 @@ cudaError_t sample(const SampleArgs& a, cudaStream_t st);
 // a13 (K8): per-CTA partial (sum p, sum p^2, count) over owned bitstrings; bad_flag set if
 // any x >= 2^n.  Returns grid size used.
 int xeb_grid();
-cudaError_t xeb_partials(const float2* amps, const unsigned long long* x, uint64_t count, int n_local_bits,
-                         uint64_t rank, int n_bits, double* part /* 3*grid */, int* bad_flag, cudaStream_t st);
+// where a logical index lives: canonical (ptab == nullptr: rank = x >> nl) or a kept permuted
+// layout (ptab = kPermTables x 256 byte tables mapping logical block bits to physical ones)
+constexpr int kPermTables = 5;   // logical block index up to 40 bits
+struct Locator {
+    int nl;                 // local index bits
+    uint64_t rank;
+    int b;                  // block bits (positions < b are the same physically and logically)
+    const uint64_t* ptab;
+};
+cudaError_t xeb_partials(const float2* amps, const unsigned long long* x, uint64_t count, const Locator& L,
+                         int n_bits, double* part /* 3*grid */, int* bad_flag, cudaStream_t st);
 cudaError_t xeb_finalize(const double* part, int grid, double* out3, cudaStream_t st);
 
 // p_out[i] = |a_{x_i}|^2 if x_i is on this rank else 0
-cudaError_t gather_prob(const float2* amps, const unsigned long long* x, uint64_t count, int n_local_bits,
-                        uint64_t rank, int n_bits, double* p_out, int* bad_flag, cudaStream_t st);
+cudaError_t gather_prob(const float2* amps, const unsigned long long* x, uint64_t count, const Locator& L,
+                        int n_bits, double* p, int* bad_flag, cudaStream_t st);
+// out[lb] = in[perm(lb)] for lb < n (logical block order from physical); ptab as in Locator
+cudaError_t perm_blocks(const double* in, double* out, uint64_t n, const uint64_t* ptab, cudaStream_t st);
+// *out = last index with inc[i] > inc[i-1] (0 if none)
+cudaError_t last_nonzero(const double* inc, uint64_t n, unsigned long long* out, cudaStream_t st);
 
 cudaError_t init_basis(float2* amps, uint64_t n_amps, int set_one, cudaStream_t st);
 

@@ -416,6 +416,8 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         P.n_passes++;
     }
 
+    P.restore_begin = (int)P.items.size();
+    P.final_pos = pos;
     // ---- 3. final restore: globals home
     for (int round = 0; round < 3 && n_global > 0; round++) {
         std::vector<std::pair<int, int>> pairs;

@@ -30,18 +30,22 @@ def main():
     for name, (text, k) in CASES.items():
         c = rcs.Circuit.from_qasm(text)
         n = c.n_qubits
-        st = rcs.State.build(ctx, c, fuse_k=k, timing=True, staging_bytes=1 << 20)
-        shard = torch.from_numpy(st.copy_out().view(np.float32).copy()).cuda()
-        parts = [torch.empty_like(shard) for _ in range(world)] if True else None
-        dist.all_gather(parts, shard)
+        keep = name.endswith("_keep")
+        st = rcs.State.build(ctx, c, fuse_k=k, timing=True, staging_bytes=1 << 20, keep_layout=keep)
+        report = dict(st.report)
         x = st.sample(20000, seed=SHOT_SEED)
         xr = st.xeb(x)
         p = st.probabilities(x[:100])
+        if keep:
+            st.canonicalize()
+        shard = torch.from_numpy(st.copy_out().view(np.float32).copy()).cuda()
+        parts = [torch.empty_like(shard) for _ in range(world)]
+        dist.all_gather(parts, shard)
         if rank == 0:
             full = torch.cat(parts).cpu().numpy().view(np.complex64)
             np.save(os.path.join(os.environ["MGPU_OUT"], f"{name}_state.npy"), full)
             np.save(os.path.join(os.environ["MGPU_OUT"], f"{name}_x.npy"), x)
-            results[name] = {"n": n, "xeb": xr, "report": st.report, "p": p.tolist(), "norm": st.norm}
+            results[name] = {"n": n, "xeb": xr, "report": report, "p": p.tolist(), "norm": st.norm}
         st.free()
     if rank == 0:
         with open(os.path.join(os.environ["MGPU_OUT"], "results.json"), "w") as f:

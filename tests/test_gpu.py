@@ -92,6 +92,34 @@ def test_virtual_global_bitwise_equals_single(rcs, ctx, g):
     check_amps(psig, ref)
 
 
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_keep_layout_matches_canonical(rcs, ctx, g):
+    """keep_layout skips the final restore; the logical-order CDF over the permuted layout gives
+    the same T, shots, probabilities and XEB bit for bit (same block sums, same scan order), and
+    canonicalize() then yields the canonical amplitudes."""
+    text = emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=10 + g))
+    c = rcs.Circuit.from_qasm(text)
+    can = rcs.State.build(ctx, c, virtual_global=g)
+    kept = rcs.State.build(ctx, c, virtual_global=g, keep_layout=True)
+    assert kept.report["layout_kept"] == 1
+    assert kept.report["n_remaps"] + kept.report["n_swaps"] < can.report["n_remaps"] + can.report["n_swaps"]
+    assert kept.norm == can.norm
+    xa = can.sample(200_000, seed=SHOT_SEED)
+    xb = kept.sample(200_000, seed=SHOT_SEED)
+    assert np.array_equal(xa, xb)
+    u = oracle.uniforms(4, 3000)
+    u[:3] = [0.0, 1.0 - 2.0 ** -53, 0.5]
+    assert np.array_equal(can.sample_uniforms(u), kept.sample_uniforms(u))
+    assert np.array_equal(can.probabilities(xa[:5000]), kept.probabilities(xa[:5000]))
+    assert can.xeb(xa) == kept.xeb(xa)
+    with pytest.raises(rcs.RcsError) as e:
+        kept.copy_out()
+    assert e.value.status == "RCS_ERR_ARG"
+    kept.canonicalize()
+    assert np.array_equal(kept.copy_out(), can.copy_out())
+    assert np.array_equal(kept.sample(10_000, seed=1), can.sample(10_000, seed=1))
+
+
 def test_empty_and_tiny_circuits(rcs, ctx):
     for n in (1, 2, 3, 7):
         st, psi = gpu_state(rcs, ctx, f"OPENQASM 2.0;\nqreg q[{n}];\n")

@@ -25,6 +25,7 @@ CASES = {
     "grid20_k6": (emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=3)), 6),
     "c2_k6": (config_qasm("c2"), 6),
     "grid26_k6": (emit_qasm(generate(2, 13, 14, "ABCD", seed=5)), 6),
+    "c2_k6_keep": (config_qasm("c2"), 6),          # keep_layout: no final restore
 }
 
 
@@ -56,7 +57,7 @@ def test_sharded_build_sample_xeb(world, mode, tmp_path, cuda_ok):
     import paper_2512_07311_b200 as rcs
     ctx = rcs.Context(0)
     for name, (text, k) in CASES.items():
-        full = np.load(tmp_path / f"{name}_state.npy")
+        full = np.load(tmp_path / f"{name}_state.npy")      # (keep cases: after canonicalize)
         single = rcs.State.build(ctx, rcs.Circuit.from_qasm(text), fuse_k=k)
         ref1 = single.copy_out()
         assert np.array_equal(full, ref1), name            # bitwise P-invariance
@@ -69,6 +70,7 @@ def test_sharded_build_sample_xeb(world, mode, tmp_path, cuda_ok):
             assert rep["n_pipelined"] > 0, rep
         if mode in ("p2p_seq", "nccl") or k == 4:
             assert rep["n_pipelined"] == 0, rep
+        assert rep["layout_kept"] == (1 if name.endswith("_keep") else 0), rep
         x = np.load(tmp_path / f"{name}_x.npy")
         xs = single.sample(20000, seed=SHOT_SEED)
         u = oracle.uniforms(SHOT_SEED, 20000)
