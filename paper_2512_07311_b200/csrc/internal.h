@@ -60,6 +60,7 @@ struct Plan {
     // physical position of qubit q before them (>= n - n_global: a rank bit)
     int restore_begin = 0;
     std::vector<int> final_pos;
+    std::vector<int> initial_pos;   // empty: canonical start (qubit q at position q)
 };
 
 // low physical positions never moved by remaps: keeps qubit 0 at bit 0 (the CUDA-core pass
@@ -74,6 +75,7 @@ constexpr int kFuseSeeds = 4;
 // fuser: pick among the seeds by the block count of a greedy completion (rollout)
 constexpr bool kFuseLookahead = true;
 constexpr bool kRemapPrefetch = true;   // remaps also bring in soon-needed global qubits
+constexpr bool kInitialPlacement = true;   // start with the latest-used qubits global (free: |0> state)
 
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err);
 

@@ -344,6 +344,30 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         auto it = std::lower_bound(uses[q].begin(), uses[q].end(), from);
         return it == uses[q].end() ? INT_MAX : *it;
     };
+    // initial layout: |0...0> is invariant under qubit permutations, so the global positions may
+    // start with any qubits at no cost -- take the movable ones whose first use is latest
+    if (kInitialPlacement && n_global > 0) {
+        std::vector<int> movable;
+        for (int q = kPinnedLow; q < n; q++) movable.push_back(q);
+        std::stable_sort(movable.begin(), movable.end(), [&](int a, int b2) {
+            const int fa = next_use(a, 0), fb = next_use(b2, 0);
+            if (fa != fb) return fa > fb;
+            return a > b2;
+        });
+        std::vector<int> want(movable.begin(), movable.begin() + n_global);
+        std::vector<int> freeg;   // global positions whose qubit is not wanted
+        for (int G = n_local; G < n; G++)
+            if (!std::count(want.begin(), want.end(), occ[G])) freeg.push_back(G);
+        size_t fi = 0;
+        for (int q : want) {
+            if (pos[q] >= n_local) continue;
+            const int G = freeg[fi++], L = pos[q], qg = occ[G];
+            std::swap(occ[G], occ[L]);
+            pos[q] = G;
+            pos[qg] = L;
+        }
+        P.initial_pos = pos;
+    }
     auto emit_remap = [&](const std::vector<std::pair<int, int>>& pairs) {
         Item it;
         it.type = RCS_ITEM_REMAP;
