@@ -35,14 +35,15 @@ struct rcs_context {
     std::shared_ptr<const rcs::TcPack> tc_hold;   // keeps that pack alive
     // remaps over NVLink: CUDA-IPC mappings of the peers' shards (re-checked every build)
     bool p2p = false;                 // every peer mappable
+    bool p2p_stage = false;           // and every peer's pull staging area too
     char* d_xchg = nullptr;           // device buffer for the handle all-gather
-    cudaIpcMemHandle_t peer_handle[8];
-    uint64_t peer_off[8] = {0};
-    void* peer_map[8] = {nullptr};
+    cudaIpcMemHandle_t peer_handle[2][8];   // [0] amplitude shards, [1] pull staging
+    uint64_t peer_off[2][8] = {};
+    void* peer_map[2][8] = {};
     float* d_bar = nullptr;           // 1-float all-reduce used as a stream-ordered barrier
     // pipelined remaps (f1): a second stream for the chunked peer swaps + per-chunk events
     cudaStream_t xstream = nullptr;
-    cudaEvent_t ev_a[16] = {}, ev_s[16] = {};
+    cudaEvent_t ev_a[16] = {}, ev_s[16] = {}, ev_p[16] = {}, ev_b[16] = {};
     // sampling / XEB chunk buffers, shared by every state of this context
     unsigned long long* xbuf = nullptr;
     double* dbuf = nullptr;
@@ -81,11 +82,14 @@ struct rcs_state {
     uint64_t* ptab = nullptr;        // logical -> physical block byte tables (device)
     uint64_t nblocks_all = 0;
     uint64_t last_block = 0;
+    float2* pull_stage = nullptr;    // 2 x pull_stage_elems (world >= 4)
+    uint64_t pull_stage_elems = 0;
 };
 
 namespace {
 
 constexpr uint64_t kChunkShots = 1ull << 22;
+constexpr int kPullCb = 3;   // pull-mode remaps: 8 chunks
 constexpr uint64_t kAlign = 256;
 
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -130,6 +134,7 @@ struct Layout {
     bool kept = false;
     uint64_t nblocks_all = 0, gbuf_off = 0, ptab_off = 0;
     uint64_t stage_end = 0;
+    uint64_t pull_off = 0, pull_elems = 0;   // world >= 4: 2 x pull_elems complex64
 };
 
 // keep: a kept (permuted) final layout is possible (keep_layout and world > 1 or virtual global)
@@ -151,6 +156,11 @@ Layout scratch_layout(int nl, int world, int virt, uint64_t staging_bytes, int b
     if (world > 1) st = staging_bytes ? staging_bytes : (256ull << 20);
     uint64_t end = align_up(L.stage_off + st);
     L.stage_end = end;
+    if (world >= 4) {   // pull-mode remaps: outgoing elements of one 2^-kPullCb chunk, twice
+        L.pull_elems = (1ull << (nl - kPullCb)) / (uint64_t)world * (uint64_t)(world - 1);
+        L.pull_off = end;
+        end = align_up(L.pull_off + 2 * L.pull_elems * 8);
+    }
     if (L.kept) {
         L.gbuf_off = end;
         L.ptab_off = align_up(L.gbuf_off + L.nblocks_all * 8);
@@ -250,8 +260,10 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
 // --- NVLink peer mapping -----------------------------------------------------------------
 typedef int (*PFN_getAddressRange)(unsigned long long*, size_t*, unsigned long long);
 
-rcs_status setup_peers(rcs_context* c, void* amps, rcs_error* err) {
+// Maps every peer's amplitude shard (buffer 0) and, if given, its pull staging area (buffer 1).
+rcs_status setup_peers(rcs_context* c, void* amps, rcs_error* err, void* stage = nullptr) {
     c->p2p = false;
+    c->p2p_stage = false;
     if (getenv("RCS_REMAP_NCCL")) return RCS_OK;   // force the NCCL send/recv path
     for (int r = 0; r < c->world; r++) {
         if (r == c->rank) continue;
@@ -269,47 +281,82 @@ rcs_status setup_peers(rcs_context* c, void* amps, rcs_error* err) {
             return RCS_OK;
         get_range = (PFN_getAddressRange)fn;
     }
-    unsigned long long base = 0;
-    size_t size = 0;
-    if (get_range(&base, &size, (unsigned long long)amps) != 0) return RCS_OK;
     struct Rec {
-        cudaIpcMemHandle_t h;
-        uint64_t off;
-        int ok;
+        cudaIpcMemHandle_t h[2];
+        uint64_t off[2];
+        int ok[2];
+        int same;   // buffer 1 lies in buffer 0's allocation
     } mine{};
-    mine.off = (uint64_t)amps - base;
-    mine.ok = cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess;
-    if (!mine.ok) cudaGetLastError();
+    unsigned long long base[2] = {0, 0};
+    void* bufs[2] = {amps, stage};
+    for (int i = 0; i < 2; i++) {
+        if (!bufs[i]) continue;
+        size_t size = 0;
+        if (get_range(&base[i], &size, (unsigned long long)bufs[i]) != 0) {
+            if (i == 0) return RCS_OK;
+            continue;
+        }
+        mine.off[i] = (uint64_t)bufs[i] - base[i];
+        if (i == 1 && base[1] == base[0]) {
+            mine.same = 1;
+            mine.ok[1] = 1;
+            continue;
+        }
+        mine.ok[i] = cudaIpcGetMemHandle(&mine.h[i], (void*)base[i]) == cudaSuccess;
+        if (!mine.ok[i]) cudaGetLastError();
+    }
     const size_t rec = (sizeof(Rec) + 15) / 16 * 16;
-    if (!c->d_xchg) CUDA_TRY(cudaMalloc(&c->d_xchg, rec * (c->world + 1)));
+    if (!c->d_xchg) CUDA_TRY(cudaMalloc(&c->d_xchg, rec * (8 + 1)));
     if (!c->d_bar) CUDA_TRY(cudaMalloc(&c->d_bar, 16));
     CUDA_TRY(cudaMemcpyAsync(c->d_xchg, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
     NCCL_TRY(ncclAllGather(c->d_xchg, c->d_xchg + rec, rec, ncclChar, c->comm, c->stream));
     std::vector<char> all(rec * c->world);
     CUDA_TRY(cudaMemcpyAsync(all.data(), c->d_xchg + rec, rec * c->world, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    bool ok = true;
-    for (int r = 0; r < c->world; r++) ok = ok && reinterpret_cast<Rec*>(all.data() + rec * r)->ok;
-    if (!ok) return RCS_OK;
+    bool ok0 = true, ok1 = stage != nullptr;
+    for (int r = 0; r < c->world; r++) {
+        const Rec* pr = reinterpret_cast<const Rec*>(all.data() + rec * r);
+        ok0 = ok0 && pr->ok[0];
+        ok1 = ok1 && pr->ok[1];
+    }
+    if (!ok0) return RCS_OK;
+    auto open = [&](int r, int i, const cudaIpcMemHandle_t& h, void** out) -> bool {
+        // cached by handle; the same allocation may back both buffers
+        for (int j = 0; j < 2; j++)
+            if (c->peer_map[j][r] && std::memcmp(&c->peer_handle[j][r], &h, sizeof h) == 0) {
+                *out = c->peer_map[j][r];
+                return true;
+            }
+        void* mp = nullptr;
+        if (cudaIpcOpenMemHandle(&mp, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        *out = mp;
+        return true;
+    };
     for (int r = 0; r < c->world; r++) {
         if (r == c->rank) continue;
         const Rec* pr = reinterpret_cast<const Rec*>(all.data() + rec * r);
-        if (c->peer_map[r] && std::memcmp(&c->peer_handle[r], &pr->h, sizeof pr->h) == 0) {
-            c->peer_off[r] = pr->off;
-            continue;
+        void* m0 = nullptr;
+        void* m1 = nullptr;
+        if (!open(r, 0, pr->h[0], &m0)) return RCS_OK;
+        if (ok1 && !pr->same && !open(r, 1, pr->h[1], &m1)) ok1 = false;
+        if (ok1 && pr->same) m1 = m0;
+        // close mappings no longer referenced
+        for (int j = 0; j < 2; j++) {
+            void* old = c->peer_map[j][r];
+            if (old && old != m0 && old != m1 && old != c->peer_map[1 - j][r]) cudaIpcCloseMemHandle(old);
         }
-        if (c->peer_map[r]) cudaIpcCloseMemHandle(c->peer_map[r]);
-        c->peer_map[r] = nullptr;
-        void* mp = nullptr;
-        if (cudaIpcOpenMemHandle(&mp, pr->h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
-            return RCS_OK;
-        }
-        c->peer_map[r] = mp;
-        c->peer_handle[r] = pr->h;
-        c->peer_off[r] = pr->off;
+        c->peer_map[0][r] = m0;
+        c->peer_handle[0][r] = pr->h[0];
+        c->peer_off[0][r] = pr->off[0];
+        c->peer_map[1][r] = ok1 ? m1 : nullptr;
+        c->peer_handle[1][r] = pr->same ? pr->h[0] : pr->h[1];
+        c->peer_off[1][r] = pr->off[1];
     }
     c->p2p = true;
+    c->p2p_stage = ok1;
     return RCS_OK;
 }
 
@@ -350,12 +397,52 @@ void make_swap_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint
             if ((code >> i) & 1) mask |= 1ull << it.b[i];
         }
         const int pc = A.npeers++;
-        A.peer[pc] = reinterpret_cast<float2*>(static_cast<char*>(c->peer_map[peer]) + c->peer_off[peer]);
+        A.peer[pc] = reinterpret_cast<float2*>(static_cast<char*>(c->peer_map[0][peer]) + c->peer_off[0][peer]);
         A.mask[pc] = mask;
         const uint64_t half = count / 2;
         A.m_begin[pc] = c->rank < peer ? 0 : half;
         A.m_count[pc] = c->rank < peer ? half : count - half;
         *bytes_sent += count * 8ull;
+    }
+}
+
+// Pull-mode arguments for one chunk: peers in ascending code order (the same order every rank
+// uses for its staging groups, so my group on peer p is at index my_code - (my_code > code_p)).
+void make_pull_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint64_t fixval, int buf,
+                    dev::PullArgs& A, uint64_t* bytes_sent) {
+    rcs_context* c = s->ctx;
+    const int j = it.k, nl = s->nl;
+    A = dev::PullArgs{};
+    A.local = s->amps;
+    A.j = j;
+    int lpos[8];
+    for (int i = 0; i < j; i++) lpos[i] = it.b[i];
+    std::sort(lpos, lpos + j);
+    for (int i = 0; i < j; i++) A.lpos[i] = lpos[i];
+    A.nfix = nfix;
+    for (int i = 0; i < nfix; i++) A.fix[i] = fix[i];
+    A.fixval = fixval;
+    A.count = 1ull << (nl - j - nfix);
+    const uint64_t group_elems = A.count;   // per peer
+    A.stage = s->pull_stage + (size_t)buf * s->pull_stage_elems;
+    int my_code = 0;
+    for (int i = 0; i < j; i++) my_code |= ((c->rank >> (it.a[i] - nl)) & 1) << i;
+    for (int code = 0; code < (1 << j); code++) {
+        if (code == my_code) continue;
+        int peer = c->rank;
+        uint64_t mask = 0;
+        for (int i = 0; i < j; i++) {
+            const int gb = it.a[i] - nl;
+            peer = (peer & ~(1 << gb)) | (((code >> i) & 1) << gb);
+            if ((code >> i) & 1) mask |= 1ull << it.b[i];
+        }
+        const int pc = A.npeers++;
+        A.mask[pc] = mask;
+        const int slot = my_code - (my_code > code ? 1 : 0);
+        const float2* base = reinterpret_cast<const float2*>(static_cast<char*>(c->peer_map[1][peer]) +
+                                                             c->peer_off[1][peer]);
+        A.peer_stage[pc] = base + (size_t)buf * s->pull_stage_elems + (size_t)slot * group_elems;
+        *bytes_sent += A.count * 8ull;
     }
 }
 
@@ -386,8 +473,9 @@ struct Span {   // timing: item time += sign * elapsed(a, b)
 };
 
 rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, const PassRef* pb, const int* fix,
-                              int cb, int reserve, uint64_t* bytes_sent, uint64_t* pass_bytes, size_t ia, size_t ir,
-                              size_t ib, std::vector<Span>* spans, std::vector<cudaEvent_t>* owned, rcs_error* err) {
+                              int cb, int reserve, bool pull, uint64_t* bytes_sent, uint64_t* pass_bytes, size_t ia,
+                              size_t ir, size_t ib, std::vector<Span>* spans, std::vector<cudaEvent_t>* owned,
+                              rcs_error* err) {
     rcs_context* c = s->ctx;
     const int nch = 1 << cb;
     if (!c->xstream) CUDA_TRY(cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
@@ -410,16 +498,44 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
     };
     const int sms = std::max(1, c->num_sms - reserve);
     cudaEvent_t t0 = spans ? tev(c->stream) : nullptr;
-    // A: all chunks, in order, on the main stream
+    if (pull) {
+        for (int ch = 0; ch < nch; ch++) {
+            if (!c->ev_p[ch]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_p[ch], cudaEventDisableTiming));
+            if (!c->ev_b[ch]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_b[ch], cudaEventDisableTiming));
+        }
+    }
+    // A: all chunks, in order, on the main stream.  Pull mode: pack(c) follows A(c) on the main
+    // stream (all SMs), pull(c) runs on xstream after a barrier.  The staging is double-buffered:
+    // pack(c) waits for barrier(c-1), which every peer passes only after its pull(c-2) from the
+    // same buffer.
     for (int ch = 0; ch < nch; ch++) {
         if (pa) {
             CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch)));
         }
         CUDA_TRY(cudaEventRecord(c->ev_a[ch], c->stream));
+        if (pull) {
+            dev::PullArgs A;
+            make_pull_args(s, it, fix, cb, fixval(ch), ch & 1, A, bytes_sent);
+            if (ch >= 2) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_b[ch - 1], 0));
+            CUDA_TRY(dev::remap_pack(A, c->stream));
+            CUDA_TRY(cudaEventRecord(c->ev_p[ch], c->stream));
+            CUDA_TRY(cudaStreamWaitEvent(c->xstream, c->ev_p[ch], 0));
+            rcs_status st = stream_barrier(c, c->xstream, err);
+            if (st) return st;
+            CUDA_TRY(cudaEventRecord(c->ev_b[ch], c->xstream));
+            A.max_grid = reserve * 8;
+            CUDA_TRY(dev::remap_pull(A, c->xstream));
+            CUDA_TRY(cudaEventRecord(c->ev_s[ch], c->xstream));
+        }
     }
     if (pa) *pass_bytes += 16ull * s->n_amps;
     cudaEvent_t tA = spans ? tev(c->stream) : nullptr;
     if (spans && pa) spans->push_back({ia, t0, tA, 1});
+    if (pull) {
+        rcs_status st = stream_barrier(c, c->xstream, err);   // peers done reading my staging
+        if (st) return st;
+        CUDA_TRY(cudaEventRecord(c->ev_b[0], c->xstream));
+    } else {
     // swaps: chunk by chunk on xstream
     for (int ch = 0; ch < nch; ch++) {
         dev::PeerSwapArgs A;
@@ -433,7 +549,8 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
         if (st) return st;
         CUDA_TRY(cudaEventRecord(c->ev_s[ch], c->xstream));
     }
-    // B: chunk c after every rank swapped chunk c
+    }
+    // B: chunk c after every rank exchanged chunk c
     for (int ch = 0; ch < nch; ch++) {
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
         if (pb) {
@@ -447,6 +564,7 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
         }
     }
     if (pb) *pass_bytes += 16ull * s->n_amps;
+    if (pull) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_b[0], 0));   // final barrier
     if (spans) spans->push_back({ir, tA, tev(c->stream), 1});
     return RCS_OK;
 }
@@ -784,8 +902,10 @@ rcs_status rcs_context_create(int device, int rank, int world, const void* nccl_
 void rcs_context_free(rcs_context* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    for (int r = 0; r < 8; r++)
-        if (c->peer_map[r]) cudaIpcCloseMemHandle(c->peer_map[r]);
+    for (int r = 0; r < 8; r++) {
+        if (c->peer_map[0][r]) cudaIpcCloseMemHandle(c->peer_map[0][r]);
+        if (c->peer_map[1][r] && c->peer_map[1][r] != c->peer_map[0][r]) cudaIpcCloseMemHandle(c->peer_map[1][r]);
+    }
     if (c->d_xchg) cudaFree(c->d_xchg);
     if (c->d_bar) cudaFree(c->d_bar);
     if (c->xbuf) cudaFree(c->xbuf);
@@ -793,10 +913,9 @@ void rcs_context_free(rcs_context* c) {
     if (c->xeb_part) cudaFree(c->xeb_part);
     if (c->bad) cudaFree(c->bad);
     if (c->d_tc) cudaFree(c->d_tc);
-    for (int i = 0; i < 16; i++) {
-        if (c->ev_a[i]) cudaEventDestroy(c->ev_a[i]);
-        if (c->ev_s[i]) cudaEventDestroy(c->ev_s[i]);
-    }
+    for (int i = 0; i < 16; i++)
+        for (cudaEvent_t e : {c->ev_a[i], c->ev_s[i], c->ev_p[i], c->ev_b[i]})
+            if (e) cudaEventDestroy(e);
     if (c->xstream) cudaStreamDestroy(c->xstream);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
@@ -882,6 +1001,10 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     s->staging = reinterpret_cast<float2*>(sc + L.stage_off);
     s->staging_elems = (L.stage_end - L.stage_off) / sizeof(float2);
     s->plan = plan_ptr;
+    if (L.pull_elems) {
+        s->pull_stage = reinterpret_cast<float2*>(sc + L.pull_off);
+        s->pull_stage_elems = L.pull_elems;
+    }
     // keep_layout: skip the restore items when the final layout is not canonical
     bool keep = false;
     if (L.kept) {
@@ -959,7 +1082,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         ctx->tc_cap = tc_words;
     }
     if (ctx->world > 1 && P.n_remaps > 0) {
-        rcs_status r = setup_peers(ctx, s->amps, err);
+        rcs_status r = setup_peers(ctx, s->amps, err, s->pull_stage);
         if (r) return fail(r);
     }
     BUILD_TRY(cudaEventRecord(eb0, stream));
@@ -982,6 +1105,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     static const int ov_on = getenv("RCS_OVERLAP") ? atoi(getenv("RCS_OVERLAP")) : 1;
     static const int ov_cb = getenv("RCS_OVERLAP_CHUNKS") ? atoi(getenv("RCS_OVERLAP_CHUNKS")) : 2;
     static const int ov_res = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 32;
+    static const int ov_pull = getenv("RCS_REMAP_PULL") ? atoi(getenv("RCS_REMAP_PULL")) : 1;
     auto is_tc = [&](size_t i) { return i < n_exec && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
     auto tc_ref = [&](size_t i) {
         return PassRef{tcp->pos[i].data(), ctx->d_tc + (size_t)tc_slot[i] * tc_words_each};
@@ -1000,10 +1124,14 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
                 if (has_a) excl |= dev::tc_reserved_mask(nl, tcp->pos[ii].data());
                 if (has_b) excl |= dev::tc_reserved_mask(nl, tcp->pos[ir + 1].data());
                 int fix[4];
-                if ((has_a || has_b) && choose_chunk_bits(nl, excl, ov_cb, fix)) {
+                // world >= 4: pull mode (8 chunks) when every rank's staging is mapped
+                const bool pull = ov_pull && ctx->world >= 4 && ctx->p2p_stage && s->pull_stage &&
+                                  (1ull << (nl - kPullCb)) / (1ull << rm.k) * ((1ull << rm.k) - 1) <= s->pull_stage_elems;
+                const int cbg = pull ? kPullCb : ov_cb;
+                if ((has_a || has_b) && cbg <= 4 && choose_chunk_bits(nl, excl, cbg, fix)) {
                     PassRef ra = has_a ? tc_ref(ii) : PassRef{}, rb = has_b ? tc_ref(ir + 1) : PassRef{};
-                    rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, has_b ? &rb : nullptr, fix, ov_cb,
-                                                      ov_res, &remap_bytes, &pass_bytes, ii, ir, ir + 1,
+                    rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, has_b ? &rb : nullptr, fix, cbg,
+                                                      ov_res, pull, &remap_bytes, &pass_bytes, ii, ir, ir + 1,
                                                       o.timing ? &spans : nullptr, &owned, err);
                     if (r) return fail(r);
                     n_pipelined++;

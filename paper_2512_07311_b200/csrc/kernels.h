@@ -61,6 +61,27 @@ struct PeerSwapArgs {
 };
 cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st);
 
+// Pull-mode remap (world >= 4: remote reads outrun mixed read/write swaps on NVSwitch):
+// pack copies this rank's outgoing elements of one chunk to its staging area, grouped by
+// destination ([pc][m], contiguous); pull reads each peer's group for this rank from the
+// peer's staging and writes it to the positions the outgoing elements came from.
+struct PullArgs {
+    float2* local;
+    float2* stage;               // this rank's staging (pack target)
+    const float2* peer_stage[7]; // peers' staging areas (pull sources), already offset to my slot
+    int npeers;
+    int j;
+    int lpos[8];                 // remapped local positions, ascending
+    uint64_t mask[7];            // local L-bit pattern of the elements exchanged with peer pc
+    int nfix;
+    int fix[4];                  // chunk positions (ascending) and value
+    uint64_t fixval;
+    uint64_t count;              // elements per peer in this chunk (even)
+    int max_grid;
+};
+cudaError_t remap_pack(const PullArgs& a, cudaStream_t st);
+cudaError_t remap_pull(const PullArgs& a, cudaStream_t st);
+
 // a9 (K5): bsum[blk] = sum_{x in blk} |a_x|^2 (fp64) for blocks of 2^b amps; part[c] = per-CTA
 // partial sum of p^2 (fixed grid => deterministic).  Returns the number of partials used.
 int block_sums_grid();
