@@ -112,7 +112,8 @@ typedef struct {
     int n_pipelined;         /* remaps run as chunked NVLink swaps overlapped with the adjacent
                                 tensor-core passes; env RCS_OVERLAP=0 disables,
                                 RCS_OVERLAP_CHUNKS = log2 chunks (default 2), RCS_OVERLAP_SMS =
-                                SMs left to the swaps (default 32)                              */
+                                SMs left to the swaps (default 32); RCS_REMAP_PULL=1 (world >= 4):
+                                staged pulls instead of in-place swaps (measured slower at N=4) */
 } rcs_build_report;
 
 typedef struct {

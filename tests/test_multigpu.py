@@ -34,7 +34,7 @@ def ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-MODES = ["p2p", "p2p_swap", "p2p_seq", "p2p_c8", "nccl"]
+MODES = ["p2p", "p2p_pull", "p2p_seq", "p2p_c8", "nccl"]
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -51,8 +51,8 @@ def test_sharded_build_sample_xeb(world, mode, tmp_path, cuda_ok):
         env["RCS_OVERLAP"] = "0"      # peer swaps not pipelined with the neighbouring passes
     elif mode == "p2p_c8":
         env["RCS_OVERLAP_CHUNKS"] = "3"   # 8 pipeline chunks
-    elif mode == "p2p_swap":
-        env["RCS_REMAP_PULL"] = "0"       # in-place swaps also at world >= 4 (default: staged pulls)
+    elif mode == "p2p_pull":
+        env["RCS_REMAP_PULL"] = "1"       # staged pulls at world >= 4 (default: in-place swaps)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                         "--master-addr", "127.0.0.1", "--master-port", str(29500 + world + 10 * MODES.index(mode)),
                         os.path.join(ROOT, "tests", "mgpu_worker.py")], env=env, capture_output=True, text=True,
@@ -71,7 +71,7 @@ def test_sharded_build_sample_xeb(world, mode, tmp_path, cuda_ok):
         assert np.abs(d).max() <= 1e-5 and np.linalg.norm(d) <= 1e-5
         rep = res[name]["report"]
         assert rep["n_remaps"] > 0 or world == 1
-        if k == 6 and mode in ("p2p", "p2p_swap", "p2p_c8"):
+        if k == 6 and mode in ("p2p", "p2p_pull", "p2p_c8"):
             assert rep["n_pipelined"] > 0, rep
         if mode in ("p2p_seq", "nccl") or k == 4:
             assert rep["n_pipelined"] == 0, rep
