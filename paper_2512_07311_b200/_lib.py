@@ -34,7 +34,7 @@ class rcs_build_report(C.Structure):
                 ("pass_ms_min", C.c_double), ("pass_ms_max", C.c_double), ("remap_ms", C.c_double),
                 ("blocksum_ms", C.c_double), ("pass_bytes", C.c_uint64), ("remap_bytes", C.c_uint64),
                 ("norm", C.c_double), ("n_tc_passes", C.c_int), ("swap_ms", C.c_double),
-                ("layout_kept", C.c_int), ("n_pipelined", C.c_int)]
+                ("layout_kept", C.c_int), ("n_pipelined", C.c_int), ("n_paired", C.c_int)]
 
 
 class rcs_sample_report(C.Structure):

@@ -43,6 +43,9 @@ struct rcs_context {
     float* d_bar = nullptr;           // 1-float all-reduce used as a stream-ordered barrier
     // pipelined remaps (f1): a second stream for the chunked peer swaps + per-chunk events
     cudaStream_t xstream = nullptr;
+    // paired tensor-core passes (K11): per-chunk completion counters
+    unsigned* d_done = nullptr;
+    uint64_t done_cap = 0;
     cudaEvent_t ev_a[16] = {}, ev_s[16] = {}, ev_p[16] = {}, ev_b[16] = {};
     // sampling / XEB chunk buffers, shared by every state of this context
     unsigned long long* xbuf = nullptr;
@@ -90,6 +93,7 @@ namespace {
 
 constexpr uint64_t kChunkShots = 1ull << 22;
 constexpr int kPullCb = 3;   // pull-mode remaps: 8 chunks
+constexpr int kPairMaxChunkBits = 19;   // paired passes: chunk <= 2^19 amplitudes (4 MB)
 constexpr uint64_t kAlign = 256;
 
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -917,6 +921,7 @@ void rcs_context_free(rcs_context* c) {
         for (cudaEvent_t e : {c->ev_a[i], c->ev_s[i], c->ev_p[i], c->ev_b[i]})
             if (e) cudaEventDestroy(e);
     if (c->xstream) cudaStreamDestroy(c->xstream);
+    if (c->d_done) cudaFree(c->d_done);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -1097,7 +1102,9 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     if (keep)
         BUILD_TRY(cudaMemcpyAsync(s->ptab, ptab_host.data(), ptab_host.size() * 8, cudaMemcpyHostToDevice, stream));
     uint64_t pass_bytes = 0, remap_bytes = 0;
-    int n_pipelined = 0;
+    int n_pipelined = 0, n_paired = 0;
+    std::vector<size_t> half_span;   // paired launches: the span is split evenly over both passes
+    const int tc_pair = getenv("RCS_TC_PAIR") ? atoi(getenv("RCS_TC_PAIR")) : 1;   // read per build (tests toggle it)
     std::vector<float> mbuf;
     std::vector<Span> spans;
     std::vector<cudaEvent_t> owned;
@@ -1145,6 +1152,38 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             BUILD_TRY(cudaEventCreate(&e0));
             owned.push_back(e0);
             BUILD_TRY(cudaEventRecord(e0, stream));
+        }
+        // two consecutive tensor-core passes in one launch (K11): pass B re-reads pass A's output
+        // from L2 chunk by chunk, one HBM round trip for both
+        if (tc_pair && is_tc(ii) && is_tc(ii + 1)) {
+            const int* pp[2] = {tcp->pos[ii].data(), tcp->pos[ii + 1].data()};
+            const int cbits = dev::tc_multi_chunk_bits(nl, 2, pp);
+            if (cbits > 0 && cbits <= kPairMaxChunkBits && nl - cbits >= 4) {
+                const uint64_t need = 1ull << (nl - cbits);
+                if (ctx->done_cap < need) {
+                    if (ctx->d_done) cudaFree(ctx->d_done);
+                    ctx->d_done = nullptr;
+                    ctx->done_cap = 0;
+                    BUILD_TRY(cudaMalloc(&ctx->d_done, need * sizeof(unsigned)));
+                    ctx->done_cap = need;
+                }
+                const uint32_t* aa[2] = {ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
+                                         ctx->d_tc + (size_t)tc_slot[ii + 1] * tc_words_each};
+                BUILD_TRY(dev::gate_pass_tc_multi(s->amps, nl, 2, pp, aa, ctx->num_sms, ctx->d_done, ctx->done_cap,
+                                                  stream));
+                pass_bytes += 32ull * n_amps;   // algorithmic: two passes (HBM sees one round trip)
+                n_paired++;
+                if (o.timing) {
+                    cudaEvent_t e1;
+                    BUILD_TRY(cudaEventCreate(&e1));
+                    owned.push_back(e1);
+                    BUILD_TRY(cudaEventRecord(e1, stream));
+                    spans.push_back({ii, e0, e1, 1});
+                    half_span.push_back(ii);
+                }
+                ii++;
+                continue;
+            }
         }
         if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
             BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tcp->pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
@@ -1212,6 +1251,10 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             if (sp.a && sp.b) cudaEventElapsedTime(&t, sp.a, sp.b);
             item_ms[sp.item] += sp.sign * (double)t;
         }
+        for (size_t ii : half_span) {
+            item_ms[ii] *= 0.5;
+            item_ms[ii + 1] = item_ms[ii];
+        }
         for (size_t ii = 0; ii < n_exec; ii++) {
             const double t = item_ms[ii];
             if (P.items[ii].type == RCS_ITEM_PASS) {
@@ -1236,6 +1279,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     R.norm = s->T_total;
     R.n_tc_passes = n_tc;
     R.n_pipelined = n_pipelined;
+    R.n_paired = n_paired;
     if (rep) *rep = R;
     *out = s;
     return RCS_OK;

@@ -24,6 +24,13 @@ cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const u
                          cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0);
 // positions a chunk bit must avoid for this pass: the 12-bit tile sub-cube and the bit above its run
 uint64_t tc_reserved_mask(int n_local_bits, const int* pos);
+// K11: np (1 or 2) consecutive 6-qubit passes in one launch; pass B re-reads pass A's output
+// from L2 chunk by chunk.  done: >= 2^(nl - chunk_bits) zeroed-by-us counters.
+// tc_multi_chunk_bits: |union of both passes' sub-cubes and pair bits| (-1 if invalid).
+int tc_multi_chunk_bits(int n_local_bits, int np, const int* const* pos);
+cudaError_t gate_pass_tc_multi(float2* amps, int n_local_bits, int np, const int* const* pos,
+                               const uint32_t* const* d_a, int num_sms, unsigned* done, uint64_t done_cap,
+                               cudaStream_t st);
 
 // a6 (K1) fused dense gate pass: amps <- M (x) over every group of 2^k amplitudes that
 // differ only in the physical bits pos[0..k) (matrix bit i <-> pos[i]); M is 2^k x 2^k

@@ -65,7 +65,7 @@ constexpr uint32_t kCtlBytes = 2560;   // barriers + offset tables; total <= 227
 static_assert(18 * 8 + 3 * 64 * 8 + 24 * 4 + 2 * 64 * 2 <= 2560, "control block overflow");
 constexpr uint32_t kSmemBytes = kRaw * kRawBytes + kStages * kStageBytes + kStagingBytes + kCtlBytes;
 #ifndef RCS_TC_ACCS
-#define RCS_TC_ACCS 3                        // accumulators per D buffer (precision / energy trade)
+#define RCS_TC_ACCS 2                        // accumulators per D buffer (= K11's, so pairing never changes a result)
 #endif
 constexpr int kAccs = RCS_TC_ACCS;
 constexpr int kAccCols = kAccs * TN;         // one D buffer
@@ -518,6 +518,405 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// =====================================================================================
+// K11: the same pass applied to 1 or 2 consecutive blocks in ONE launch (fewer
+// HBM round trips).  The index space is cut into chunks: C = both passes' 12-bit tile
+// sub-cubes and their pair bits r; a chunk fixes the remaining (H) positions, so it holds
+// complete tiles of both passes.  Groups of gs CTAs own chunks (chunk k -> group k mod
+// ngroups); a CTA walks A(k_0), A(k_1), B(k_0), A(k_2), B(k_1), ... over its share of each
+// chunk's tile pairs.  Pass A's outputs are stored with the default (L2-allocating) policy and
+// pass B reads them back from L2 once every member of the group has finished A(k) (per-chunk
+// completion counter, release/acquire at gpu scope; all CTAs are co-resident).  HBM traffic:
+// one read and one write per amplitude for both passes.  Arithmetic per tile is identical to
+// K9 (same MMA sequence, same epilogue sums), so pairing never changes a result.
+struct TcPass {
+    const uint32_t* a;       // packed A (hi, lo)
+    int pos[6];              // physical position of matrix bit i
+    int jpos[6];             // 6 lowest non-target positions
+    int sub[12];             // tile sub-cube positions, ascending
+    int r;                   // first position outside the sub-cube (tile-pair bit)
+    int rot;                 // converters use lane-rotated reads (>= 2 targets in the 4 lowest cube bits)
+    int nw;                  // within-chunk tile positions, ascending (wpos[0] == r)
+    int wpos[12];
+    int sso[32];             // staging offset (floats) of sub-cube index 128 i
+    uint64_t sgo[32];        // global offset (amplitudes) of sub-cube index 128 i
+};
+struct TcMulti {
+    float2* amps;
+    int np;                  // passes in this launch (1 or 2)
+    TcPass ps[2];
+    int nh;                  // chunk-index positions, ascending
+    int hpos[48];
+    uint64_t nchunks;
+    uint64_t npairs;         // tile pairs per chunk per pass
+    int gs;                  // CTAs per group
+    unsigned* done;          // [nchunks] pass-A completion counters (np == 2), zeroed by the host
+};
+
+__device__ __forceinline__ uint64_t pdep_pos(uint64_t x, const int* pos, int n) {
+    uint64_t r = 0;
+    for (int i = 0; i < n; i++) r |= ((x >> i) & 1ull) << pos[i];
+    return r;
+}
+
+// the tile sequence every role of a CTA walks (identically)
+struct TcSched {
+    uint64_t g, m, gsz, ngroups, nchunks, npairs;
+    int np;
+    int s, ph, h;            // ph 0: pass A on chunk(s); ph 1: pass B on chunk(s - 1)
+    uint64_t u;
+    bool live;
+    __device__ uint64_t chunk_of(int ss) const { return g + (uint64_t)ss * ngroups; }
+    __device__ bool phase_ok() const {
+        return ph == 0 ? chunk_of(s) < nchunks : (s >= 1 && chunk_of(s - 1) < nchunks);
+    }
+    // phases in order (s, 0), (s, 1), (s + 1, 0), ...; (s, 1) exists only for np == 2.  After the
+    // last chunk of this group both phases of a step are empty, and so are all later ones.
+    __device__ void normalize() {
+        while (live) {
+            if (phase_ok() && u < npairs) return;
+            if (np == 2 && ph == 0) {
+                ph = 1;
+            } else {
+                s++;
+                ph = 0;
+            }
+            u = m;
+            if (ph == 0 && chunk_of(s) >= nchunks && (np == 1 || s < 1 || chunk_of(s - 1) >= nchunks)) live = false;
+        }
+    }
+    __device__ void begin() { s = 0; ph = 0; h = 0; u = m; live = true; normalize(); }
+    __device__ void advance() {
+        h ^= 1;
+        if (h) return;
+        u += gsz;
+        normalize();
+    }
+    __device__ uint64_t chunk() const { return ph == 0 ? chunk_of(s) : chunk_of(s - 1); }
+};
+
+__global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_constant__ TcMulti p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    float2* raw = reinterpret_cast<float2*>(smem);
+    uint8_t* stages = smem + kRaw * kRawBytes;
+    float* staging = reinterpret_cast<float*>(stages + kStages * kStageBytes);
+    uint8_t* ctl = reinterpret_cast<uint8_t*>(staging) + kStagingBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ctl);   // [kStages]
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;                    // [2]
+    uint64_t* tempty = tfull + 2;
+    uint64_t* rfull = tempty + 2;                         // [2] raw pair slots
+    uint64_t* rempty = rfull + 2;
+    uint64_t* offr = rempty + 2;                          // [2][64] run offsets per pass
+    uint16_t* soft = reinterpret_cast<uint16_t*>(offr + 128);   // [2][64]
+    uint16_t* sofj = soft + 128;                                 // [2][64]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sofj + 128);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; s++) {
+            mbar_init(&full[s], kLoadWarps * 32);
+            mbar_init(&empty[s], 1);
+        }
+        for (int d = 0; d < 2; d++) {
+            mbar_init(&tfull[d], 1);
+            mbar_init(&tempty[d], kEpiThreads);
+        }
+        for (int r = 0; r < 2; r++) {
+            mbar_init(&rfull[r], 1);
+            mbar_init(&rempty[r], 2 * kLoadWarps * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (threadIdx.x < 64 * p.np) {
+        const int x = threadIdx.x & 63, P = threadIdx.x >> 6;
+        const TcPass& q = p.ps[P];
+        uint64_t orr = 0;
+        int st = 0, sj = 0;
+        for (int i = 0; i < 6; i++) {
+            int rt = 0, rj = 0;
+            for (int b = 0; b < 12; b++) {
+                rt += q.sub[b] < q.pos[i];
+                rj += q.sub[b] < q.jpos[i];
+            }
+            if ((x >> i) & 1) {
+                st |= 1 << rt;
+                sj |= 1 << rj;
+            }
+        }
+        for (int b = q.r; b < 12; b++)
+            if ((x >> (b - q.r)) & 1) orr |= 1ull << q.sub[b];
+        offr[64 * P + x] = orr;
+        const int lowm = (1 << q.r) - 1;
+        soft[64 * P + x] = (uint16_t)(((st & ~lowm) << 1) | (st & lowm));
+        sofj[64 * P + x] = (uint16_t)(((sj & ~lowm) << 1) | (sj & lowm));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    // TMEM: A of pass P at [128 P, 128 P + 128) (hi, lo); D[d] at 256 + 128 d (2 accumulators)
+    if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+        const int q = warp - kEpiWarp0;
+        const int m = q * 32 + lane;
+        for (int P = 0; P < p.np; P++)
+            for (int h = 0; h < 2; h++)
+                for (int c0 = 0; c0 < 64; c0 += 32) {
+                    uint32_t r[32];
+                    const uint4* src =
+                        reinterpret_cast<const uint4*>(p.ps[P].a + (size_t)h * 128 * 64 + (size_t)m * 64 + c0);
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {
+                        const uint4 v = __ldg(src + c);
+                        r[4 * c] = v.x;
+                        r[4 * c + 1] = v.y;
+                        r[4 * c + 2] = v.z;
+                        r[4 * c + 3] = v.w;
+                    }
+                    TMEM_ST32(tmem + ((uint32_t)(q * 32) << 16) + 128 * P + h * 64 + c0, r);
+                }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    TcSched sc0;
+    {
+        const uint64_t gs = (uint64_t)p.gs;
+        sc0.ngroups = (gridDim.x + gs - 1) / gs;
+        sc0.g = blockIdx.x / gs;
+        sc0.m = blockIdx.x % gs;
+        const uint64_t g0 = sc0.g * gs;
+        sc0.gsz = (uint64_t)gridDim.x - g0 < gs ? (uint64_t)gridDim.x - g0 : gs;
+        sc0.nchunks = p.nchunks;
+        sc0.npairs = p.npairs;
+        sc0.np = p.np;
+        sc0.begin();
+    }
+    auto tile_base = [&](const TcSched& sc) {
+        const TcPass& q = p.ps[sc.ph];
+        return pdep_pos(2 * sc.u + (uint64_t)sc.h, q.wpos, q.nw) | pdep_pos(sc.chunk(), p.hpos, p.nh);
+    };
+
+    if (warp == kProdWarp) {
+        // ---------------- TMA producer: both tiles of a pair
+        TcSched sc = sc0;
+        uint64_t it = 0;
+        int wait_s = -1;
+        for (; sc.live; sc.advance(), it++) {
+            if (sc.h) continue;   // odd half: copied with its pair
+            const TcPass& q = p.ps[sc.ph];
+            if (sc.ph == 1 && sc.s != wait_s) {
+                // pass B reads pass A's output of this chunk: every member of the group must be done
+                wait_s = sc.s;
+                if (lane == 0) {
+                    const unsigned* cnt = p.done + sc.chunk();
+                    unsigned v;
+                    while (true) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+                        if (v >= (unsigned)sc.gsz) break;
+                        __nanosleep(256);
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                __syncwarp();
+            }
+            const int slot = (it >> 1) & 1;
+            const uint64_t use = it >> 2;
+            mbar_wait(&rempty[slot], (use & 1) ^ 1);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[slot])),
+                             "r"(kRawBytes * 2)
+                             : "memory");
+            __syncwarp();
+            const int nruns = 1 << (12 - q.r);
+            const uint32_t copy_bytes = (8u << q.r) * 2u;
+            const float2* src = p.amps + tile_base(sc);
+            const uint32_t dst = su32(raw + (size_t)slot * 8192);
+            for (int u = lane; u < nruns; u += 32)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dst + u * copy_bytes),
+                    "l"(src + offr[64 * sc.ph + u]), "r"(copy_bytes), "r"(su32(&rfull[slot]))
+                    : "memory");
+        }
+    } else if (warp < kLoadWarps) {
+        // ---------------- converters: thread = column j, target octets `to` and `to + 4`
+        const int lt = threadIdx.x;
+        const int j = lt & 63;
+        const int to = lt >> 6;
+        TcSched sc = sc0;
+        uint64_t it = 0;
+        for (; sc.live; sc.advance(), it++) {
+            const int P = sc.ph;
+            const TcPass& q = p.ps[P];
+            const int rho = q.rot ? (lane & 7) : 0;
+            const int sj = sofj[64 * P + j];
+            const int slot = (it >> 1) & 1;
+            const uint64_t use = it >> 2;
+            mbar_wait(&rfull[slot], use & 1);
+            const float2* rb = raw + (size_t)slot * 8192 + (sc.h ? (1 << q.r) : 0);
+            float2 b[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                b[i] = f2mul(rb[soft[64 * P + 8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj], 32768.f);
+            mbar_arrive(&rempty[slot]);
+            const int s = it % kStages;
+            mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+            uint8_t* bhi = stages + s * kStageBytes;
+            uint8_t* blo = bhi + kBBytes;
+#pragma unroll
+            for (int g = 0; g < 2; g++) {
+                uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+                for (int e2 = 0; e2 < 4; e2++) {
+                    const float2 v0 = b[8 * g + 2 * e2], v1 = b[8 * g + 2 * e2 + 1];
+                    split_h2(v0.x, v1.x, rh[e2], rl[e2]);
+                    split_h2(v0.y, v1.y, ih[e2], il[e2]);
+                }
+                if (q.rot) {
+                    rot_h8(rh, rho);
+                    rot_h8(rl, rho);
+                    rot_h8(ih, rho);
+                    rot_h8(il, rho);
+                }
+                const int c = to + 4 * g;
+                const uint32_t ore = bchunk(j, c), oim = bchunk(j, c + 8);
+                *reinterpret_cast<uint4*>(bhi + ore) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
+                *reinterpret_cast<uint4*>(bhi + oim) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
+                *reinterpret_cast<uint4*>(blo + ore) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+                *reinterpret_cast<uint4*>(blo + oim) = make_uint4(il[0], il[1], il[2], il[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&full[s]);
+        }
+    } else if (warp == kMmaWarp) {
+        // ---------------- MMA issuer (2 accumulators: cross terms + hh k-steps 0-3, hh k-steps 4-7)
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        TcSched sc = sc0;
+        uint64_t it = 0;
+        for (; sc.live; sc.advance(), it++) {
+            const int s = it % kStages, d = it & 1;
+            mbar_wait(&full[s], (it / kStages) & 1);
+            mbar_wait(&tempty[d], ((it >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                const uint32_t sb = su32(stages + s * kStageBytes);
+                const uint32_t d0 = tmem + 256 + d * 2 * TN;
+                const uint64_t bh0 = bdesc(sb), bl0 = bdesc(sb + kBBytes);
+                const uint32_t ah = tmem + 128 * sc.ph, al = ah + 64;
+                MMA_F16(d0, ah, bl0, idesc, 0);
+                MMA_F16(d0, al, bh0, idesc, 1);
+#pragma unroll
+                for (int ks = 1; ks < TK / 16; ks++) {
+                    MMA_F16(d0, ah + ks * 8, bl0 + ks * 16, idesc, 1);
+                    MMA_F16(d0, al + ks * 8, bh0 + ks * 16, idesc, 1);
+                }
+#pragma unroll
+                for (int ks = 0; ks < 4; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                MMA_F16(d0 + TN, ah + 4 * 8, bh0 + 4 * 16, idesc, 0);
+#pragma unroll
+                for (int ks = 5; ks < 8; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&empty[s])));
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&tfull[d])));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
+        // ---------------- epilogue
+        const int q4 = warp & 3;
+        const int et = threadIdx.x - kEpiWarp0 * 32;
+        const int m = q4 * 32 + lane;
+        const int trow = m >> 1, comp = m & 1;
+        const float* sld[2];
+        uint64_t gb[2];
+        for (int P = 0; P < 2; P++) {   // sub-cube index et -> (t, j, global offset) per pass
+            const TcPass& q = p.ps[P < p.np ? P : 0];
+            int t = 0, jj = 0;
+            uint64_t go = 0;
+            for (int b = 0; b < 12; b++) {
+                if (!((et >> b) & 1)) continue;
+                go |= 1ull << q.sub[b];
+                for (int i = 0; i < 6; i++) {
+                    if (q.pos[i] == q.sub[b]) t |= 1 << i;
+                    if (q.jpos[i] == q.sub[b]) jj |= 1 << i;
+                }
+            }
+            sld[P] = staging + t * kPitchF + 2 * jj;
+            gb[P] = go;
+        }
+        float* st = staging + trow * kPitchF + comp;
+        TcSched sc = sc0;
+        uint64_t it = 0;
+        for (; sc.live; it++) {
+            const int d = it & 1;
+            const int P = sc.ph;
+            mbar_wait(&tfull[d], (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float us = 1.f / (16384.f * 32768.f);
+            const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + 256 + d * 2 * TN;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                uint32_t a0[32], a1[32];
+                TMEM_LD32(ta + 32 * h, a0);
+                TMEM_LD32(ta + TN + 32 * h, a1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+                if (h == 1) {
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(&tempty[d]);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    float o0, o1;   // (acc0 + acc1) * 2^-29
+                    asm("{\n.reg .b64 x, y, u;\n"
+                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\n"
+                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\n"
+                        "mov.b64 {%0, %1}, x;\n}"
+                        : "=f"(o0), "=f"(o1)
+                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(us));
+                    st[2 * (32 * h + c)] = o0;
+                    st[2 * (32 * h + c) + 2] = o1;
+                }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const TcPass& q = p.ps[P];
+            float2* dst = p.amps + (tile_base(sc) | gb[P]);
+            const float* sl = sld[P];
+            if (P == 0 && p.np == 2) {   // re-read by pass B from L2: default (allocating) stores
+#pragma unroll 8
+                for (int i = 0; i < 32; i++) dst[q.sgo[i]] = *reinterpret_cast<const float2*>(sl + q.sso[i]);
+            } else {
+#pragma unroll 8
+                for (int i = 0; i < 32; i++) __stcs(dst + q.sgo[i], *reinterpret_cast<const float2*>(sl + q.sso[i]));
+            }
+            TcSched nx = sc;
+            nx.advance();
+            if (p.np == 2 && P == 0 && !(nx.live && nx.ph == 0 && nx.s == sc.s)) {
+                // this CTA's last pass-A tile of the chunk: publish after all epilogue stores
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (et == 0) {
+                    unsigned* cnt = p.done + sc.chunk();
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+                }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // staging reused by the next tile
+            sc = nx;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 }  // namespace
 
 size_t tc_matrix_words() { return 2 * 128 * 64; }
@@ -654,6 +1053,121 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
         k_pass_tc<true><<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
     else
         k_pass_tc<false><<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
+    return cudaGetLastError();
+}
+
+
+namespace {
+// per-pass tables of K11 (same derivation as gate_pass_tc)
+bool fill_pass(TcPass& q, int nl, const int* pos, const uint32_t* d_a, uint64_t* submask) {
+    q = TcPass{};
+    q.a = d_a;
+    uint64_t tmask = 0;
+    for (int i = 0; i < 6; i++) {
+        q.pos[i] = pos[i];
+        tmask |= 1ull << pos[i];
+    }
+    int nj = 0;
+    for (int b = 0; b < nl && nj < 6; b++)
+        if (!((tmask >> b) & 1)) q.jpos[nj++] = b;
+    if (nj != 6) return false;
+    int na = 0;
+    uint64_t sm = 0;
+    for (int b = 0; b < nl && na < 12; b++) {
+        bool in = (tmask >> b) & 1;
+        for (int i = 0; i < 6; i++) in = in || q.jpos[i] == b;
+        if (in) {
+            q.sub[na++] = b;
+            sm |= 1ull << b;
+        }
+    }
+    if (na != 12) return false;
+    q.r = 0;
+    while (q.r < 12 && q.sub[q.r] == q.r) q.r++;
+    if (q.r >= nl) return false;
+    for (int i = 0; i < 32; i++) {
+        const int sidx = 128 * i;
+        int t = 0, jj = 0;
+        uint64_t go = 0;
+        for (int b = 0; b < 12; b++) {
+            if (!((sidx >> b) & 1)) continue;
+            go |= 1ull << q.sub[b];
+            for (int k = 0; k < 6; k++) {
+                if (q.pos[k] == q.sub[b]) t |= 1 << k;
+                if (q.jpos[k] == q.sub[b]) jj |= 1 << k;
+            }
+        }
+        q.sso[i] = t * kPitchF + 2 * jj;
+        q.sgo[i] = go;
+    }
+    int low_targets = 0;
+    for (int i = 0; i < 4; i++) low_targets += (int)((tmask >> q.sub[i]) & 1);
+    q.rot = low_targets >= 2 ? 1 : 0;
+    *submask = sm;
+    return true;
+}
+}  // namespace
+
+int tc_multi_chunk_bits(int nl, int np, const int* const* pos) {
+    uint64_t c = 0;
+    for (int P = 0; P < np; P++) {
+        TcPass q;
+        uint64_t sm;
+        if (!fill_pass(q, nl, pos[P], nullptr, &sm)) return -1;
+        c |= sm | (1ull << q.r);
+    }
+    return __builtin_popcountll(c);
+}
+
+cudaError_t gate_pass_tc_multi(float2* amps, int nl, int np, const int* const* pos, const uint32_t* const* d_a,
+                               int num_sms, unsigned* done, uint64_t done_cap, cudaStream_t st) {
+    if (np < 1 || np > 2 || nl < 13) return cudaErrorInvalidValue;
+    TcMulti m{};
+    m.amps = amps;
+    m.np = np;
+    uint64_t cmask = 0, sub[2] = {0, 0};
+    for (int P = 0; P < np; P++) {
+        if (!fill_pass(m.ps[P], nl, pos[P], d_a[P], &sub[P])) return cudaErrorInvalidValue;
+        cmask |= sub[P] | (1ull << m.ps[P].r);
+    }
+    const int nc = __builtin_popcountll(cmask);
+    for (int P = 0; P < np; P++) {
+        TcPass& q = m.ps[P];
+        q.nw = 0;
+        for (int b = 0; b < nl; b++)
+            if (((cmask >> b) & 1) && !((sub[P] >> b) & 1)) q.wpos[q.nw++] = b;
+        if (q.nw != nc - 12 || q.wpos[0] != q.r || q.nw > 12) return cudaErrorInvalidValue;
+    }
+    m.nh = 0;
+    for (int b = 0; b < nl; b++)
+        if (!((cmask >> b) & 1)) m.hpos[m.nh++] = b;
+    m.nchunks = 1ull << m.nh;
+    m.npairs = 1ull << (nc - 13);
+    uint64_t grid = (uint64_t)num_sms;
+    if (np == 1) {
+        m.gs = 1;
+        if (grid > m.nchunks * m.npairs) grid = m.nchunks * m.npairs;
+    } else {
+        // group size: keep ~2 chunks per group in flight within ~64 MB of L2
+        const uint64_t chunk_bytes = 8ull << nc;
+        uint64_t gs = (grid * 2 * chunk_bytes + (64ull << 20) - 1) / (64ull << 20);
+        if (gs < 4) gs = 4;
+        if (gs > m.npairs) gs = m.npairs;
+        if (gs > grid) gs = grid;
+        m.gs = (int)gs;
+        if (!done || done_cap < m.nchunks) return cudaErrorInvalidValue;
+        m.done = done;
+        cudaError_t e = cudaMemsetAsync(done, 0, m.nchunks * sizeof(unsigned), st);
+        if (e != cudaSuccess) return e;
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_pass_tc_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    count_launch();
+    k_pass_tc_multi<<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(m);
     return cudaGetLastError();
 }
 

@@ -92,6 +92,36 @@ def test_virtual_global_bitwise_equals_single(rcs, ctx, g):
     check_amps(psig, ref)
 
 
+@pytest.mark.parametrize("case", ["c2", "grid20", "rand17", "rand19", "c3"])
+def test_paired_passes_bitwise_equal(rcs, ctx, case, monkeypatch):
+    """K11 runs two consecutive tensor-core passes per launch (pass B re-reads pass A's output
+    from L2 chunk by chunk); its per-tile arithmetic is K9's, so the state must be bit-identical
+    to one pass per launch -- on small and full-size (C3, n=32) states."""
+    text = {"c2": config_qasm("c2"), "grid20": emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=8)),
+            "rand17": random_qasm(17, 220, 5), "rand19": random_qasm(19, 260, 6), "c3": config_qasm("c3")}[case]
+    c = rcs.Circuit.from_qasm(text)
+    paired = rcs.State.build(ctx, c, fuse_k=6)
+    assert paired.report["n_paired"] > 0
+    xa = paired.sample(100_000, seed=SHOT_SEED)
+    if case == "c3":
+        head_a = paired.copy_out(0, 1 << 22)
+        tail_a = paired.copy_out((1 << 32) - (1 << 22), 1 << 22)
+    else:
+        psi_a = paired.copy_out()
+    del paired
+    monkeypatch.setenv("RCS_TC_PAIR", "0")
+    single = rcs.State.build(ctx, c, fuse_k=6)
+    assert single.report["n_paired"] == 0
+    if case == "c3":
+        assert np.array_equal(head_a, single.copy_out(0, 1 << 22))
+        assert np.array_equal(tail_a, single.copy_out((1 << 32) - (1 << 22), 1 << 22))
+    else:
+        assert np.array_equal(psi_a, single.copy_out())
+        if case != "c3":
+            check_amps(psi_a.astype(np.complex128), oracle.build_state(text))
+    assert np.array_equal(xa, single.sample(100_000, seed=SHOT_SEED))
+
+
 @pytest.mark.parametrize("g", [1, 2, 3])
 def test_keep_layout_matches_canonical(rcs, ctx, g):
     """keep_layout skips the final restore; the logical-order CDF over the permuted layout gives
