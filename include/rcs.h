@@ -115,7 +115,7 @@ typedef struct {
                                 SMs left to the swaps (default 32); RCS_REMAP_PULL=1 (world >= 4):
                                 staged pulls instead of in-place swaps (measured slower at N=4) */
     int n_paired;            /* launches that ran two consecutive tensor-core passes (K11, one HBM
-                                round trip for both; env RCS_TC_PAIR=0 disables)               */
+                                round trip for both; experimental, env RCS_TC_PAIR=1 enables)  */
 } rcs_build_report;
 
 typedef struct {

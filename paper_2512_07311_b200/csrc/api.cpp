@@ -93,7 +93,7 @@ namespace {
 
 constexpr uint64_t kChunkShots = 1ull << 22;
 constexpr int kPullCb = 3;   // pull-mode remaps: 8 chunks
-constexpr int kPairMaxChunkBits = 19;   // paired passes: chunk <= 2^19 amplitudes (4 MB)
+constexpr int kPairMaxChunkBits = 18;   // paired passes: chunk <= 2^18 amplitudes (2 MB)
 constexpr uint64_t kAlign = 256;
 
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -1104,7 +1104,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     uint64_t pass_bytes = 0, remap_bytes = 0;
     int n_pipelined = 0, n_paired = 0;
     std::vector<size_t> half_span;   // paired launches: the span is split evenly over both passes
-    const int tc_pair = getenv("RCS_TC_PAIR") ? atoi(getenv("RCS_TC_PAIR")) : 1;   // read per build (tests toggle it)
+    // K11 pairing is off by default: measured no faster than one pass per launch
+    const int tc_pair = getenv("RCS_TC_PAIR") ? atoi(getenv("RCS_TC_PAIR")) : 0;   // read per build (tests toggle it)
     std::vector<float> mbuf;
     std::vector<Span> spans;
     std::vector<cudaEvent_t> owned;
@@ -1158,7 +1159,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         if (tc_pair && is_tc(ii) && is_tc(ii + 1)) {
             const int* pp[2] = {tcp->pos[ii].data(), tcp->pos[ii + 1].data()};
             const int cbits = dev::tc_multi_chunk_bits(nl, 2, pp);
-            if (cbits > 0 && cbits <= kPairMaxChunkBits && nl - cbits >= 4) {
+            const int max_bits = getenv("RCS_PAIR_MAXBITS") ? atoi(getenv("RCS_PAIR_MAXBITS")) : kPairMaxChunkBits;
+            if (cbits > 0 && cbits <= max_bits && nl - cbits >= 4) {
                 const uint64_t need = 1ull << (nl - cbits);
                 if (ctx->done_cap < need) {
                     if (ctx->d_done) cudaFree(ctx->d_done);

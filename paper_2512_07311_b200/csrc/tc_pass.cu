@@ -538,6 +538,8 @@ struct TcPass {
     int rot;                 // converters use lane-rotated reads (>= 2 targets in the 4 lowest cube bits)
     int nw;                  // within-chunk tile positions, ascending (wpos[0] == r)
     int wpos[12];
+    uint64_t wmask;          // their mask
+    uint64_t wstep;          // deposit of 2 gs (the member's pair stride)
     int sso[32];             // staging offset (floats) of sub-cube index 128 i
     uint64_t sgo[32];        // global offset (amplitudes) of sub-cube index 128 i
 };
@@ -547,9 +549,12 @@ struct TcMulti {
     TcPass ps[2];
     int nh;                  // chunk-index positions, ascending
     int hpos[48];
+    uint64_t hmask;          // their mask
+    uint64_t hstep;          // deposit of ngroups (a group's chunk stride)
     uint64_t nchunks;
     uint64_t npairs;         // tile pairs per chunk per pass
     int gs;                  // CTAs per group
+    int depth;               // chunk-steps between a chunk's pass A and its pass B
     unsigned* done;          // [nchunks] pass-A completion counters (np == 2), zeroed by the host
 };
 
@@ -559,40 +564,78 @@ __device__ __forceinline__ uint64_t pdep_pos(uint64_t x, const int* pos, int n) 
     return r;
 }
 
-// the tile sequence every role of a CTA walks (identically)
+// masked increment of a deposited index: pdep(x + y, M) = ((pdep(x, M) | ~M) + pdep(y, M)) & M
+__device__ __forceinline__ uint64_t dep_add(uint64_t dx, uint64_t dy, uint64_t mask) { return ((dx | ~mask) + dy) & mask; }
+
+// The tile sequence every role of a CTA walks (identically): step s = pass A on chunk(s), then
+// pass B on chunk(s - depth); `depth` chunk-steps of other work between a chunk's pass A and its
+// pass B hide the pipeline latency and the group members' skew.  With BASE the walker also keeps
+// the deposited tile base incrementally (a few 64-bit ops per tile).
+template <bool BASE>
 struct TcSched {
-    uint64_t g, m, gsz, ngroups, nchunks, npairs;
-    int np;
-    int s, ph, h;            // ph 0: pass A on chunk(s); ph 1: pass B on chunk(s - 1)
+    const TcMulti* p;
+    uint64_t g, m, ngroups;
+    int s, ph, h;            // ph 0: pass A on chunk(s); ph 1: pass B on chunk(s - depth)
     uint64_t u;
     bool live;
+    uint64_t dW;             // deposit of 2u into the current pass's within-chunk positions
+    uint64_t dHa;            // deposit of chunk(s)
+    uint64_t dHb;            // deposit of chunk(s - depth) (valid once s >= depth)
+    uint64_t dH0;            // deposit of chunk(0) = g
     __device__ uint64_t chunk_of(int ss) const { return g + (uint64_t)ss * ngroups; }
-    __device__ bool phase_ok() const {
-        return ph == 0 ? chunk_of(s) < nchunks : (s >= 1 && chunk_of(s - 1) < nchunks);
+    __device__ bool b_ok(int ss) const { return p->np == 2 && ss >= p->depth && chunk_of(ss - p->depth) < p->nchunks; }
+    __device__ bool phase_ok() const { return ph == 0 ? chunk_of(s) < p->nchunks : b_ok(s); }
+    __device__ void enter() {   // first pair of the member in the current phase
+        u = m;
+        if (BASE) dW = pdep_pos(2 * m, p->ps[ph].wpos, p->ps[ph].nw);
     }
-    // phases in order (s, 0), (s, 1), (s + 1, 0), ...; (s, 1) exists only for np == 2.  After the
-    // last chunk of this group both phases of a step are empty, and so are all later ones.
     __device__ void normalize() {
         while (live) {
-            if (phase_ok() && u < npairs) return;
-            if (np == 2 && ph == 0) {
+            if (u < p->npairs && phase_ok()) return;
+            if (p->np == 2 && ph == 0) {
                 ph = 1;
             } else {
                 s++;
                 ph = 0;
+                if (BASE) {
+                    dHa = dep_add(dHa, p->hstep, p->hmask);
+                    if (s == p->depth) dHb = dH0;
+                    else if (s > p->depth) dHb = dep_add(dHb, p->hstep, p->hmask);
+                }
             }
-            u = m;
-            if (ph == 0 && chunk_of(s) >= nchunks && (np == 1 || s < 1 || chunk_of(s - 1) >= nchunks)) live = false;
+            enter();
+            if (ph == 0 && chunk_of(s) >= p->nchunks && !b_ok(s) && !b_ok(s + 1)) live = false;
         }
     }
-    __device__ void begin() { s = 0; ph = 0; h = 0; u = m; live = true; normalize(); }
+    __device__ void begin(const TcMulti* pp, uint64_t gg, uint64_t mm, uint64_t ng) {
+        p = pp;
+        g = gg;
+        m = mm;
+        ngroups = ng;
+        s = 0;
+        ph = 0;
+        h = 0;
+        live = true;
+        if (BASE) {
+            dHa = dH0 = pdep_pos(g, p->hpos, p->nh);
+            dHb = p->depth == 0 ? dH0 : 0;
+        }
+        enter();
+        normalize();
+    }
     __device__ void advance() {
         h ^= 1;
         if (h) return;
-        u += gsz;
+        u += (uint64_t)p->gs;
+        if (BASE) dW = dep_add(dW, p->ps[ph].wstep, p->ps[ph].wmask);
         normalize();
     }
-    __device__ uint64_t chunk() const { return ph == 0 ? chunk_of(s) : chunk_of(s - 1); }
+    __device__ uint64_t chunk() const { return ph == 0 ? chunk_of(s) : chunk_of(s - p->depth); }
+    __device__ uint64_t base() const {
+        return dW | (h ? (1ull << p->ps[ph].r) : 0ull) | (ph == 0 ? dHa : dHb);
+    }
+    // the member's last tile of this pass-A phase (its A(chunk) is then complete)
+    __device__ bool last_of_phase() const { return h == 1 && u + (uint64_t)p->gs >= p->npairs; }
 };
 
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_constant__ TcMulti p) {
@@ -685,43 +728,32 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
 
-    TcSched sc0;
-    {
-        const uint64_t gs = (uint64_t)p.gs;
-        sc0.ngroups = (gridDim.x + gs - 1) / gs;
-        sc0.g = blockIdx.x / gs;
-        sc0.m = blockIdx.x % gs;
-        const uint64_t g0 = sc0.g * gs;
-        sc0.gsz = (uint64_t)gridDim.x - g0 < gs ? (uint64_t)gridDim.x - g0 : gs;
-        sc0.nchunks = p.nchunks;
-        sc0.npairs = p.npairs;
-        sc0.np = p.np;
-        sc0.begin();
-    }
-    auto tile_base = [&](const TcSched& sc) {
-        const TcPass& q = p.ps[sc.ph];
-        return pdep_pos(2 * sc.u + (uint64_t)sc.h, q.wpos, q.nw) | pdep_pos(sc.chunk(), p.hpos, p.nh);
-    };
+    const uint64_t ngroups = gridDim.x / (unsigned)p.gs;   // equal groups (host sizes the grid)
+    const uint64_t grp = blockIdx.x / (unsigned)p.gs, mem = blockIdx.x % (unsigned)p.gs;
 
     if (warp == kProdWarp) {
         // ---------------- TMA producer: both tiles of a pair
-        TcSched sc = sc0;
+        uint64_t pol_first;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+        TcSched<true> sc;
+        sc.begin(&p, grp, mem, ngroups);
         uint64_t it = 0;
         int wait_s = -1;
         for (; sc.live; sc.advance(), it++) {
             if (sc.h) continue;   // odd half: copied with its pair
-            const TcPass& q = p.ps[sc.ph];
-            if (sc.ph == 1 && sc.s != wait_s) {
+            const int P = sc.ph;
+            if (P == 1 && sc.s != wait_s) {
                 // pass B reads pass A's output of this chunk: every member of the group must be done
                 wait_s = sc.s;
                 if (lane == 0) {
                     const unsigned* cnt = p.done + sc.chunk();
                     unsigned v;
                     while (true) {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-                        if (v >= (unsigned)sc.gsz) break;
-                        __nanosleep(256);
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+                        if (v >= (unsigned)p.gs) break;
+                        __nanosleep(128);
                     }
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 __syncwarp();
@@ -734,15 +766,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
                              "r"(kRawBytes * 2)
                              : "memory");
             __syncwarp();
-            const int nruns = 1 << (12 - q.r);
-            const uint32_t copy_bytes = (8u << q.r) * 2u;
-            const float2* src = p.amps + tile_base(sc);
+            const int r = p.ps[P].r;
+            const int nruns = 1 << (12 - r);
+            const uint32_t copy_bytes = (8u << r) * 2u;
+            const float2* src = p.amps + sc.base();
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
-            for (int u = lane; u < nruns; u += 32)
+            for (int u = lane; u < nruns; u += 32)   // inputs are read once: L2 evict-first
                 asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        dst + u * copy_bytes),
-                    "l"(src + offr[64 * sc.ph + u]), "r"(copy_bytes), "r"(su32(&rfull[slot]))
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+                    "[%3], %4;" ::"r"(dst + u * copy_bytes),
+                    "l"(src + offr[64 * P + u]), "r"(copy_bytes), "r"(su32(&rfull[slot])), "l"(pol_first)
                     : "memory");
         }
     } else if (warp < kLoadWarps) {
@@ -750,26 +783,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
         const int lt = threadIdx.x;
         const int j = lt & 63;
         const int to = lt >> 6;
-        TcSched sc = sc0;
+        int boff[2][16];   // raw-slot element offsets per pass (tile-invariant)
+        for (int P = 0; P < 2; P++) {
+            const int PP = P < p.np ? P : 0;
+            const int rho = p.ps[PP].rot ? (lane & 7) : 0;
+            const int sj = sofj[64 * PP + j];
+#pragma unroll
+            for (int i = 0; i < 16; i++) boff[P][i] = soft[64 * PP + 8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj;
+        }
+        TcSched<false> sc;
+        sc.begin(&p, grp, mem, ngroups);
         uint64_t it = 0;
         for (; sc.live; sc.advance(), it++) {
             const int P = sc.ph;
-            const TcPass& q = p.ps[P];
-            const int rho = q.rot ? (lane & 7) : 0;
-            const int sj = sofj[64 * P + j];
             const int slot = (it >> 1) & 1;
             const uint64_t use = it >> 2;
             mbar_wait(&rfull[slot], use & 1);
-            const float2* rb = raw + (size_t)slot * 8192 + (sc.h ? (1 << q.r) : 0);
+            const float2* rb = raw + (size_t)slot * 8192 + (sc.h ? (1 << p.ps[P].r) : 0);
             float2 b[16];
+            if (P == 0) {
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-                b[i] = f2mul(rb[soft[64 * P + 8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj], 32768.f);
+                for (int i = 0; i < 16; i++) b[i] = f2mul(rb[boff[0][i]], 32768.f);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; i++) b[i] = f2mul(rb[boff[1][i]], 32768.f);
+            }
             mbar_arrive(&rempty[slot]);
             const int s = it % kStages;
             mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
             uint8_t* bhi = stages + s * kStageBytes;
             uint8_t* blo = bhi + kBBytes;
+            const bool rot = p.ps[P].rot != 0;
+            const int rho = lane & 7;
 #pragma unroll
             for (int g = 0; g < 2; g++) {
                 uint32_t rh[4], rl[4], ih[4], il[4];
@@ -779,7 +824,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
                     split_h2(v0.x, v1.x, rh[e2], rl[e2]);
                     split_h2(v0.y, v1.y, ih[e2], il[e2]);
                 }
-                if (q.rot) {
+                if (rot) {
                     rot_h8(rh, rho);
                     rot_h8(rl, rho);
                     rot_h8(ih, rho);
@@ -798,7 +843,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
     } else if (warp == kMmaWarp) {
         // ---------------- MMA issuer (2 accumulators: cross terms + hh k-steps 0-3, hh k-steps 4-7)
         const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        TcSched sc = sc0;
+        TcSched<false> sc;
+        sc.begin(&p, grp, mem, ngroups);
         uint64_t it = 0;
         for (; sc.live; sc.advance(), it++) {
             const int s = it % kStages, d = it & 1;
@@ -853,9 +899,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
             gb[P] = go;
         }
         float* st = staging + trow * kPitchF + comp;
-        TcSched sc = sc0;
+        uint64_t pol_last;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+        TcSched<true> sc;
+        sc.begin(&p, grp, mem, ngroups);
         uint64_t it = 0;
-        for (; sc.live; it++) {
+        for (; sc.live; sc.advance(), it++) {
             const int d = it & 1;
             const int P = sc.ph;
             mbar_wait(&tfull[d], (it >> 1) & 1);
@@ -886,21 +935,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            const TcPass& q = p.ps[P];
-            float2* dst = p.amps + (tile_base(sc) | gb[P]);
-            const float* sl = sld[P];
-            if (P == 0 && p.np == 2) {   // re-read by pass B from L2: default (allocating) stores
+            const uint64_t tb = sc.base();
+            if (P == 0) {
+                float2* dst = p.amps + (tb | gb[0]);
+                if (p.np == 2) {   // re-read by pass B from L2: keep (evict-last)
 #pragma unroll 8
-                for (int i = 0; i < 32; i++) dst[q.sgo[i]] = *reinterpret_cast<const float2*>(sl + q.sso[i]);
+                    for (int i = 0; i < 32; i++) {
+                        const float2 v = *reinterpret_cast<const float2*>(sld[0] + p.ps[0].sso[i]);
+                        asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dst + p.ps[0].sgo[i]),
+                                     "f"(v.x), "f"(v.y), "l"(pol_last)
+                                     : "memory");
+                    }
+                } else {
+#pragma unroll 8
+                    for (int i = 0; i < 32; i++)
+                        __stcs(dst + p.ps[0].sgo[i], *reinterpret_cast<const float2*>(sld[0] + p.ps[0].sso[i]));
+                }
             } else {
+                float2* dst = p.amps + (tb | gb[1]);
 #pragma unroll 8
-                for (int i = 0; i < 32; i++) __stcs(dst + q.sgo[i], *reinterpret_cast<const float2*>(sl + q.sso[i]));
+                for (int i = 0; i < 32; i++)
+                    __stcs(dst + p.ps[1].sgo[i], *reinterpret_cast<const float2*>(sld[1] + p.ps[1].sso[i]));
             }
-            TcSched nx = sc;
-            nx.advance();
-            if (p.np == 2 && P == 0 && !(nx.live && nx.ph == 0 && nx.s == sc.s)) {
-                // this CTA's last pass-A tile of the chunk: publish after all epilogue stores
-                __threadfence();
+            if (p.np == 2 && P == 0 && sc.last_of_phase()) {
+                // this CTA's last pass-A tile of the chunk: publish after all epilogue stores (the
+                // named barrier orders them before thread 0's gpu-scope release)
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (et == 0) {
                     unsigned* cnt = p.done + sc.chunk();
@@ -908,7 +967,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");   // staging reused by the next tile
-            sc = nx;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1148,17 +1206,37 @@ cudaError_t gate_pass_tc_multi(float2* amps, int nl, int np, const int* const* p
         m.gs = 1;
         if (grid > m.nchunks * m.npairs) grid = m.nchunks * m.npairs;
     } else {
-        // group size: keep ~2 chunks per group in flight within ~64 MB of L2
-        const uint64_t chunk_bytes = 8ull << nc;
-        uint64_t gs = (grid * 2 * chunk_bytes + (64ull << 20) - 1) / (64ull << 20);
-        if (gs < 4) gs = 4;
-        if (gs > m.npairs) gs = m.npairs;
-        if (gs > grid) gs = grid;
+        // depth chunk-steps of slack, each member holding ~kSlackTiles tiles of other work
+        // between a chunk's pass A and pass B; in flight: ngroups x (depth + 1) chunks
+        const int depth_env = getenv("RCS_PAIR_DEPTH") ? atoi(getenv("RCS_PAIR_DEPTH")) : 2;
+        const int slack_env = getenv("RCS_PAIR_SLACK") ? atoi(getenv("RCS_PAIR_SLACK")) : 16;
+        const uint64_t chunk_tiles = 2 * m.npairs;
+        m.depth = depth_env < 1 ? 1 : depth_env;
+        const uint64_t want = (chunk_tiles * (uint64_t)m.depth + slack_env - 1) / (uint64_t)slack_env;
+        uint64_t gs = 1;   // power of two <= npairs: every member gets the same number of pairs
+        while (gs * 2 <= want && gs * 2 <= m.npairs && gs * 2 <= grid) gs *= 2;
         m.gs = (int)gs;
+        grid = grid / gs * gs;   // equal groups (a few SMs idle rather than one slow group)
         if (!done || done_cap < m.nchunks) return cudaErrorInvalidValue;
         m.done = done;
         cudaError_t e = cudaMemsetAsync(done, 0, m.nchunks * sizeof(unsigned), st);
         if (e != cudaSuccess) return e;
+    }
+    // incremental deposits: a member's pair stride 2 gs inside a chunk, a group's chunk stride
+    auto pdep_host = [](uint64_t x, const int* pos, int n) {
+        uint64_t r = 0;
+        for (int i = 0; i < n; i++) r |= ((x >> i) & 1ull) << pos[i];
+        return r;
+    };
+    const uint64_t ngroups = grid / (uint64_t)m.gs;
+    m.hmask = 0;
+    for (int i = 0; i < m.nh; i++) m.hmask |= 1ull << m.hpos[i];
+    m.hstep = pdep_host(ngroups, m.hpos, m.nh);
+    for (int P = 0; P < np; P++) {
+        TcPass& q = m.ps[P];
+        q.wmask = 0;
+        for (int i = 0; i < q.nw; i++) q.wmask |= 1ull << q.wpos[i];
+        q.wstep = pdep_host(2ull * (uint64_t)m.gs, q.wpos, q.nw);
     }
     static bool attr = false;
     if (!attr) {

@@ -92,14 +92,15 @@ def test_virtual_global_bitwise_equals_single(rcs, ctx, g):
     check_amps(psig, ref)
 
 
-@pytest.mark.parametrize("case", ["c2", "grid20", "rand17", "rand19", "c3"])
+@pytest.mark.parametrize("case", ["c2", "grid22", "rand21", "rand23", "c3"])
 def test_paired_passes_bitwise_equal(rcs, ctx, case, monkeypatch):
     """K11 runs two consecutive tensor-core passes per launch (pass B re-reads pass A's output
     from L2 chunk by chunk); its per-tile arithmetic is K9's, so the state must be bit-identical
     to one pass per launch -- on small and full-size (C3, n=32) states."""
-    text = {"c2": config_qasm("c2"), "grid20": emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=8)),
-            "rand17": random_qasm(17, 220, 5), "rand19": random_qasm(19, 260, 6), "c3": config_qasm("c3")}[case]
+    text = {"c2": config_qasm("c2"), "grid22": emit_qasm(generate(2, 11, 16, "ABCD", seed=8)),
+            "rand21": random_qasm(21, 300, 5), "rand23": random_qasm(23, 320, 6), "c3": config_qasm("c3")}[case]
     c = rcs.Circuit.from_qasm(text)
+    monkeypatch.setenv("RCS_TC_PAIR", "1")
     paired = rcs.State.build(ctx, c, fuse_k=6)
     assert paired.report["n_paired"] > 0
     xa = paired.sample(100_000, seed=SHOT_SEED)
