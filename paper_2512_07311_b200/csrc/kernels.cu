@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(kThreads) k_pack(float2* __restrict__ amps, fl
 }
 
 // peer swap (remap over NVLink): each thread moves U 16-B vectors each way, loads first
-constexpr int kSwapU = 4;
+#ifndef RCS_SWAP_U
+#define RCS_SWAP_U 4
+#endif
+constexpr int kSwapU = RCS_SWAP_U;   // 16-B vectors per thread in flight (loads first)
 __global__ void __launch_bounds__(kThreads) k_peer_swap(const __grid_constant__ PeerSwapArgs a) {
     const int pc = blockIdx.y;
     const uint64_t nvec = a.m_count[pc] >> 1;   // 16-B vectors (2 amplitudes)

@@ -3,7 +3,7 @@
 TAG=${1:-all4}; OUT=gpurun_out/$TAG; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 timeout 1800 python -m pytest tests -m gpu -q -x > $OUT/gpu_tests.log 2>&1; echo "rc=$?" >> $OUT/gpu_tests.log
-CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --no-cpu-baseline > $OUT/bench_N1.json 2> $OUT/bench_N1.err
+CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py > $OUT/bench_N1.json 2> $OUT/bench_N1.err
 for M in 2 4; do
   DEV=$(seq -s, 0 $((M-1)))
   CUDA_VISIBLE_DEVICES=$DEV timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $M \
