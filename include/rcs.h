@@ -112,7 +112,7 @@ typedef struct {
     int n_pipelined;         /* remaps run as chunked NVLink swaps overlapped with the adjacent
                                 tensor-core passes; env RCS_OVERLAP=0 disables,
                                 RCS_OVERLAP_CHUNKS = log2 chunks (default 2), RCS_OVERLAP_SMS =
-                                SMs left to the swaps (default 32); RCS_REMAP_PULL=1 (world >= 4):
+                                SMs left to the swaps (default 32 at N=2, 16 at N>=4); RCS_REMAP_PULL=1 (world >= 4):
                                 staged pulls instead of in-place swaps (measured slower at N=4) */
     int n_paired;            /* launches that ran two consecutive tensor-core passes (K11, one HBM
                                 round trip for both; experimental, env RCS_TC_PAIR=1 enables)  */

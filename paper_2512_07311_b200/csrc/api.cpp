@@ -1112,7 +1112,9 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     // pipelined remaps (f1): on unless RCS_OVERLAP=0; 2^cb chunks, `reserve` SMs left to the swaps
     static const int ov_on = getenv("RCS_OVERLAP") ? atoi(getenv("RCS_OVERLAP")) : 1;
     static const int ov_cb = getenv("RCS_OVERLAP_CHUNKS") ? atoi(getenv("RCS_OVERLAP_CHUNKS")) : 2;
-    static const int ov_res = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 32;
+    // SMs left to the swaps: 32 at N=2, 16 at N>=4 (sweeps in profiles/r01_ovl*)
+    static const int ov_res_env = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 0;
+    const int ov_res = ov_res_env > 0 ? ov_res_env : (ctx->world >= 4 ? 16 : 32);
     static const int ov_pull = getenv("RCS_REMAP_PULL") ? atoi(getenv("RCS_REMAP_PULL")) : 0;
     auto is_tc = [&](size_t i) { return i < n_exec && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
     auto tc_ref = [&](size_t i) {
