@@ -167,6 +167,11 @@ rcs_status rcs_plan_create(const rcs_circuit *c, int fuse_k, int n_global, rcs_p
 rcs_status rcs_plan_summary(const rcs_plan *p, int *n_items, int *n_passes, int *n_remaps, int *n_swaps);
 /* matrix_out (may be NULL): 2 * 4^k doubles, row-major interleaved complex, fp64 product. */
 rcs_status rcs_plan_item_get(const rcs_plan *p, int i, rcs_plan_item *out, double *matrix_out);
+/* Layout bookkeeping of the plan (host): items [*restore_begin, n_items) only restore the
+ * canonical layout (skipped by keep_layout); final_pos[q] (n entries, may be NULL) = physical
+ * position of qubit q before them (>= n - n_global: a rank bit); initial_pos likewise at the
+ * start (the global qubits may start permuted: |0...0> is permutation invariant). */
+rcs_status rcs_plan_layout(const rcs_plan *p, int *restore_begin, int *final_pos, int *initial_pos);
 void rcs_plan_free(rcs_plan *p);
 
 /* ---- context ------------------------------------------------------------------------ */

@@ -101,6 +101,15 @@ class Plan:
                 pass
             self._h = None
 
+    def layout(self) -> dict:
+        """restore_begin, final_pos (qubit -> physical position before the restore), initial_pos."""
+        n = self.circuit.n_qubits
+        rb = C.c_int()
+        fp = (C.c_int * n)()
+        ip = (C.c_int * n)()
+        check(lib().rcs_plan_layout(self._h, C.byref(rb), fp, ip), None, "rcs_plan_layout")
+        return {"restore_begin": rb.value, "final_pos": list(fp), "initial_pos": list(ip)}
+
     def items(self) -> list:
         out = []
         it = rcs_plan_item()

@@ -69,6 +69,7 @@ SIGNATURES = {
     "rcs_plan_summary": (C.c_int, [VP, IP, IP, IP, IP]),
     "rcs_plan_item_get": (C.c_int, [VP, C.c_int, C.POINTER(rcs_plan_item), DP]),
     "rcs_plan_free": (None, [VP]),
+    "rcs_plan_layout": (C.c_int, [VP, IP, IP, IP]),
     "rcs_nccl_unique_id_bytes": (C.c_int, []),
     "rcs_nccl_unique_id": (C.c_int, [VP, E]),
     "rcs_context_create": (C.c_int, [C.c_int, C.c_int, C.c_int, VP, VP, PP, E]),

@@ -826,6 +826,17 @@ rcs_status rcs_plan_create(const rcs_circuit* c, int fuse_k, int n_global, rcs_p
     return RCS_OK;
 }
 
+rcs_status rcs_plan_layout(const rcs_plan* p, int* restore_begin, int* final_pos, int* initial_pos) {
+    if (!p) return RCS_ERR_ARG;
+    const Plan& P = p->p;
+    if (restore_begin) *restore_begin = P.restore_begin;
+    for (int q = 0; q < P.n; q++) {
+        if (final_pos) final_pos[q] = q < (int)P.final_pos.size() ? P.final_pos[q] : q;
+        if (initial_pos) initial_pos[q] = q < (int)P.initial_pos.size() ? P.initial_pos[q] : q;
+    }
+    return RCS_OK;
+}
+
 rcs_status rcs_plan_summary(const rcs_plan* p, int* n_items, int* n_passes, int* n_remaps, int* n_swaps) {
     if (!p) return RCS_ERR_ARG;
     if (n_items) *n_items = (int)p->p.items.size();

@@ -135,6 +135,35 @@ def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
     assert np.abs(psi - ref).max() < 1e-12
 
 
+@pytest.mark.parametrize("g", [1, 2, 3])
+@pytest.mark.parametrize("grid", [(3, 5, 14, "EFGH"), (2, 8, 20, "ABCDCDAB"), (4, 4, 12, "ABCD")])
+def test_kept_layout_plan(rcs, g, grid):
+    """keep_layout executes items [0, restore_begin): the physical state then equals the oracle
+    state with qubit q moved to final_pos[q] (pins the layout the logical CDF relies on)."""
+    rows, cols, cyc, pat = grid
+    n = rows * cols
+    if n - g - 6 < 6:
+        pytest.skip("too few movable local qubits")
+    text = emit_qasm(generate(rows, cols, cyc, pat, seed=20 + g))
+    ref = oracle.build_state(text)
+    c = rcs.Circuit.from_qasm(text)
+    p = rcs.Plan(c, 6 if n - g >= 12 else 4, g)
+    lay = p.layout()
+    items = p.items()
+    assert all(it["type"] == "pass" for it in items[:lay["restore_begin"]][-1:])
+    assert all(it["type"] != "pass" for it in items[lay["restore_begin"]:])
+    assert sorted(lay["final_pos"]) == list(range(n)) and sorted(lay["initial_pos"]) == list(range(n))
+    assert all(lay["final_pos"][q] == q for q in range(6))           # positions 0..5 pinned
+    psi = run_plan(items[:lay["restore_begin"]], n)
+    # physical index of logical x: bit q of x goes to position final_pos[q]
+    x = np.arange(1 << n, dtype=np.int64)
+    phys = np.zeros_like(x)
+    for q in range(n):
+        phys |= ((x >> q) & 1) << lay["final_pos"][q]
+    assert np.abs(psi[phys] - ref).max() < 1e-12
+    assert np.abs(run_plan(items, n) - ref).max() < 1e-12             # with the restore: canonical
+
+
 def test_plan_rejects_bad_arguments(rcs):
     c = rcs.Circuit.from_qasm(config_qasm("c1"))
     with pytest.raises(rcs.RcsError):
