@@ -92,70 +92,102 @@ struct Fuser {
         return r;
     }
 
-    // greedy growth of a block seeded by ready gate g0 (qubit set S, absorbed gates cur)
-    void grow(int g0, std::vector<int>& S, std::vector<int>& cur) const {
-        S.clear();
-        for (int j = 0; j < nq(g0); j++) S.push_back(qb(g0, j));
-        std::sort(S.begin(), S.end());
-        cur = closure(S);
+    // candidate extensions of qubit set S (closure cur): the qubits of the next gate on a qubit
+    // of S, or of a gate that is ready elsewhere (disjoint from S), within k qubits
+    std::set<std::vector<int>> extensions(const std::vector<int>& S, const std::vector<int>& cur) const {
+        std::map<int, int> h;
+        for (int q : S) h[q] = head[q];
+        for (int g : cur)
+            for (int j = 0; j < nq(g); j++) h[qb(g, j)]++;
+        std::set<std::vector<int>> cands;
+        for (int q : S) {
+            if (h[q] >= (int)per_q[q].size()) continue;
+            int g = per_q[q][h[q]];
+            std::vector<int> ext;
+            for (int j = 0; j < nq(g); j++)
+                if (!std::count(S.begin(), S.end(), qb(g, j))) ext.push_back(qb(g, j));
+            if (!ext.empty() && (int)(S.size() + ext.size()) <= k) cands.insert(ext);
+        }
+        for (int q = 0; q < C.n; q++) {
+            if (std::count(S.begin(), S.end(), q) || head[q] >= (int)per_q[q].size()) continue;
+            int g = per_q[q][head[q]];
+            bool ready = true;
+            std::vector<int> ext;
+            for (int j = 0; j < nq(g); j++) {
+                int qq = qb(g, j);
+                if (per_q[qq][head[qq]] != g) ready = false;
+                if (!std::count(S.begin(), S.end(), qq)) ext.push_back(qq);
+            }
+            if (ready && (int)(S.size() + ext.size()) <= k) {
+                std::sort(ext.begin(), ext.end());
+                cands.insert(ext);
+            }
+        }
+        return cands;
+    }
+
+    int weight(const std::vector<int>& gates) const {   // 2q gates count double
+        int w = 0;
+        for (int g : gates) w += nq(g);
+        return w;
+    }
+
+    // greedy continuation: add the extension with the largest gain per added qubit until k
+    void grow_from(std::vector<int>& S, std::vector<int>& cur) const {
         while ((int)S.size() < k) {
-            // candidate extensions: qubits of gates at the heads reachable after the closure
-            std::map<int, int> h;
-            for (int q : S) h[q] = head[q];
-            for (int g : cur)
-                for (int j = 0; j < nq(g); j++) h[qb(g, j)]++;
-            std::set<std::vector<int>> cands;
-            for (int q : S) {
-                if (h[q] >= (int)per_q[q].size()) continue;
-                int g = per_q[q][h[q]];
-                std::vector<int> ext;
-                for (int j = 0; j < nq(g); j++)
-                    if (!std::count(S.begin(), S.end(), qb(g, j))) ext.push_back(qb(g, j));
-                if (!ext.empty() && (int)(S.size() + ext.size()) <= k) cands.insert(ext);
-            }
-            // gates that are ready elsewhere (disjoint from S)
-            for (int q = 0; q < C.n; q++) {
-                if (std::count(S.begin(), S.end(), q) || head[q] >= (int)per_q[q].size()) continue;
-                int g = per_q[q][head[q]];
-                bool ready = true;
-                std::vector<int> ext;
-                for (int j = 0; j < nq(g); j++) {
-                    int qq = qb(g, j);
-                    if (per_q[qq][head[qq]] != g) ready = false;
-                    if (!std::count(S.begin(), S.end(), qq)) ext.push_back(qq);
-                }
-                if (ready && (int)(S.size() + ext.size()) <= k) {
-                    std::sort(ext.begin(), ext.end());
-                    cands.insert(ext);
-                }
-            }
-            int best_score = (int)cur.size();
+            const int base = weight(cur);
+            int bgain = 0;
             std::vector<int> best_ext, best_cl;
-            for (const auto& ext : cands) {
+            for (const auto& ext : extensions(S, cur)) {
                 std::vector<int> cl = closure(merged(S, ext));
-                // weight 2q gates double: they are what forces extra passes
-                int score = 0;
-                for (int g : cl) score += nq(g);
-                int base = 0;
-                for (int g : cur) base += nq(g);
-                int gain = score - base;
-                int bgain = 0;
-                if (!best_cl.empty()) {
-                    for (int g : best_cl) bgain += nq(g);
-                    bgain -= base;
-                }
+                const int gain = weight(cl) - base;
                 if (gain <= 0) continue;
                 // prefer larger gain per added qubit, then fewer qubits
                 if (best_cl.empty() || gain * (int)best_ext.size() > bgain * (int)ext.size() ||
                     (gain * (int)best_ext.size() == bgain * (int)ext.size() && ext.size() < best_ext.size())) {
                     best_ext = ext;
                     best_cl = cl;
+                    bgain = gain;
                 }
             }
-            (void)best_score;
             if (best_cl.empty()) break;
             S = merged(S, best_ext);
             cur = best_cl;
+        }
+    }
+
+    // growth of a block seeded by ready gate g0 (qubit set S, absorbed gates cur); with
+    // `grow_lookahead`, every step tries each extension followed by the greedy continuation and
+    // keeps the one whose finished block absorbs the most
+    bool grow_lookahead = false;
+    void grow(int g0, std::vector<int>& S, std::vector<int>& cur) const {
+        S.clear();
+        for (int j = 0; j < nq(g0); j++) S.push_back(qb(g0, j));
+        std::sort(S.begin(), S.end());
+        cur = closure(S);
+        if (!grow_lookahead) {
+            grow_from(S, cur);
+            return;
+        }
+        while ((int)S.size() < k) {
+            const int base = weight(cur);
+            int best = -1;
+            std::vector<int> bS, bcur;
+            for (const auto& ext : extensions(S, cur)) {
+                std::vector<int> S1 = merged(S, ext), c1 = closure(S1);
+                if (weight(c1) <= base) continue;
+                grow_from(S1, c1);
+                const int w = weight(c1);
+                if (w > best) {
+                    best = w;
+                    bS = S1;
+                    bcur = c1;
+                }
+            }
+            if (best < 0) break;
+            S = bS;   // the finished block of the best first step
+            cur = bcur;
+            break;
         }
     }
 
@@ -179,6 +211,7 @@ struct Fuser {
         Fuser f = *this;
         f.seeds = 0;
         f.lookahead = false;
+        f.grow_lookahead = false;
         int n = 0;
         Block b;
         while (f.next_block(b)) n++;
@@ -313,12 +346,33 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
     P.n_global = n_global;
     P.fuse_k = k;
 
-    // ---- 1. fusion
-    Fuser F(c, k);
-    F.seeds = getenv("RCS_FUSE_SEEDS") ? atoi(getenv("RCS_FUSE_SEEDS")) : kFuseSeeds;
-    F.lookahead = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
-    Block B;
-    while (F.next_block(B)) {
+    // ---- 1. fusion: two growth strategies (plain greedy, greedy with one-step lookahead) run in
+    // parallel; the one needing fewer blocks wins (ties: plain).  Both are deterministic and
+    // independent of the sharding, so the plan stays P-invariant.
+    const int seeds = getenv("RCS_FUSE_SEEDS") ? atoi(getenv("RCS_FUSE_SEEDS")) : kFuseSeeds;
+    const bool la = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
+    const int strat = getenv("RCS_FUSE_GROWLA") ? atoi(getenv("RCS_FUSE_GROWLA")) : -1;   // -1: both
+    std::vector<Block> cand[2];
+    auto fuse = [&](int which) {
+        Fuser F(c, k);
+        F.seeds = seeds;
+        F.lookahead = la;
+        F.grow_lookahead = which == 1;
+        Block B;
+        while (F.next_block(B)) {
+            cand[which].push_back(B);
+            B = Block();
+        }
+    };
+    if (strat < 0) {
+        std::thread t1(fuse, 1);
+        fuse(0);
+        t1.join();
+    } else {
+        fuse(strat ? 1 : 0);
+    }
+    const int win = strat >= 0 ? (strat ? 1 : 0) : (cand[1].size() < cand[0].size() ? 1 : 0);
+    for (Block& B : cand[win]) {
         const int kb = (int)B.qubits.size();
         const int D = 1 << kb;
         B.matrix.assign((size_t)D * D, {0.0, 0.0});
@@ -329,8 +383,7 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
             int lb1 = g.q1 >= 0 ? (int)(std::find(B.qubits.begin(), B.qubits.end(), g.q1) - B.qubits.begin()) : -1;
             apply_to_block(B.matrix, kb, g, lb0, lb1);
         }
-        P.blocks.push_back(B);
-        B = Block();
+        P.blocks.push_back(std::move(B));
     }
 
     // ---- 2. layout + remaps
