@@ -391,8 +391,10 @@ void make_swap_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint
     for (int i = 0; i < j; i++)
         if ((my_code >> i) & 1) A.my_mask |= 1ull << it.b[i];
     const uint64_t count = 1ull << (nl - j - nfix);
-    for (int code = 0; code < (1 << j); code++) {
-        if (code == my_code) continue;
+    static const int rounds = getenv("RCS_SWAP_ROUNDS") ? atoi(getenv("RCS_SWAP_ROUNDS")) : 0;   // measured: no gain
+    A.rounds = rounds;
+    for (int x = 1; x < (1 << j); x++) {   // peers in XOR-pattern order: round x pairs code with code^x
+        const int code = my_code ^ x;
         int peer = c->rank;
         uint64_t mask = 0;
         for (int i = 0; i < j; i++) {

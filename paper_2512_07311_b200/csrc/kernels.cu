@@ -674,6 +674,22 @@ cudaError_t unpack(float2* amps, const float2* buf, int j, const int* lpos, uint
 }
 
 cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st) {
+    if (a.rounds && a.npeers > 1) {
+        // one peer at a time (the caller orders peers by code XOR, so every rank pairs with the
+        // same partner in the same round): disjoint pairwise exchanges instead of an all-to-all
+        for (int i = 0; i < a.npeers; i++) {
+            PeerSwapArgs b = a;
+            b.rounds = 0;
+            b.npeers = 1;
+            b.peer[0] = a.peer[i];
+            b.mask[0] = a.mask[i];
+            b.m_begin[0] = a.m_begin[i];
+            b.m_count[0] = a.m_count[i];
+            cudaError_t e = peer_swap(b, st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     uint64_t maxv = 0;
     for (int i = 0; i < a.npeers; i++) maxv = a.m_count[i] / 2 > maxv ? a.m_count[i] / 2 : maxv;
     if (maxv == 0) return cudaSuccess;

@@ -65,6 +65,7 @@ struct PeerSwapArgs {
     int fix[4];
     uint64_t fixval;                   // ... and their bits
     int max_grid;                      // 0: default
+    int rounds;                        // 1: exchange with one peer at a time (pairwise rounds)
 };
 cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st);
 
