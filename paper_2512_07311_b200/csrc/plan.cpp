@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <set>
 #include <thread>
 
@@ -32,178 +33,200 @@ namespace rcs {
 
 namespace {
 
+// Qubit sets are 64-bit masks (n <= 63); per-qubit gate lists are shared read-only between the
+// fuser and its rollout copies.
+struct FuseTables {
+    std::vector<std::vector<int>> per_q;   // gate ids per qubit, source order
+    std::vector<uint64_t> gmask;           // qubits of gate g
+    std::vector<int> gw;                   // 1 or 2: 2q gates count double
+};
+
 struct Fuser {
     const Circuit& C;
-    int k;
-    std::vector<std::vector<int>> per_q;   // gate ids per qubit, source order
+    int k, n;
+    std::shared_ptr<const FuseTables> T;
     std::vector<int> head;                 // first unassigned position in per_q[q]
     std::vector<char> assigned;
+    size_t first_unassigned = 0;
 
     int seeds = 0;
+    bool lookahead = false;
+    bool grow_lookahead = false;
+    int grow_depth = 1;
+    int grow_beam = 0;   // 0: every extension
 
-    Fuser(const Circuit& c, int k_) : C(c), k(k_) {
-        per_q.assign(c.n, {});
+    Fuser(const Circuit& c, int k_) : C(c), k(k_), n(c.n) {
+        auto t = std::make_shared<FuseTables>();
+        t->per_q.assign(c.n, {});
         for (int i = 0; i < (int)c.gates.size(); i++) {
-            per_q[c.gates[i].q0].push_back(i);
-            if (c.gates[i].q1 >= 0) per_q[c.gates[i].q1].push_back(i);
+            const Gate& g = c.gates[i];
+            t->per_q[g.q0].push_back(i);
+            uint64_t m = 1ull << g.q0;
+            if (g.q1 >= 0) {
+                t->per_q[g.q1].push_back(i);
+                m |= 1ull << g.q1;
+            }
+            t->gmask.push_back(m);
+            t->gw.push_back(g.q1 >= 0 ? 2 : 1);
         }
+        T = t;
         head.assign(c.n, 0);
         assigned.assign(c.gates.size(), 0);
     }
 
-    int nq(int g) const { return C.gates[g].q1 >= 0 ? 2 : 1; }
-    int qb(int g, int j) const { return j == 0 ? C.gates[g].q0 : C.gates[g].q1; }
+    int next_gate(int q, int pos) const {
+        const auto& v = T->per_q[q];
+        return pos < (int)v.size() ? v[pos] : -1;
+    }
 
-    // gates absorbed by qubit set S (sorted) starting from the current heads
-    std::vector<int> closure(const std::vector<int>& S) const {
-        std::map<int, int> h;
-        for (int q : S) h[q] = head[q];
-        std::vector<int> got;
+    // gates absorbed by qubit set S from the current heads (repeatedly: a gate whose qubits are
+    // all in S and at their heads); returns their total weight, optionally the gates in order
+    // and the resulting per-qubit heads
+    int closure(uint64_t S, std::vector<int>* got = nullptr, int* hout = nullptr) const {
+        int h[64];
+        for (uint64_t m = S; m; m &= m - 1) h[__builtin_ctzll(m)] = head[__builtin_ctzll(m)];
+        int w = 0;
         bool progress = true;
         while (progress) {
             progress = false;
-            for (int q : S) {
-                int pos = h[q];
-                if (pos >= (int)per_q[q].size()) continue;
-                int g = per_q[q][pos];
+            for (uint64_t m = S; m; m &= m - 1) {
+                const int q = __builtin_ctzll(m);
+                const int g = next_gate(q, h[q]);
+                if (g < 0 || (T->gmask[g] & ~S)) continue;
                 bool ok = true;
-                for (int j = 0; j < nq(g); j++) {
-                    auto it = h.find(qb(g, j));
-                    if (it == h.end() || it->second >= (int)per_q[qb(g, j)].size() ||
-                        per_q[qb(g, j)][it->second] != g) {
-                        ok = false;
-                        break;
-                    }
+                for (uint64_t mm = T->gmask[g]; mm && ok; mm &= mm - 1) {
+                    const int qq = __builtin_ctzll(mm);
+                    ok = next_gate(qq, h[qq]) == g;
                 }
                 if (!ok) continue;
-                for (int j = 0; j < nq(g); j++) h[qb(g, j)]++;
-                got.push_back(g);
+                for (uint64_t mm = T->gmask[g]; mm; mm &= mm - 1) h[__builtin_ctzll(mm)]++;
+                w += T->gw[g];
+                if (got) got->push_back(g);
                 progress = true;
             }
         }
-        return got;
-    }
-
-    static std::vector<int> merged(const std::vector<int>& S, const std::vector<int>& ext) {
-        std::vector<int> r = S;
-        for (int q : ext)
-            if (!std::count(r.begin(), r.end(), q)) r.push_back(q);
-        std::sort(r.begin(), r.end());
-        return r;
-    }
-
-    // candidate extensions of qubit set S (closure cur): the qubits of the next gate on a qubit
-    // of S, or of a gate that is ready elsewhere (disjoint from S), within k qubits
-    std::set<std::vector<int>> extensions(const std::vector<int>& S, const std::vector<int>& cur) const {
-        std::map<int, int> h;
-        for (int q : S) h[q] = head[q];
-        for (int g : cur)
-            for (int j = 0; j < nq(g); j++) h[qb(g, j)]++;
-        std::set<std::vector<int>> cands;
-        for (int q : S) {
-            if (h[q] >= (int)per_q[q].size()) continue;
-            int g = per_q[q][h[q]];
-            std::vector<int> ext;
-            for (int j = 0; j < nq(g); j++)
-                if (!std::count(S.begin(), S.end(), qb(g, j))) ext.push_back(qb(g, j));
-            if (!ext.empty() && (int)(S.size() + ext.size()) <= k) cands.insert(ext);
-        }
-        for (int q = 0; q < C.n; q++) {
-            if (std::count(S.begin(), S.end(), q) || head[q] >= (int)per_q[q].size()) continue;
-            int g = per_q[q][head[q]];
-            bool ready = true;
-            std::vector<int> ext;
-            for (int j = 0; j < nq(g); j++) {
-                int qq = qb(g, j);
-                if (per_q[qq][head[qq]] != g) ready = false;
-                if (!std::count(S.begin(), S.end(), qq)) ext.push_back(qq);
-            }
-            if (ready && (int)(S.size() + ext.size()) <= k) {
-                std::sort(ext.begin(), ext.end());
-                cands.insert(ext);
-            }
-        }
-        return cands;
-    }
-
-    int weight(const std::vector<int>& gates) const {   // 2q gates count double
-        int w = 0;
-        for (int g : gates) w += nq(g);
+        if (hout)
+            for (uint64_t m = S; m; m &= m - 1) hout[__builtin_ctzll(m)] = h[__builtin_ctzll(m)];
         return w;
     }
 
-    // greedy continuation: add the extension with the largest gain per added qubit until k
-    void grow_from(std::vector<int>& S, std::vector<int>& cur) const {
-        while ((int)S.size() < k) {
-            const int base = weight(cur);
-            int bgain = 0;
-            std::vector<int> best_ext, best_cl;
-            for (const auto& ext : extensions(S, cur)) {
-                std::vector<int> cl = closure(merged(S, ext));
-                const int gain = weight(cl) - base;
+    // candidate extensions of S: the other qubits of the next gate on a qubit of S (after the
+    // closure), or the qubits of a gate that is ready elsewhere, within k qubits
+    void extensions(uint64_t S, std::vector<uint64_t>& out) const {
+        out.clear();
+        int h[64];
+        closure(S, nullptr, h);
+        const int size = __builtin_popcountll(S);
+        auto add = [&](uint64_t ext) {
+            if (!ext || size + __builtin_popcountll(ext) > k) return;
+            for (uint64_t e : out)
+                if (e == ext) return;
+            out.push_back(ext);
+        };
+        for (uint64_t m = S; m; m &= m - 1) {
+            const int q = __builtin_ctzll(m);
+            const int g = next_gate(q, h[q]);
+            if (g >= 0) add(T->gmask[g] & ~S);
+        }
+        for (int q = 0; q < n; q++) {
+            if ((S >> q) & 1) continue;
+            const int g = next_gate(q, head[q]);
+            if (g < 0 || !ready(g)) continue;
+            add(T->gmask[g] & ~S);
+        }
+        // deterministic order: ascending by (size, mask)
+        std::sort(out.begin(), out.end(), [](uint64_t x, uint64_t y) {
+            const int a = __builtin_popcountll(x), b = __builtin_popcountll(y);
+            return a != b ? a < b : x < y;
+        });
+    }
+
+    // greedy continuation: the extension with the largest gain per added qubit, until k
+    void grow_from(uint64_t& S, int& w) const {
+        std::vector<uint64_t> ex;
+        while (__builtin_popcountll(S) < k) {
+            extensions(S, ex);
+            int bgain = 0, bsize = 0;
+            uint64_t best = 0;
+            int bw = w;
+            for (uint64_t e : ex) {
+                const int w1 = closure(S | e);
+                const int gain = w1 - w, sz = __builtin_popcountll(e);
                 if (gain <= 0) continue;
-                // prefer larger gain per added qubit, then fewer qubits
-                if (best_cl.empty() || gain * (int)best_ext.size() > bgain * (int)ext.size() ||
-                    (gain * (int)best_ext.size() == bgain * (int)ext.size() && ext.size() < best_ext.size())) {
-                    best_ext = ext;
-                    best_cl = cl;
+                if (!best || gain * bsize > bgain * sz) {
+                    best = e;
                     bgain = gain;
+                    bsize = sz;
+                    bw = w1;
                 }
             }
-            if (best_cl.empty()) break;
-            S = merged(S, best_ext);
-            cur = best_cl;
+            if (!best) break;
+            S |= best;
+            w = bw;
         }
     }
 
-    // growth of a block seeded by ready gate g0 (qubit set S, absorbed gates cur); with
-    // `grow_lookahead`, every step tries each extension followed by the greedy continuation and
-    // keeps the one whose finished block absorbs the most
-    bool grow_lookahead = false;
-    void grow(int g0, std::vector<int>& S, std::vector<int>& cur) const {
-        S.clear();
-        for (int j = 0; j < nq(g0); j++) S.push_back(qb(g0, j));
-        std::sort(S.begin(), S.end());
-        cur = closure(S);
-        if (!grow_lookahead) {
-            grow_from(S, cur);
+    // `depth` levels of exhaustive extension choice, then greedy; keeps the heaviest block
+    void grow_deep(uint64_t& S, int& w, int depth) const {
+        if (depth == 0 || __builtin_popcountll(S) >= k) {
+            grow_from(S, w);
             return;
         }
-        while ((int)S.size() < k) {
-            const int base = weight(cur);
-            int best = -1;
-            std::vector<int> bS, bcur;
-            for (const auto& ext : extensions(S, cur)) {
-                std::vector<int> S1 = merged(S, ext), c1 = closure(S1);
-                if (weight(c1) <= base) continue;
-                grow_from(S1, c1);
-                const int w = weight(c1);
-                if (w > best) {
-                    best = w;
-                    bS = S1;
-                    bcur = c1;
-                }
-            }
-            if (best < 0) break;
-            S = bS;   // the finished block of the best first step
-            cur = bcur;
-            break;
+        std::vector<uint64_t> ex;
+        extensions(S, ex);
+        // keep the `grow_beam` extensions with the best gain per added qubit
+        std::vector<std::pair<double, uint64_t>> ranked;
+        for (uint64_t e : ex) {
+            const int w1 = closure(S | e);
+            if (w1 > w) ranked.push_back({-(double)(w1 - w) / __builtin_popcountll(e), e});
         }
+        std::stable_sort(ranked.begin(), ranked.end(),
+                         [](const std::pair<double, uint64_t>& x, const std::pair<double, uint64_t>& y) {
+                             return x.first < y.first;
+                         });
+        if (grow_beam > 0 && (int)ranked.size() > grow_beam) ranked.resize(grow_beam);
+        int best = -1;
+        uint64_t bS = S;
+        for (const auto& re : ranked) {
+            uint64_t S1 = S | re.second;
+            int w1 = closure(S1);
+            grow_deep(S1, w1, depth - 1);
+            if (w1 > best) {
+                best = w1;
+                bS = S1;
+            }
+        }
+        if (best < 0) {
+            grow_from(S, w);
+            return;
+        }
+        S = bS;
+        w = best;
+    }
+
+    void grow(int g0, uint64_t& S, int& w) const {
+        S = T->gmask[g0];
+        w = closure(S);
+        if (grow_lookahead) grow_deep(S, w, grow_depth);
+        else grow_from(S, w);
     }
 
     bool ready(int g) const {
-        for (int j = 0; j < nq(g); j++) {
-            const int q = qb(g, j);
-            if (head[q] >= (int)per_q[q].size() || per_q[q][head[q]] != g) return false;
+        for (uint64_t m = T->gmask[g]; m; m &= m - 1) {
+            const int q = __builtin_ctzll(m);
+            if (next_gate(q, head[q]) != g) return false;
         }
         return true;
     }
 
-    void commit(const std::vector<int>& cur) {
-        for (int g : cur) {
+    void commit(uint64_t S) {
+        std::vector<int> got;
+        closure(S, &got);
+        for (int g : got) {
             assigned[g] = 1;
-            for (int j = 0; j < nq(g); j++) head[qb(g, j)]++;
+            for (uint64_t m = T->gmask[g]; m; m &= m - 1) head[__builtin_ctzll(m)]++;
         }
+        while (first_unassigned < assigned.size() && assigned[first_unassigned]) first_unassigned++;
     }
 
     // number of blocks the plain greedy (earliest-gate seed) needs from the current state
@@ -212,72 +235,65 @@ struct Fuser {
         f.seeds = 0;
         f.lookahead = false;
         f.grow_lookahead = false;
-        int n = 0;
-        Block b;
-        while (f.next_block(b)) n++;
-        return n;
+        int cnt = 0;
+        uint64_t S;
+        while (f.next_set(S)) cnt++;
+        return cnt;
     }
 
-    bool lookahead = false;
-
-    // next block: grow from the earliest unassigned gate and from up to `seeds` other ready
-    // gates; keep the block absorbing the most gate-qubits (2q gates count double), or with
-    // `lookahead`, the one whose greedy completion needs the fewest blocks
-    bool next_block(Block& B) {
-        int g0 = -1;
-        for (int i = 0; i < (int)assigned.size(); i++)
-            if (!assigned[i]) { g0 = i; break; }
-        if (g0 < 0) return false;
+    // next block's qubit set (committed): grow from the earliest unassigned gate and from up to
+    // `seeds` other ready gates; keep the heaviest block, or with `lookahead` the one whose
+    // greedy completion needs the fewest blocks (candidates evaluated in parallel threads)
+    bool next_set(uint64_t& out) {
+        if (first_unassigned >= assigned.size()) return false;
+        const int g0 = (int)first_unassigned;
         std::vector<int> cand{g0};
         for (int i = g0 + 1; i < (int)assigned.size() && (int)cand.size() < 1 + seeds; i++)
             if (!assigned[i] && ready(i)) cand.push_back(i);
-        std::vector<int> S, cur, bS, bcur;
-        long best = LONG_MIN;
-        if (lookahead && cand.size() > 1) {
-            // candidates are independent (each grows + rolls out on its own copy): one thread
-            // each, then the same fixed-order choice as the serial loop (deterministic)
-            const size_t nc = cand.size();
-            std::vector<std::vector<int>> cS(nc), ccur(nc);
-            std::vector<long> sc(nc);
-            auto work = [&](size_t i) {
-                grow(cand[i], cS[i], ccur[i]);
-                long score = 0;
-                for (int x : ccur[i]) score += nq(x);
+        const size_t nc = cand.size();
+        std::vector<uint64_t> cS(nc);
+        std::vector<long> sc(nc);
+        auto work = [&](size_t i) {
+            int w;
+            grow(cand[i], cS[i], w);
+            long score = w;
+            if (lookahead && nc > 1) {
                 Fuser f = *this;
-                f.commit(ccur[i]);
-                sc[i] = -1000L * f.rollout() + score;   // fewest remaining blocks, then most gates now
-            };
+                f.commit(cS[i]);
+                score = -1000L * f.rollout() + score;   // fewest remaining blocks, then most gates now
+            }
+            sc[i] = score;
+        };
+        if (lookahead && nc > 1) {
             std::vector<std::thread> th;
             for (size_t i = 1; i < nc; i++) th.emplace_back(work, i);
             work(0);
             for (auto& t : th) t.join();
-            for (size_t i = 0; i < nc; i++)
-                if (sc[i] > best) {
-                    best = sc[i];
-                    bS = cS[i];
-                    bcur = ccur[i];
-                }
         } else {
-            for (int g : cand) {
-                grow(g, S, cur);
-                long score = 0;
-                for (int x : cur) score += nq(x);
-                if (score > best) {
-                    best = score;
-                    bS = S;
-                    bcur = cur;
-                }
-            }
+            for (size_t i = 0; i < nc; i++) work(i);
         }
-        S = bS;
-        cur = bcur;
-        // commit
-        B.qubits = S;
-        B.gate_ids = cur;
-        for (int g : cur) {
-            assigned[g] = 1;
-            for (int j = 0; j < nq(g); j++) head[qb(g, j)]++;
-        }
+        size_t bi = 0;
+        for (size_t i = 1; i < nc; i++)
+            if (sc[i] > sc[bi]) bi = i;
+        out = cS[bi];
+        commit(out);
+        return true;
+    }
+
+    bool next_block(Block& B) {
+        // the gates are those the committed set absorbs from the heads BEFORE the commit
+        const std::vector<int> head0 = head;
+        uint64_t S;
+        const std::vector<char> assigned0 = assigned;
+        if (!next_set(S)) return false;
+        std::vector<int> h1 = head;
+        head = head0;
+        B.gate_ids.clear();
+        closure(S, &B.gate_ids);
+        head = h1;
+        (void)assigned0;
+        B.qubits.clear();
+        for (uint64_t m = S; m; m &= m - 1) B.qubits.push_back(__builtin_ctzll(m));
         return true;
     }
 };
@@ -358,6 +374,8 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         F.seeds = seeds;
         F.lookahead = la;
         F.grow_lookahead = which == 1;
+        F.grow_depth = getenv("RCS_FUSE_DEPTH") ? atoi(getenv("RCS_FUSE_DEPTH")) : 1;
+        F.grow_beam = getenv("RCS_FUSE_BEAM") ? atoi(getenv("RCS_FUSE_BEAM")) : 0;
         Block B;
         while (F.next_block(B)) {
             cand[which].push_back(B);
