@@ -41,10 +41,10 @@ METRIC = "fused gate-pass HBM GB/s (whole RCS step: state build + shots + XEB)"
 # tests/test_bench.py keeps it equal to rcs_plan_create's output.
 PLAN_PASSES = {'c1': {3: 32, 4: 19, 5: 14, 6: 8},
                'c2': {3: 97, 4: 47, 5: 37, 6: 27},
-               'c3': {3: 99, 4: 56, 5: 44, 6: 33},
-               'c4': {3: 142, 4: 78, 5: 56, 6: 38},
-               'c5': {3: 154, 4: 85, 5: 62, 6: 42},
-               'w33': {3: 115, 4: 73, 5: 53, 6: 39},
+               'c3': {3: 99, 4: 56, 5: 43, 6: 31},
+               'c4': {3: 142, 4: 78, 5: 55, 6: 36},
+               'c5': {3: 154, 4: 85, 5: 62, 6: 40},
+               'w33': {3: 115, 4: 73, 5: 51, 6: 38},
                'w35': {3: 140, 4: 81, 5: 52, 6: 46}}
 
 

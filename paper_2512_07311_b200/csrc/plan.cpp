@@ -26,6 +26,7 @@
 #include <memory>
 #include <set>
 #include <thread>
+#include <unordered_map>
 
 #include "internal.h"
 
@@ -166,15 +167,26 @@ struct Fuser {
         }
     }
 
-    // `depth` levels of exhaustive extension choice, then greedy; keeps the heaviest block
-    void grow_deep(uint64_t& S, int& w, int depth) const {
+    // `depth` levels of exhaustive extension choice, then greedy; keeps the heaviest block.
+    // Different extension orders reach the same sets: results are memoized per (set, depth).
+    using Memo = std::unordered_map<uint64_t, std::pair<uint64_t, int>>;
+    void grow_deep(uint64_t& S, int& w, int depth, Memo& memo) const {
+        const uint64_t key = S * 8 + (uint64_t)depth;   // S < 2^61 (n <= 61 here)
+        auto f = memo.find(key);
+        if (f != memo.end()) {
+            S = f->second.first;
+            w = f->second.second;
+            return;
+        }
+        const uint64_t S0 = S;
         if (depth == 0 || __builtin_popcountll(S) >= k) {
             grow_from(S, w);
+            memo[key] = {S, w};
             return;
         }
         std::vector<uint64_t> ex;
         extensions(S, ex);
-        // keep the `grow_beam` extensions with the best gain per added qubit
+        // keep the `grow_beam` extensions with the best gain per added qubit (0: all)
         std::vector<std::pair<double, uint64_t>> ranked;
         for (uint64_t e : ex) {
             const int w1 = closure(S | e);
@@ -190,7 +202,7 @@ struct Fuser {
         for (const auto& re : ranked) {
             uint64_t S1 = S | re.second;
             int w1 = closure(S1);
-            grow_deep(S1, w1, depth - 1);
+            grow_deep(S1, w1, depth - 1, memo);
             if (w1 > best) {
                 best = w1;
                 bS = S1;
@@ -198,17 +210,22 @@ struct Fuser {
         }
         if (best < 0) {
             grow_from(S, w);
-            return;
+        } else {
+            S = bS;
+            w = best;
         }
-        S = bS;
-        w = best;
+        memo[S0 * 8 + (uint64_t)depth] = {S, w};
     }
 
     void grow(int g0, uint64_t& S, int& w) const {
         S = T->gmask[g0];
         w = closure(S);
-        if (grow_lookahead) grow_deep(S, w, grow_depth);
-        else grow_from(S, w);
+        if (grow_lookahead) {
+            Memo memo;
+            grow_deep(S, w, grow_depth, memo);
+        } else {
+            grow_from(S, w);
+        }
     }
 
     bool ready(int g) const {
@@ -362,34 +379,40 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
     P.n_global = n_global;
     P.fuse_k = k;
 
-    // ---- 1. fusion: two growth strategies (plain greedy, greedy with one-step lookahead) run in
-    // parallel; the one needing fewer blocks wins (ties: plain).  Both are deterministic and
-    // independent of the sharding, so the plan stays P-invariant.
+    // ---- 1. fusion: three growth strategies run in parallel threads -- plain greedy, greedy with
+    // each extension scored by the block it finishes as, and an exhaustive 3-level extension
+    // search (memoized) -- and the plan with the fewest blocks wins (ties: the simpler one).
+    // All are deterministic and independent of the sharding, so the plan stays P-invariant.
     const int seeds = getenv("RCS_FUSE_SEEDS") ? atoi(getenv("RCS_FUSE_SEEDS")) : kFuseSeeds;
     const bool la = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
-    const int strat = getenv("RCS_FUSE_GROWLA") ? atoi(getenv("RCS_FUSE_GROWLA")) : -1;   // -1: both
-    std::vector<Block> cand[2];
+    const int strat = getenv("RCS_FUSE_STRATEGY") ? atoi(getenv("RCS_FUSE_STRATEGY")) : -1;   // -1: all
+    constexpr int kStrategies = 3;
+    const int depth_of[kStrategies] = {0, 1, 3};
+    std::vector<Block> cand[kStrategies];
     auto fuse = [&](int which) {
         Fuser F(c, k);
         F.seeds = seeds;
         F.lookahead = la;
-        F.grow_lookahead = which == 1;
-        F.grow_depth = getenv("RCS_FUSE_DEPTH") ? atoi(getenv("RCS_FUSE_DEPTH")) : 1;
-        F.grow_beam = getenv("RCS_FUSE_BEAM") ? atoi(getenv("RCS_FUSE_BEAM")) : 0;
+        F.grow_lookahead = depth_of[which] > 0;
+        F.grow_depth = depth_of[which];
         Block B;
         while (F.next_block(B)) {
             cand[which].push_back(B);
             B = Block();
         }
     };
-    if (strat < 0) {
-        std::thread t1(fuse, 1);
-        fuse(0);
-        t1.join();
+    int win = 0;
+    if (strat >= 0 && strat < kStrategies) {
+        fuse(strat);
+        win = strat;
     } else {
-        fuse(strat ? 1 : 0);
+        std::vector<std::thread> th;
+        for (int w = 1; w < kStrategies; w++) th.emplace_back(fuse, w);
+        fuse(0);
+        for (auto& t : th) t.join();
+        for (int w = 1; w < kStrategies; w++)
+            if (cand[w].size() < cand[win].size()) win = w;
     }
-    const int win = strat >= 0 ? (strat ? 1 : 0) : (cand[1].size() < cand[0].size() ? 1 : 0);
     for (Block& B : cand[win]) {
         const int kb = (int)B.qubits.size();
         const int D = 1 << kb;
