@@ -387,7 +387,7 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
     const bool la = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
     const int strat = getenv("RCS_FUSE_STRATEGY") ? atoi(getenv("RCS_FUSE_STRATEGY")) : -1;   // -1: all
     constexpr int kStrategies = 3;
-    const int depth_of[kStrategies] = {0, 1, 3};
+    const int depth_of[kStrategies] = {0, 1, getenv("RCS_FUSE_DEPTH") ? atoi(getenv("RCS_FUSE_DEPTH")) : 3};
     std::vector<Block> cand[kStrategies];
     auto fuse = [&](int which) {
         Fuser F(c, k);
