@@ -685,9 +685,16 @@ rcs_status sample_impl(rcs_state* s, uint64_t shots, uint64_t seed, uint64_t off
     if (st) return st;
     const bool out_dev = is_device_ptr(out_x);
     const bool u_dev = u ? is_device_ptr(u) : false;
-    cudaEvent_t e0, e1;
-    CUDA_TRY(cudaEventCreate(&e0));
-    CUDA_TRY(cudaEventCreate(&e1));
+    struct Events {   // destroyed on every exit path
+        cudaEvent_t a = nullptr, b = nullptr;
+        ~Events() {
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } ev;
+    CUDA_TRY(cudaEventCreate(&ev.a));
+    CUDA_TRY(cudaEventCreate(&ev.b));
+    cudaEvent_t e0 = ev.a, e1 = ev.b;
     CUDA_TRY(cudaEventRecord(e0, c->stream));
     for (uint64_t s0 = 0; s0 < shots; s0 += s->chunk) {
         const uint64_t cnt = std::min(s->chunk, shots - s0);
@@ -733,8 +740,6 @@ rcs_status sample_impl(rcs_state* s, uint64_t shots, uint64_t seed, uint64_t off
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     if (rep) {
         rep->shots = shots;
         rep->total_prob = s->T_total;
@@ -1052,7 +1057,10 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             }
     }
 
+    // every event this build creates is owned here and destroyed on every exit path
+    std::vector<cudaEvent_t> owned;
     auto fail = [&](rcs_status code) {
+        for (auto& e : owned) cudaEventDestroy(e);
         delete s;
         return code;
     };
@@ -1068,8 +1076,11 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     cudaStream_t stream = ctx->stream;
     cudaEvent_t eb0, eb1, ec0;
     BUILD_TRY(cudaEventCreate(&eb0));
+    owned.push_back(eb0);
     BUILD_TRY(cudaEventCreate(&eb1));
+    owned.push_back(eb1);
     BUILD_TRY(cudaEventCreate(&ec0));
+    owned.push_back(ec0);
     // tensor-core passes: packed operands cached per (circuit, plan, n_local); the device copy
     // lives in the context and is re-uploaded only when the circuit or plan changes
     std::shared_ptr<const TcPack> tcp;
@@ -1121,7 +1132,6 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     const int tc_pair = getenv("RCS_TC_PAIR") ? atoi(getenv("RCS_TC_PAIR")) : 0;   // read per build (tests toggle it)
     std::vector<float> mbuf;
     std::vector<Span> spans;
-    std::vector<cudaEvent_t> owned;
     // pipelined remaps (f1): on unless RCS_OVERLAP=0; 2^cb chunks, `reserve` SMs left to the swaps
     static const int ov_on = getenv("RCS_OVERLAP") ? atoi(getenv("RCS_OVERLAP")) : 1;
     static const int ov_cb = getenv("RCS_OVERLAP_CHUNKS") ? atoi(getenv("RCS_OVERLAP_CHUNKS")) : 2;
@@ -1286,11 +1296,9 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             }
         }
     }
-    for (auto& e : owned) cudaEventDestroy(e);
+    for (auto& e : owned) cudaEventDestroy(e);   // includes eb0, eb1, ec0
+    owned.clear();
     if (R.pass_ms_min > R.pass_ms_max) R.pass_ms_min = 0;
-    cudaEventDestroy(eb0);
-    cudaEventDestroy(eb1);
-    cudaEventDestroy(ec0);
     R.pass_bytes = pass_bytes;
     R.remap_bytes = remap_bytes;
     R.norm = s->T_total;
