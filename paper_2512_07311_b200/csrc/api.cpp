@@ -13,6 +13,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <unistd.h>
@@ -362,6 +363,89 @@ rcs_status setup_peers(rcs_context* c, void* amps, rcs_error* err, void* stage =
     c->p2p = true;
     c->p2p_stage = ok1;
     return RCS_OK;
+}
+
+// Fusion shared by the ranks of a context (world > 1): the strategies are split round-robin
+// over the ranks, the block counts all-gathered, and the winning rank (fewest blocks, ties to
+// the lower strategy -- the single-process rule, so the plan equals the 1-GPU plan) broadcasts
+// its blocks; every rank then derives matrices and remaps itself.
+rcs_status plan_distributed(rcs_context* c, const Circuit& circ, int fuse_k, int plan_g, Plan& out, rcs_error* err) {
+    const int k = plan_block_k(circ.n, fuse_k, plan_g);
+    std::vector<Block> mine[kFuseStrategies];
+    int64_t cnt[kFuseStrategies];
+    {
+        std::vector<std::thread> th;
+        for (int s = 0; s < kFuseStrategies; s++) {
+            cnt[s] = INT64_MAX;
+            if (s % c->world != c->rank || k <= 0) continue;
+            th.emplace_back([&, s] { fuse_strategy(circ, k, s, mine[s]); });
+        }
+        for (auto& t : th) t.join();
+        for (int s = 0; s < kFuseStrategies; s++)
+            if (s % c->world == c->rank && k > 0) cnt[s] = (int64_t)mine[s].size();
+    }
+    int64_t* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, sizeof(int64_t) * kFuseStrategies * (c->world + 1)));
+    struct Free {
+        void* p;
+        ~Free() { cudaFree(p); }
+    } fr{d};
+    CUDA_TRY(cudaMemcpyAsync(d, cnt, sizeof cnt, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(ncclAllGather(d, d + kFuseStrategies, kFuseStrategies, ncclInt64, c->comm, c->stream));
+    std::vector<int64_t> all((size_t)kFuseStrategies * c->world);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), d + kFuseStrategies, all.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    int win = 0;
+    int64_t best = INT64_MAX;
+    for (int s = 0; s < kFuseStrategies; s++) {
+        const int64_t v = all[(size_t)(s % c->world) * kFuseStrategies + s];
+        if (v < best) {
+            best = v;
+            win = s;
+        }
+    }
+    const int owner = win % c->world;
+    // serialize: [nblocks, (qubit mask, ngates, gate ids...) per block]
+    std::vector<int64_t> buf;
+    if (c->rank == owner) {
+        buf.push_back((int64_t)mine[win].size());
+        for (const Block& B : mine[win]) {
+            int64_t m = 0;
+            for (int q : B.qubits) m |= 1ll << q;
+            buf.push_back(m);
+            buf.push_back((int64_t)B.gate_ids.size());
+            for (int g : B.gate_ids) buf.push_back(g);
+        }
+    }
+    int64_t len = (int64_t)buf.size();
+    int64_t* dl = nullptr;
+    CUDA_TRY(cudaMalloc(&dl, 8));
+    Free fr2{dl};
+    CUDA_TRY(cudaMemcpyAsync(dl, &len, 8, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(ncclBroadcast(dl, dl, 1, ncclInt64, owner, c->comm, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&len, dl, 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    buf.resize((size_t)len);
+    int64_t* db = nullptr;
+    CUDA_TRY(cudaMalloc(&db, 8 * (size_t)std::max<int64_t>(len, 1)));
+    Free fr3{db};
+    if (c->rank == owner) CUDA_TRY(cudaMemcpyAsync(db, buf.data(), 8 * len, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(ncclBroadcast(db, db, len, ncclInt64, owner, c->comm, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(buf.data(), db, 8 * len, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::vector<Block> blocks;
+    size_t at = 0;
+    const int64_t nb = len > 0 ? buf[at++] : 0;
+    for (int64_t b = 0; b < nb; b++) {
+        Block B;
+        const int64_t m = buf[at++];
+        for (int q = 0; q < 63; q++)
+            if ((m >> q) & 1) B.qubits.push_back(q);
+        const int64_t ng = buf[at++];
+        for (int64_t i = 0; i < ng; i++) B.gate_ids.push_back((int)buf[at++]);
+        blocks.push_back(std::move(B));
+    }
+    return build_plan(circ, fuse_k, plan_g, out, err, &blocks);
 }
 
 // stream-ordered barrier over all ranks (no rank proceeds past it before every rank reached it)
@@ -996,7 +1080,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             plan_ptr = f->second;
         } else {
             auto np = std::make_shared<Plan>();
-            rcs_status pst = build_plan(circ->c, o.fuse_k, plan_g, *np, err);
+            rcs_status pst = ctx->world > 1 ? plan_distributed(ctx, circ->c, o.fuse_k, plan_g, *np, err)
+                                            : build_plan(circ->c, o.fuse_k, plan_g, *np, err);
             if (pst) return pst;
             plan_ptr = np;
             cc->plans[key] = plan_ptr;

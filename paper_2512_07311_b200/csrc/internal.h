@@ -77,7 +77,13 @@ constexpr bool kFuseLookahead = true;
 constexpr bool kRemapPrefetch = true;   // remaps also bring in soon-needed global qubits
 constexpr bool kInitialPlacement = true;   // start with the latest-used qubits global (free: |0> state)
 
-rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err);
+// given: the fused blocks (qubits + gate ids) to use instead of running the fuser
+rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err,
+                      const std::vector<Block>* given = nullptr);
+constexpr int kFuseStrategies = 3;
+void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out);
+int fuse_best(const Circuit& c, int k, std::vector<Block>* cand /* [kFuseStrategies] */);
+int plan_block_k(int n, int fuse_k, int n_global);   // the block width build_plan uses
 
 void set_error(rcs_error* err, int code, const char* fmt, ...);
 

@@ -353,7 +353,53 @@ void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb
 
 }  // namespace
 
-rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err) {
+// Fusion strategies (P-independent, deterministic): 0 plain greedy, 1 greedy with every
+// candidate extension scored by the block it finishes as, 2 exhaustive 3-level extension search
+// (memoized); all with the rollout lookahead over seed gates.  The plan with the fewest blocks
+// wins, ties to the lower index.
+void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) {
+    const int seeds = getenv("RCS_FUSE_SEEDS") ? atoi(getenv("RCS_FUSE_SEEDS")) : kFuseSeeds;
+    const bool la = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
+    const int deep = getenv("RCS_FUSE_DEPTH") ? atoi(getenv("RCS_FUSE_DEPTH")) : 3;
+    const int depth_of[kFuseStrategies] = {0, 1, deep};
+    Fuser F(c, k);
+    F.seeds = seeds;
+    F.lookahead = la;
+    F.grow_lookahead = depth_of[which] > 0;
+    F.grow_depth = depth_of[which];
+    out.clear();
+    Block B;
+    while (F.next_block(B)) {
+        out.push_back(B);
+        B = Block();
+    }
+}
+
+int fuse_best(const Circuit& c, int k, std::vector<Block>* cand) {
+    const int strat = getenv("RCS_FUSE_STRATEGY") ? atoi(getenv("RCS_FUSE_STRATEGY")) : -1;   // -1: all
+    if (strat >= 0 && strat < kFuseStrategies) {
+        fuse_strategy(c, k, strat, cand[strat]);
+        return strat;
+    }
+    std::vector<std::thread> th;
+    for (int w = 1; w < kFuseStrategies; w++) th.emplace_back([&, w] { fuse_strategy(c, k, w, cand[w]); });
+    fuse_strategy(c, k, 0, cand[0]);
+    for (auto& t : th) t.join();
+    int win = 0;
+    for (int w = 1; w < kFuseStrategies; w++)
+        if (cand[w].size() < cand[win].size()) win = w;
+    return win;
+}
+
+int plan_block_k(int n, int fuse_k, int n_global) {
+    const int n_local = n - n_global;
+    if (fuse_k <= 0) fuse_k = n_local >= kTcMinLocal ? 6 : 4;
+    if (fuse_k == 6 && n_local < kTcMinLocal) fuse_k = 5;
+    return std::min(fuse_k, n_local);
+}
+
+rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err,
+                      const std::vector<Block>* given) {
     if (fuse_k > 6) {
         set_error(err, RCS_ERR_ARG, "fuse_k must be in [1, 6] (got %d)", fuse_k);
         return RCS_ERR_ARG;
@@ -379,39 +425,13 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
     P.n_global = n_global;
     P.fuse_k = k;
 
-    // ---- 1. fusion: three growth strategies run in parallel threads -- plain greedy, greedy with
-    // each extension scored by the block it finishes as, and an exhaustive 3-level extension
-    // search (memoized) -- and the plan with the fewest blocks wins (ties: the simpler one).
-    // All are deterministic and independent of the sharding, so the plan stays P-invariant.
-    const int seeds = getenv("RCS_FUSE_SEEDS") ? atoi(getenv("RCS_FUSE_SEEDS")) : kFuseSeeds;
-    const bool la = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
-    const int strat = getenv("RCS_FUSE_STRATEGY") ? atoi(getenv("RCS_FUSE_STRATEGY")) : -1;   // -1: all
-    constexpr int kStrategies = 3;
-    const int depth_of[kStrategies] = {0, 1, getenv("RCS_FUSE_DEPTH") ? atoi(getenv("RCS_FUSE_DEPTH")) : 3};
-    std::vector<Block> cand[kStrategies];
-    auto fuse = [&](int which) {
-        Fuser F(c, k);
-        F.seeds = seeds;
-        F.lookahead = la;
-        F.grow_lookahead = depth_of[which] > 0;
-        F.grow_depth = depth_of[which];
-        Block B;
-        while (F.next_block(B)) {
-            cand[which].push_back(B);
-            B = Block();
-        }
-    };
+    // ---- 1. fusion (or the blocks another rank chose, see api.cpp)
+    std::vector<Block> cand[kFuseStrategies];
     int win = 0;
-    if (strat >= 0 && strat < kStrategies) {
-        fuse(strat);
-        win = strat;
+    if (given) {
+        cand[0] = *given;
     } else {
-        std::vector<std::thread> th;
-        for (int w = 1; w < kStrategies; w++) th.emplace_back(fuse, w);
-        fuse(0);
-        for (auto& t : th) t.join();
-        for (int w = 1; w < kStrategies; w++)
-            if (cand[w].size() < cand[win].size()) win = w;
+        win = fuse_best(c, k, cand);
     }
     for (Block& B : cand[win]) {
         const int kb = (int)B.qubits.size();
