@@ -161,7 +161,9 @@ Layout scratch_layout(int nl, int world, int virt, uint64_t staging_bytes, int b
     if (world > 1) st = staging_bytes ? staging_bytes : (256ull << 20);
     uint64_t end = align_up(L.stage_off + st);
     L.stage_end = end;
-    if (world >= 4) {   // pull-mode remaps: outgoing elements of one 2^-kPullCb chunk, twice
+    // pull-mode remaps (RCS_REMAP_PULL=1, world >= 4): outgoing elements of one 2^-kPullCb chunk, twice
+    static const bool pull_on = getenv("RCS_REMAP_PULL") && atoi(getenv("RCS_REMAP_PULL")) != 0;
+    if (world >= 4 && pull_on) {
         L.pull_elems = (1ull << (nl - kPullCb)) / (uint64_t)world * (uint64_t)(world - 1);
         L.pull_off = end;
         end = align_up(L.pull_off + 2 * L.pull_elems * 8);
