@@ -67,7 +67,7 @@ struct Plan {
 // moves amplitude pairs along bit 0) and makes qubits 0..5 always local, so a 5-qubit block
 // can be padded onto the tensor-core pass with one of them whatever the sharding (the
 // padded arithmetic depends on which qubit pads it: the choice must be layout-independent)
-constexpr int kPinnedLow = 6;
+constexpr int kPinnedLow = 7;
 // the tensor-core pass tiles 6 target + 6 column bits
 constexpr int kTcMinLocal = 12;
 // fuser: ready gates tried as block seeds besides the earliest unassigned one

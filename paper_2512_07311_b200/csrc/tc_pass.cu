@@ -165,6 +165,12 @@ __device__ __forceinline__ float2 f2mul(float2 v, float s) {   // packed f32x2 m
                  "r"(R[16]), "r"(R[17]), "r"(R[18]), "r"(R[19]), "r"(R[20]), "r"(R[21]), "r"(R[22]), "r"(R[23]),  \
                  "r"(R[24]), "r"(R[25]), "r"(R[26]), "r"(R[27]), "r"(R[28]), "r"(R[29]), "r"(R[30]), "r"(R[31]))
 
+#define TMEM_ST16(addr, R)                                                                                       \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+                 "%15,%16};" ::"r"(addr),                                                                          \
+                 "r"(R[0]), "r"(R[1]), "r"(R[2]), "r"(R[3]), "r"(R[4]), "r"(R[5]), "r"(R[6]), "r"(R[7]),          \
+                 "r"(R[8]), "r"(R[9]), "r"(R[10]), "r"(R[11]), "r"(R[12]), "r"(R[13]), "r"(R[14]), "r"(R[15]))
+
 #define TMEM_LD32(addr, R)                                                                                     \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
                  "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"               \
@@ -975,6 +981,217 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_co
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// =====================================================================================
+// K12: the transposed product for layouts with no target among positions 0..6.
+//     Y^T (128 j x 128 n) = X^T (128 j x 128 k) . B (128 k x 128 n),  B[k][n] = A_K9[n][k]
+// The state tile (64 target combinations t x 128 columns j = index bits 0..6, 8192 amplitudes)
+// is the TMEM operand A: converter thread j packs its row (fp16 hi/lo of re/im for every t)
+// with tcgen05.st -- no B-stage round trip through shared memory -- and the constant matrix is
+// the shared-memory operand.  D rows are columns j, so an epilogue warp stores 32 consecutive
+// amplitudes (256 B) per target combination straight from registers -- no staging.  Shared
+// memory per 8192 amplitudes: TMA 64 KB + converter reads 64 KB + MMA matrix reads 96 KB (K9:
+// ~2x that per amplitude).  K order (t + 64 c), k-steps and accumulators are K9's, so each output
+// element is the same sum of the same products.
+//   warp  13   producer: TMA of the 64 runs (1 KB each) of a tile into a raw slot
+//   warps 0-7  converters: warp w -> TMEM lanes 32 (w & 3).., t half w >> 2 -> A buffer
+//   warp  12   MMA: 24 x tcgen05.mma (M=128, N=128, K=16), A = state (TMEM), B = matrix (smem)
+//   warps 8-11 epilogue: D (2 accumulators) -> registers -> global, memory order per warp
+// TMEM: A buffers [0,128) and [128,256) (hi at +0, lo at +64); D acc 0 at 256, acc 1 at 384.
+struct TcTArgs {
+    float2* amps;
+    const uint32_t* a;       // K9-packed A (hi, lo): row n, word c = k pair (2c, 2c+1)
+    uint64_t ntiles;
+    int pos[6];              // physical position of matrix bit i (all >= 7)
+    int nins;                // 13 sub-cube positions (0..6 and the targets), ascending
+    int ins[13];
+    uint64_t fmask, dstride; // tile-index deposit (as K9)
+};
+
+constexpr uint32_t kTRaw = 8192 * 8;                  // one tile: 64 KB
+constexpr uint32_t kTMat = 2 * 128 * 128 * 2;         // B hi + lo: 64 KB
+constexpr uint32_t kTCtl = 1024;
+constexpr uint32_t kTSmem = 2 * kTRaw + kTMat + kTCtl;
+
+__global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constant__ TcTArgs p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    float2* raw = reinterpret_cast<float2*>(smem);                       // [2][64 t][128 j]
+    uint8_t* mat = smem + 2 * kTRaw;                                      // B hi | B lo (K-major)
+    uint8_t* ctl = mat + kTMat;
+    uint64_t* rfull = reinterpret_cast<uint64_t*>(ctl);   // [2]
+    uint64_t* rempty = rfull + 2;                         // [2]
+    uint64_t* afull = rempty + 2;                         // [2]
+    uint64_t* aempty = afull + 2;                         // [2]
+    uint64_t* dfull = aempty + 2;                         // [1]
+    uint64_t* dempty = dfull + 1;                         // [1]
+    uint64_t* offt = dempty + 1;                          // [64] target-combination offsets
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(offt + 64);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&rfull[i], 1);
+            mbar_init(&rempty[i], kLoadWarps * 32);
+            mbar_init(&afull[i], kLoadWarps * 32);
+            mbar_init(&aempty[i], 1);
+        }
+        mbar_init(dfull, 1);
+        mbar_init(dempty, kEpiThreads);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (threadIdx.x < 64) {
+        uint64_t ot = 0;
+        for (int i = 0; i < 6; i++)
+            if ((threadIdx.x >> i) & 1) ot |= 1ull << p.pos[i];
+        offt[threadIdx.x] = ot;
+    }
+    // the matrix as the K-major shared-memory operand: core chunk (n, c) = A_K9 words [n][4c..4c+3]
+    for (int e = threadIdx.x; e < 2 * 128 * 16; e += blockDim.x) {
+        const int h = e >> 11, n = (e >> 4) & 127, c = e & 15;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.a + (size_t)h * 128 * 64 + (size_t)n * 64 + 4 * c));
+        *reinterpret_cast<uint4*>(mat + h * (kTMat / 2) + bchunk(n, c)) = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    auto tile_base = [&](uint64_t tile) {
+        uint64_t b = tile;
+#pragma unroll
+        for (int i = 0; i < 13; i++) b = ins0(b, p.ins[i]);
+        return b;
+    };
+    const uint64_t ntiles = p.ntiles;
+    const uint64_t first = blockIdx.x;
+
+    if (warp == kProdWarp) {
+        uint64_t it = 0, bp = tile_base(first);
+        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
+            const int slot = it & 1;
+            mbar_wait(&rempty[slot], ((it >> 1) & 1) ^ 1);
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[slot])),
+                             "r"(kTRaw)
+                             : "memory");
+            __syncwarp();
+            const float2* src = p.amps + bp;
+            const uint32_t dst = su32(raw + (size_t)slot * 8192);
+            for (int t = lane; t < 64; t += 32)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dst + t * 1024u),
+                    "l"(src + offt[t]), "r"(1024u), "r"(su32(&rfull[slot]))
+                    : "memory");
+        }
+    } else if (warp < kLoadWarps) {
+        // ---------------- converters: thread j = 32 (w & 3) + lane, t in [32 (w >> 2), +32)
+        const int q = warp & 3, th = warp >> 2;
+        const int j = 32 * q + lane;
+        uint64_t it = 0;
+        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++) {
+            const int slot = it & 1, b = it & 1;
+            mbar_wait(&rfull[slot], (it >> 1) & 1);
+            mbar_wait(&aempty[b], ((it >> 1) & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float2* rb = raw + (size_t)slot * 8192 + j;
+            // K order t + 64 c: word c < 32 packs re of t = 2c, 2c+1; word 32 + c the im parts
+            uint32_t hre[16], lre[16], him[16], lim[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const int t = 32 * th + 2 * u;
+                const float2 v0 = f2mul(rb[(size_t)t * 128], 32768.f), v1 = f2mul(rb[(size_t)(t + 1) * 128], 32768.f);
+                split_h2(v0.x, v1.x, hre[u], lre[u]);
+                split_h2(v0.y, v1.y, him[u], lim[u]);
+            }
+            mbar_arrive(&rempty[slot]);
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 128 * b + 16 * th;
+            TMEM_ST16(ta, hre);             // hi, re words [16 th, +16)
+            TMEM_ST16(ta + 32, him);        // hi, im words [32 + 16 th, +16)
+            TMEM_ST16(ta + 64, lre);        // lo
+            TMEM_ST16(ta + 96, lim);
+            asm volatile("tcgen05.wait::st.sync.aligned;");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            mbar_arrive(&afull[b]);
+        }
+    } else if (warp == kMmaWarp) {
+        // ---------------- MMA issuer: M = 128 (j), N = 128 (n = 2 t_o + c_o), K = 16 per step
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        const uint64_t bh0 = bdesc(su32(mat)), bl0 = bdesc(su32(mat + kTMat / 2));
+        uint64_t it = 0;
+        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++) {
+            const int b = it & 1;
+            mbar_wait(&afull[b], (it >> 1) & 1);
+            mbar_wait(dempty, (it & 1) ^ 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                const uint32_t d0 = tmem + 256;
+                const uint32_t xh = tmem + 128 * b, xl = xh + 64;   // state hi / lo (A)
+                // cross terms first (x_hi u_lo, x_lo u_hi), then x_hi u_hi: k-steps 0-3 -> acc 0, 4-7 -> acc 1
+                MMA_F16(d0, xh, bl0, idesc, 0);
+                MMA_F16(d0, xl, bh0, idesc, 1);
+#pragma unroll
+                for (int ks = 1; ks < 8; ks++) {
+                    MMA_F16(d0, xh + ks * 8, bl0 + ks * 16, idesc, 1);
+                    MMA_F16(d0, xl + ks * 8, bh0 + ks * 16, idesc, 1);
+                }
+#pragma unroll
+                for (int ks = 0; ks < 4; ks++) MMA_F16(d0, xh + ks * 8, bh0 + ks * 16, idesc, 1);
+                MMA_F16(d0 + 128, xh + 4 * 8, bh0 + 4 * 16, idesc, 0);
+#pragma unroll
+                for (int ks = 5; ks < 8; ks++) MMA_F16(d0 + 128, xh + ks * 8, bh0 + ks * 16, idesc, 1);
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(&aempty[b])));
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    su32(dfull)));
+            }
+            __syncwarp();
+        }
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+        // ---------------- epilogue: lane quarter q holds columns j = 32 q + lane
+        const int q = warp & 3;
+        const int j = 32 * q + lane;
+        const float us = 1.f / (16384.f * 32768.f);
+        uint64_t it = 0, bp = tile_base(first);
+        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
+            mbar_wait(dfull, it & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float2* dst = p.amps + bp + j;
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256;
+#pragma unroll
+            for (int s4 = 0; s4 < 4; s4++) {   // 32 columns n = 16 target combinations (re, im)
+                uint32_t a0[32], a1[32];
+                TMEM_LD32(ta + 32 * s4, a0);
+                TMEM_LD32(ta + 128 + 32 * s4, a1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+                if (s4 == 3) {
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(dempty);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    float o0, o1;   // (acc0 + acc1) * 2^-29 of (re, im) of t = 16 s4 + c / 2
+                    asm("{\n.reg .b64 x, y, u;\n"
+                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\n"
+                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\n"
+                        "mov.b64 {%0, %1}, x;\n}"
+                        : "=f"(o0), "=f"(o1)
+                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(us));
+                    __stcs(dst + offt[16 * s4 + c / 2], make_float2(o0, o1));
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 }  // namespace
 
 size_t tc_matrix_words() { return 2 * 128 * 64; }
@@ -1024,8 +1241,50 @@ uint64_t tc_reserved_mask(int nl, const int* pos) {
     return m;
 }
 
+// K12 launcher (no target among positions 0..6; whole index space, no chunk bits)
+static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms,
+                                 cudaStream_t st) {
+    TcTArgs p{};
+    p.amps = amps;
+    p.a = d_a;
+    p.ntiles = 1ull << (nl - 13);
+    uint64_t insmask = 0x7f;
+    for (int i = 0; i < 6; i++) {
+        p.pos[i] = pos[i];
+        insmask |= 1ull << pos[i];
+    }
+    p.nins = 0;
+    for (int b = 0; b < nl; b++)
+        if ((insmask >> b) & 1) p.ins[p.nins++] = b;
+    if (p.nins != 13) return cudaErrorInvalidValue;
+    const uint64_t grid = p.ntiles < (uint64_t)num_sms ? p.ntiles : (uint64_t)num_sms;
+    p.fmask = ~insmask & ((1ull << nl) - 1);
+    uint64_t v = grid, d = 0;
+    for (int b = 0; b < 64 && v; b++)
+        if ((p.fmask >> b) & 1) {
+            if (v & 1) d |= 1ull << b;
+            v >>= 1;
+        }
+    p.dstride = d;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_pass_tct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    count_launch();
+    k_pass_tct<<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
                          const int* fix, int nfix, uint64_t fixval) {
+    {   // K12 when no target sits in positions 0..6 (read per launch: tests toggle RCS_TC_NOTRANS)
+        bool low = false;
+        for (int i = 0; i < 6; i++) low = low || pos[i] < 7;
+        if (!low && nfix == 0 && nl >= 14 && !getenv("RCS_TC_NOTRANS"))
+            return gate_pass_tct(amps, nl, pos, d_a, num_sms, st);
+    }
     if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
     p.amps = amps;
