@@ -1268,7 +1268,13 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         }
         // two consecutive tensor-core passes in one launch (K11): pass B re-reads pass A's output
         // from L2 chunk by chunk, one HBM round trip for both
-        if (tc_pair && is_tc(ii) && is_tc(ii + 1)) {
+        // (K11 implements K9's arithmetic: blocks that run on K12 -- no qubit among 0..6 -- are not paired)
+        auto k9_block = [&](size_t i) {
+            for (int t = 0; t < 6; t++)
+                if (tcp->pos[i][t] < 7) return true;
+            return false;
+        };
+        if (tc_pair && is_tc(ii) && is_tc(ii + 1) && k9_block(ii) && k9_block(ii + 1)) {
             const int* pp[2] = {tcp->pos[ii].data(), tcp->pos[ii + 1].data()};
             const int cbits = dev::tc_multi_chunk_bits(nl, 2, pp);
             const int max_bits = getenv("RCS_PAIR_MAXBITS") ? atoi(getenv("RCS_PAIR_MAXBITS")) : kPairMaxChunkBits;
