@@ -238,7 +238,7 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
         for (int i = 0; i < it.k; i++) out.pos[ii][i] = it.pos[i];
         if (it.k == 5) {   // pad qubit: lowest of the pinned qubits 0..5 not in the block
             int pad = -1;
-            for (int b = 0; b < kPinnedLow && pad < 0; b++) {
+            for (int b = 0; b < P.pinned && pad < 0; b++) {
                 bool used = false;
                 for (int i = 0; i < 5; i++) used = used || it.pos[i] == b;
                 if (!used) pad = b;
@@ -664,7 +664,7 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
 // chunk bits for a pipelined remap: the highest positions outside `excl`; false if too few
 bool choose_chunk_bits(int nl, uint64_t excl, int cb, int* fix) {
     int got = 0;
-    for (int b = nl - 1; b >= kPinnedLow && got < cb; b--)
+    for (int b = nl - 1; b >= 7 && got < cb; b--)   // above every tile sub-cube's low bits
         if (!((excl >> b) & 1)) fix[got++] = b;
     if (got < cb) return false;
     std::sort(fix, fix + cb);

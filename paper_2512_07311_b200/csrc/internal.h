@@ -58,6 +58,7 @@ struct Plan {
     int n_passes = 0, n_remaps = 0, n_swaps = 0;
     // items [restore_begin, end) only bring the layout back to canonical; final_pos[q] is the
     // physical position of qubit q before them (>= n - n_global: a rank bit)
+    int pinned = 6;                 // physical positions [0, pinned) never move (kPinnedLow or 7)
     int restore_begin = 0;
     std::vector<int> final_pos;
     std::vector<int> initial_pos;   // empty: canonical start (qubit q at position q)
@@ -67,7 +68,10 @@ struct Plan {
 // moves amplitude pairs along bit 0) and makes qubits 0..5 always local, so a 5-qubit block
 // can be padded onto the tensor-core pass with one of them whatever the sharding (the
 // padded arithmetic depends on which qubit pads it: the choice must be layout-independent)
-constexpr int kPinnedLow = 7;
+constexpr int kPinnedLow = 6;
+// 6-qubit (tensor-core) plans pin one more: the K9 / K12 choice (K12 iff no target among
+// positions 0..6) must be a function of the block alone
+inline int pinned_low(int k) { return k >= 5 ? 7 : kPinnedLow; }
 // the tensor-core pass tiles 6 target + 6 column bits
 constexpr int kTcMinLocal = 12;
 // fuser: ready gates tried as block seeds besides the earliest unassigned one

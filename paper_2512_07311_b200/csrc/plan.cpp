@@ -415,15 +415,17 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
     // 6-qubit blocks run only on the tensor-core pass, which needs n_local >= 12
     if (fuse_k == 6 && n_local < kTcMinLocal) fuse_k = 5;
     int k = std::min(fuse_k, n_local);
-    if (n_global > 0 && n_local - kPinnedLow < k) {
+    const int pinned = pinned_low(k);
+    if (n_global > 0 && n_local - pinned < k) {
         set_error(err, RCS_ERR_ARG, "too many global qubits: n=%d g=%d leaves %d movable local qubits < k=%d",
-                  n, n_global, n_local - kPinnedLow, k);
+                  n, n_global, n_local - pinned, k);
         return RCS_ERR_ARG;
     }
     Plan P;
     P.n = n;
     P.n_global = n_global;
     P.fuse_k = k;
+    P.pinned = pinned_low(k);
 
     // ---- 1. fusion (or the blocks another rank chose, see api.cpp)
     std::vector<Block> cand[kFuseStrategies];
@@ -462,7 +464,7 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
     // start with any qubits at no cost -- take the movable ones whose first use is latest
     if (kInitialPlacement && n_global > 0) {
         std::vector<int> movable;
-        for (int q = kPinnedLow; q < n; q++) movable.push_back(q);
+        for (int q = pinned; q < n; q++) movable.push_back(q);
         std::stable_sort(movable.begin(), movable.end(), [&](int a, int b2) {
             const int fa = next_use(a, 0), fb = next_use(b2, 0);
             if (fa != fb) return fa > fb;
@@ -504,7 +506,7 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
             if (pos[q] >= n_local) need.push_back(q);
         if (!need.empty()) {
             std::vector<int> cand;
-            for (int p = kPinnedLow; p < n_local; p++) {
+            for (int p = pinned; p < n_local; p++) {
                 int q = occ[p];
                 if (!std::count(blk.qubits.begin(), blk.qubits.end(), q)) cand.push_back(q);
             }
@@ -568,7 +570,7 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         if (wrong.empty()) break;
         // canonical qubits sitting on the wrong global position: park them locally first
         pairs.clear();
-        int L = kPinnedLow;
+        int L = pinned;
         for (int G : wrong) {
             while (L < n_local && occ[L] >= n_local) L++;
             pairs.push_back({G, L++});

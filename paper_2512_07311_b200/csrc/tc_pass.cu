@@ -1002,8 +1002,9 @@ struct TcTArgs {
     const uint32_t* a;       // K9-packed A (hi, lo): row n, word c = k pair (2c, 2c+1)
     uint64_t ntiles;
     int pos[6];              // physical position of matrix bit i (all >= 7)
-    int nins;                // 13 sub-cube positions (0..6 and the targets), ascending
-    int ins[13];
+    int nins;                // 13 sub-cube positions (0..6 and the targets) + chunk bits, ascending
+    int ins[17];
+    uint64_t fixval;         // chunk bits (pipelined remaps), as K9
     uint64_t fmask, dstride; // tile-index deposit (as K9)
 };
 
@@ -1063,7 +1064,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     auto tile_base = [&](uint64_t tile) {
         uint64_t b = tile;
 #pragma unroll
-        for (int i = 0; i < 13; i++) b = ins0(b, p.ins[i]);
+        for (int i = 0; i < 17; i++)
+            if (i < p.nins) b = ins0(b, p.ins[i]);
         return b;
     };
     const uint64_t ntiles = p.ntiles;
@@ -1079,7 +1081,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                              "r"(kTRaw)
                              : "memory");
             __syncwarp();
-            const float2* src = p.amps + bp;
+            const float2* src = p.amps + (bp | p.fixval);
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
             for (int t = lane; t < 64; t += 32)
                 asm volatile(
@@ -1160,7 +1162,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
             mbar_wait(dfull, it & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            float2* dst = p.amps + bp + j;
+            float2* dst = p.amps + (bp | p.fixval) + j;
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256;
 #pragma unroll
             for (int s4 = 0; s4 < 4; s4++) {   // 32 columns n = 16 target combinations (re, im)
@@ -1243,20 +1245,28 @@ uint64_t tc_reserved_mask(int nl, const int* pos) {
 
 // K12 launcher (no target among positions 0..6; whole index space, no chunk bits)
 static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const int* fix, int nfix, uint64_t fixval) {
     TcTArgs p{};
     p.amps = amps;
     p.a = d_a;
-    p.ntiles = 1ull << (nl - 13);
-    uint64_t insmask = 0x7f;
+    if (nl < 13 + nfix) return cudaErrorInvalidValue;
+    p.ntiles = 1ull << (nl - 13 - nfix);
+    uint64_t insmask = 0x7f, fixmask = 0;
     for (int i = 0; i < 6; i++) {
         p.pos[i] = pos[i];
         insmask |= 1ull << pos[i];
     }
+    for (int i = 0; i < nfix; i++) {
+        if (fix[i] < 0 || fix[i] >= nl || ((insmask >> fix[i]) & 1)) return cudaErrorInvalidValue;
+        fixmask |= 1ull << fix[i];
+    }
+    if (fixval & ~fixmask) return cudaErrorInvalidValue;
+    p.fixval = fixval;
+    insmask |= fixmask;
     p.nins = 0;
     for (int b = 0; b < nl; b++)
         if ((insmask >> b) & 1) p.ins[p.nins++] = b;
-    if (p.nins != 13) return cudaErrorInvalidValue;
+    if (p.nins != 13 + nfix) return cudaErrorInvalidValue;
     const uint64_t grid = p.ntiles < (uint64_t)num_sms ? p.ntiles : (uint64_t)num_sms;
     p.fmask = ~insmask & ((1ull << nl) - 1);
     uint64_t v = grid, d = 0;
@@ -1282,8 +1292,8 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
     {   // K12 when no target sits in positions 0..6 (read per launch: tests toggle RCS_TC_NOTRANS)
         bool low = false;
         for (int i = 0; i < 6; i++) low = low || pos[i] < 7;
-        if (!low && nfix == 0 && nl >= 14 && !getenv("RCS_TC_NOTRANS"))
-            return gate_pass_tct(amps, nl, pos, d_a, num_sms, st);
+        if (!low && nl >= 13 + nfix && !getenv("RCS_TC_NOTRANS"))
+            return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval);
     }
     if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
