@@ -123,6 +123,24 @@ def test_paired_passes_bitwise_equal(rcs, ctx, case, monkeypatch):
     assert np.array_equal(xa, single.sample(100_000, seed=SHOT_SEED))
 
 
+@pytest.mark.parametrize("n", [21, 26, 29])
+def test_transposed_pass_matches_k9(rcs, ctx, n, monkeypatch):
+    """K12 (blocks without qubits 0..6) against K9 on the same plan: equal up to the tensor
+    core's summation order; n = 21 also against the oracle."""
+    text = config_qasm("c3", n_qubits=n)
+    c = rcs.Circuit.from_qasm(text)
+    a = rcs.State.build(ctx, c, fuse_k=6)
+    pa = a.copy_out(0, 1 << min(n, 24)).astype(np.complex128)
+    na = a.norm
+    del a
+    monkeypatch.setenv("RCS_TC_NOTRANS", "1")
+    b = rcs.State.build(ctx, c, fuse_k=6)
+    pb = b.copy_out(0, 1 << min(n, 24)).astype(np.complex128)
+    assert np.abs(pa - pb).max() <= 1e-8 and abs(na - b.norm) <= 1e-7
+    if n == 21:
+        check_amps(pa, oracle.build_state(text))
+
+
 @pytest.mark.parametrize("g", [1, 2, 3])
 def test_keep_layout_matches_canonical(rcs, ctx, g):
     """keep_layout skips the final restore; the logical-order CDF over the permuted layout gives
