@@ -332,7 +332,7 @@ def run_ours(args):
             "remap_note": "remap_ms_total = exposed remap time (not overlapped with pass chunks)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.config, world),
-                         "kernel": ("k_pass_tc (6-qubit tcgen05 pass)" if R["n_tc_passes"] == R["n_passes"]
+                         "kernel": ("k_pass_tc + k_pass_tct (6-qubit tcgen05 passes)" if R["n_tc_passes"] == R["n_passes"]
                                     else "gate passes (k_pass_tc + k_pass_pair/k_pass_bit0)"),
                          "per_launch_bytes": per_launch,
                          "peak_source": peak_src},
