@@ -343,7 +343,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
         }
-        print(json.dumps(out), flush=True)
+        emit(out)
         print(f"[bench] {desc}: build {out['build_s']:.3f} s, {R['n_passes']} passes, pass GB/s median "
               f"{out['pass_gbs']['median']:.0f} ({achieved / peak:.1%} of {peak:.0f}), shots/s {out['shots_per_s']:.3g}, "
               f"XEB {X['F']:.4f}+-{X['sigma']:.4f} (F* {X['fstar']:.4f})", file=sys.stderr)
@@ -378,12 +378,25 @@ def run_reference(args):
            "config": {"workload": desc, "n_qubits": n, "shots": shots}, "impl": "reference",
            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sdesc},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
     return out
 
 
+_JSON_FD = None
+
+
+def emit(out: dict) -> None:
+    """The one JSON line, on the real stdout (everything else written to fd 1 goes to stderr)."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(out) + "\n").encode())
+
+
 def main():
-    # NCCL's banner (NCCL_DEBUG=VERSION/INFO) goes to stdout by default; keep stdout = one JSON line
+    # keep stdout = one JSON line: libraries (NCCL's "NCCL version" banner at NCCL_DEBUG=VERSION,
+    # which ignores NCCL_DEBUG_FILE) write to fd 1, so fd 1 becomes stderr and the line goes to a dup
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse_args()
     if args.impl == "reference":
