@@ -154,6 +154,8 @@ def oracle_sample(cfg_name: str, cfg: dict, shots: int, budget_s: float, n_small
     shots on that state.  Projection: build time scales with 2^n * gates (per-gate sweeps),
     sampling with 2^n (one streaming CDF pass) -- both linear, as in the oracle's code."""
     import oracle
+    # all host cores, also under torchrun (which exports OMP_NUM_THREADS=1 to every rank)
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     n_small = min(n_small, cfg["n_qubits"])
     text = config_qasm(cfg_name, n_qubits=n_small)
     full_gates = len(oracle.parse(config_qasm(cfg_name)).gates)

@@ -5,7 +5,9 @@ leg may import this package.  The product package never imports it.
 See rcs_oracle.c for what each function follows in the paper.
 """
 from .oracle import (Oracle, OracleError, build_oracle, parse, gate_matrix, apply_gate,
-                     build_state, total_prob, uniforms, sample, xeb, fstar, num_threads)
+                     build_state, total_prob, uniforms, sample, xeb, fstar, num_threads,
+                     set_num_threads)
 
 __all__ = ["Oracle", "OracleError", "build_oracle", "parse", "gate_matrix", "apply_gate",
-           "build_state", "total_prob", "uniforms", "sample", "xeb", "fstar", "num_threads"]
+           "build_state", "total_prob", "uniforms", "sample", "xeb", "fstar", "num_threads",
+           "set_num_threads"]

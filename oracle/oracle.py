@@ -71,6 +71,7 @@ def _L():
         lib.orc_fstar.argtypes = [dp, C.c_int]
         lib.orc_fstar.restype = C.c_double
         lib.orc_num_threads.restype = C.c_int
+        lib.orc_set_num_threads.argtypes = [C.c_int]
         _lib = lib
     return _lib
 
@@ -199,3 +200,8 @@ def fstar(psi: np.ndarray) -> float:
 
 def num_threads() -> int:
     return _L().orc_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    """Host threads for the oracle's parallel loops (bench.py times the oracle on all host cores)."""
+    _L().orc_set_num_threads(int(n))

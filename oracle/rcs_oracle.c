@@ -644,3 +644,13 @@ int orc_num_threads(void) {
     return 1;
 #endif
 }
+
+/* host threads for the parallel loops (timing only: bench.py's oracle arm under torchrun, which
+   exports OMP_NUM_THREADS=1) */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}

@@ -22,8 +22,8 @@ def test_reference_arm_prints_one_json_line(tmp_path):
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "c2", "--steps", "1",
                         "--warmup", "0", "--cpu-budget", "1"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
-    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) == 1
+    lines = r.stdout.splitlines()
+    assert len(lines) == 1 and lines[0].startswith("{")
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
