@@ -60,6 +60,7 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=-1, help="default: --steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--canonical", action="store_true", help="restore the canonical layout after every build")
+    ap.add_argument("--no-overlap", action="store_true", help="sequential remaps (no pipelining with the passes)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     return ap.parse_args()
 
@@ -220,7 +221,8 @@ def run_ours(args):
     mat_bytes = sum(8 * (1 << it["k"]) ** 2 for it in plan.items() if it["type"] == "pass")
     amps = torch.empty(1 << (n - g), dtype=torch.complex64, device=dev)
     keep = not args.canonical   # skip the final layout restore: samples/XEB are layout-independent
-    st0 = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, amps=amps, keep_layout=keep)   # sizes scratch
+    bopts = {"overlap": not args.no_overlap}
+    st0 = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, amps=amps, keep_layout=keep, **bopts)   # sizes scratch
     scratch = st0.scratch
     st0.free()
     x_dev = torch.empty(shots, dtype=torch.int64, device=dev)
@@ -231,7 +233,7 @@ def run_ours(args):
 
     def step(timing):
         st = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, timing=timing, amps=amps, scratch=scratch,
-                             keep_layout=keep)
+                             keep_layout=keep, **bopts)
         rep = rcs_sample_report()
         err = rcs_error()
         import ctypes as C
@@ -282,7 +284,7 @@ def run_ours(args):
     w0 = time.perf_counter()
     for _ in range(e2e_steps):
         c2 = rcs.Circuit.from_qasm(text)                       # host QASM in
-        st = rcs.State.build(ctx, c2, fuse_k=args.fuse_k, amps=amps, scratch=scratch, keep_layout=keep)
+        st = rcs.State.build(ctx, c2, fuse_k=args.fuse_k, amps=amps, scratch=scratch, keep_layout=keep, **bopts)
         xh = st.sample(shots, seed=SHOT_SEED)                  # bitstrings to host
         xr_h = st.xeb(xh)                                      # XEB from the host array
         st.free()

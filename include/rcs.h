@@ -75,20 +75,41 @@ typedef struct {
     int n_sx, n_sy, n_sw, n_rz, n_fsim;   /* per-kind counts */
 } rcs_circuit_counts;
 
+/* remap execution (rcs_build_opts.remap_mode) */
+enum {
+    RCS_REMAP_AUTO = 0,      /* world > 1: in-place NVLink peer swaps over CUDA-IPC mappings when every
+                                rank maps every peer (agreed over all ranks, world <= 8), else NCCL
+                                grouped send/recv; world 1 + virtual_global: in-device bit swaps   */
+    RCS_REMAP_NCCL = 1,      /* world > 1: always NCCL send/recv through the staging area           */
+    RCS_REMAP_LOOPBACK = 2   /* world 1 + virtual_global g: the buffer is 2^g virtual ranks' shards
+                                (consecutive regions) and every remap runs through the NVLink
+                                peer-swap kernel and the pipelined remap path, peers = the other
+                                regions (exercises the multi-GPU data path on one GPU)             */
+};
+
 typedef struct {
     int fuse_k;              /* max qubits per fused dense block, 1..6; 6-qubit blocks run on the
                                 tensor cores (needs n-g >= 12).  0 -> 6 if n-g >= 12, else 4        */
     int block_bits;          /* sampling block: 2^b amplitudes per fp64 CDF entry (0 -> 6)      */
     int virtual_global;      /* world == 1 only: treat the top g qubits as global and run every
-                                remap as an in-device bit swap (tests the sharded plan on 1 GPU) */
+                                remap on this device (bit swaps, or peer swaps with LOOPBACK)    */
     int timing;              /* 1: record a CUDA-event pair around every pass / remap             */
-    uint64_t staging_bytes;  /* bound of the remap staging area (0 -> 256 MiB)                   */
+    uint64_t staging_bytes;  /* bound of the NCCL remap staging area (0 -> 256 MiB)              */
     int keep_layout;         /* 1: skip the final layout restore (remaps / bit swaps that only
                                 bring the qubits back to canonical positions).  Sampling, XEB and
                                 probabilities work on the kept layout (logical CDF over all
                                 ranks); rcs_state_copy_out / rcs_snapshot_save then need
                                 rcs_state_canonicalize first (RCS_ERR_ARG otherwise).  The
                                 scratch grows to 2 x 8 x 2^(n-6) B when world > 1.           */
+    int remap_mode;          /* RCS_REMAP_* (0 = AUTO)                                             */
+    int overlap;             /* pipelined remaps: a [TC pass] -> REMAP -> [TC pass]
+                                group runs in 2^overlap_chunks chunks, swaps of chunk c overlapping
+                                passes of other chunks.  0 = on (default), -1 = off                */
+    int overlap_chunks;      /* log2 chunks, 1..4 (0 -> 2)                                         */
+    int overlap_sms;         /* SMs left to the swaps while passes run (0 -> 32 at world 2, 16 at
+                                world >= 4 and in loopback)                                        */
+    int tc_kernel;           /* 0: K12 for blocks with no target among positions 0..6, K9 otherwise
+                                (a function of the block: P-invariant); 1: K9 only (tests)         */
 } rcs_build_opts;
 
 typedef struct {
@@ -104,18 +125,17 @@ typedef struct {
                                 for pipelined remaps the time not hidden behind pass chunks    */
     double blocksum_ms;      /* timing=1: block-sum + scan (sampling CDF) time                   */
     uint64_t pass_bytes;     /* algorithmic bytes of all gate passes on this rank (16 B/amp/pass) */
-    uint64_t remap_bytes;    /* bytes this rank sent over NCCL                                   */
+    uint64_t remap_bytes;    /* bytes this rank's remaps moved out of its shard (NVLink / NCCL)   */
     double norm;             /* sum |psi|^2 over all ranks                                       */
     int n_tc_passes;         /* of n_passes, 6-qubit passes run on the tensor cores (K9)          */
     double swap_ms;          /* timing=1: sum of local bit-swap (layout restore) pass times       */
     int layout_kept;         /* 1: the state is in a permuted (non-canonical) layout            */
-    int n_pipelined;         /* remaps run as chunked NVLink swaps overlapped with the adjacent
-                                tensor-core passes; env RCS_OVERLAP=0 disables,
-                                RCS_OVERLAP_CHUNKS = log2 chunks (default 2), RCS_OVERLAP_SMS =
-                                SMs left to the swaps (default 32 at N=2, 16 at N>=4); RCS_REMAP_PULL=1 (world >= 4):
-                                staged pulls instead of in-place swaps (measured slower at N=4) */
-    int n_paired;            /* launches that ran two consecutive tensor-core passes (K11, one HBM
-                                round trip for both; experimental, env RCS_TC_PAIR=1 enables)  */
+    int n_pipelined;         /* remaps run as chunked peer swaps overlapped with the adjacent
+                                tensor-core passes (rcs_build_opts.overlap)         */
+    int n_peer_remaps;       /* remaps executed by the peer-swap kernel (NVLink or loopback)      */
+    double remap_kernel_ms;  /* timing=1: device time of the remap data movement alone (peer-swap
+                                kernels / NCCL send-recv, first start to last end per remap, also
+                                when hidden behind pass chunks): NVLink GB/s = remap_bytes / it  */
 } rcs_build_report;
 
 typedef struct {

@@ -18,8 +18,8 @@ import ctypes as C
 
 import numpy as np
 
-from ._lib import (RcsError, check, lib, rcs_build_opts, rcs_build_report, rcs_circuit_counts, rcs_error,
-                   rcs_plan_item, rcs_sample_report, rcs_xeb_report)
+from ._lib import (REMAP_MODES, RcsError, check, lib, rcs_build_opts, rcs_build_report, rcs_circuit_counts,
+                   rcs_error, rcs_plan_item, rcs_sample_report, rcs_xeb_report)
 
 __all__ = ["Circuit", "Plan", "Context", "State", "RcsError", "lib", "sha256", "snapshot_info", "shard_shots",
            "job_seed", "xeb_from_probs"]
@@ -33,6 +33,32 @@ def _ptr(t):
     if hasattr(t, "data_ptr"):
         return C.c_void_p(t.data_ptr())
     return C.c_void_p(t.ctypes.data)
+
+
+def _device_u64(ctx, x, what):
+    """A caller CUDA tensor of bitstrings as the library reads it: contiguous 64-bit integers on
+    the context's device (int64 / uint64 bit patterns); anything else is rejected."""
+    import torch
+    if x.dtype not in (torch.int64, torch.uint64):
+        raise TypeError(f"{what}: bitstrings must be int64/uint64, got {x.dtype}")
+    if x.device != torch.device("cuda", ctx.device):
+        raise ValueError(f"{what}: tensor on {x.device}, context on cuda:{ctx.device}")
+    return x.contiguous()
+
+
+def _order_after_torch(ctx):
+    """The library runs on ctx.stream: order it after the work torch queued on the current
+    stream (allocations, producers of caller tensors)."""
+    import torch
+    ctx.stream.wait_stream(torch.cuda.current_stream(torch.device("cuda", ctx.device)))
+
+
+def _order_torch_after(ctx):
+    """Results the library wrote into torch tensors: later torch work on the current stream
+    must follow the library's stream (the calls return after it drained; this also records
+    the dependency for the caching allocator's stream bookkeeping)."""
+    import torch
+    torch.cuda.current_stream(torch.device("cuda", ctx.device)).wait_stream(ctx.stream)
 
 
 class Circuit:
@@ -188,12 +214,16 @@ class State:
     @classmethod
     def build(cls, ctx: Context, circuit: Circuit, fuse_k: int = 0, block_bits: int = 0, virtual_global: int = 0,
               timing: bool = False, staging_bytes: int = 0, amps=None, scratch=None,
-              keep_layout: bool = False) -> "State":
+              keep_layout: bool = False, remap_mode: str = "auto", overlap: bool = True, overlap_chunks: int = 0,
+              overlap_sms: int = 0, tc_kernel: str = "auto") -> "State":
+        """rcs_state_build.  remap_mode: "auto" | "nccl" | "loopback" (world 1 + virtual_global: remaps
+        through the NVLink peer-swap kernel between regions of this GPU); tc_kernel: "auto" | "k9"."""
         import torch
         n = circuit.n_qubits
         g = ctx.world.bit_length() - 1
         opts = rcs_build_opts(fuse_k, block_bits, virtual_global, 1 if timing else 0, staging_bytes,
-                              1 if keep_layout else 0)
+                              1 if keep_layout else 0, REMAP_MODES[remap_mode], 0 if overlap else -1,
+                              overlap_chunks, overlap_sms, {"auto": 0, "k9": 1}[tc_kernel])
         sb = C.c_uint64()
         check(lib().rcs_state_scratch_bytes(ctx._h, circuit._h, C.byref(opts), C.byref(sb)), None,
               "rcs_state_scratch_bytes")
@@ -208,8 +238,7 @@ class State:
         h = C.c_void_p()
         rep = rcs_build_report()
         err = rcs_error()
-        # the library runs on ctx.stream; order it after torch's allocations/initialisation
-        ctx.stream.wait_stream(torch.cuda.current_stream(dev))
+        _order_after_torch(ctx)   # torch's allocations / initialisation of amps and scratch
         check(lib().rcs_state_build(ctx._h, circuit._h, C.byref(opts), _ptr(amps), amps.numel() * 8, _ptr(scratch),
                                     scratch.numel(), C.byref(h), C.byref(rep), C.byref(err)), err, "rcs_state_build")
         self._h = h
@@ -259,10 +288,17 @@ class State:
         return out
 
     def probabilities(self, x) -> np.ndarray:
-        xa = np.ascontiguousarray(np.asarray(x, dtype=np.uint64)) if not hasattr(x, "data_ptr") else x
-        p = np.empty(len(xa), dtype=np.float64)
+        """|psi_x|^2 (host float64) of host bitstrings or a CUDA int64/uint64 tensor."""
+        if hasattr(x, "data_ptr"):
+            xa = _device_u64(self.ctx, x, "probabilities")
+            _order_after_torch(self.ctx)   # the producer of x may still be queued on torch's stream
+            n = xa.numel()
+        else:
+            xa = np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
+            n = xa.size
+        p = np.empty(n, dtype=np.float64)
         err = rcs_error()
-        check(lib().rcs_probabilities(self._h, _ptr(xa), len(xa), _ptr(p), C.byref(err)), err, "rcs_probabilities")
+        check(lib().rcs_probabilities(self._h, _ptr(xa), n, _ptr(p), C.byref(err)), err, "rcs_probabilities")
         return p
 
     def sample(self, shots: int, seed: int = 2512, offset: int = 0, device: bool = False):
@@ -270,11 +306,14 @@ class State:
         import torch
         if device:
             out = torch.empty(shots, dtype=torch.int64, device=torch.device("cuda", self.ctx.device))
+            _order_after_torch(self.ctx)   # the allocation may reuse memory torch's stream still uses
         else:
             out = np.empty(shots, dtype=np.uint64)
         rep = rcs_sample_report()
         err = rcs_error()
         check(lib().rcs_sample(self._h, shots, seed, offset, _ptr(out), C.byref(rep), C.byref(err)), err, "rcs_sample")
+        if device:
+            _order_torch_after(self.ctx)
         self.last_sample = {f: getattr(rep, f) for f, _ in rep._fields_}
         return out
 
@@ -313,7 +352,7 @@ class State:
         self.amps, self.scratch = amps, scratch
         h = C.c_void_p()
         err = rcs_error()
-        ctx.stream.wait_stream(torch.cuda.current_stream(dev))
+        _order_after_torch(ctx)
         check(lib().rcs_snapshot_load(ctx._h, path.encode(), block_bits, _ptr(amps), amps.numel() * 8,
                                       _ptr(scratch), scratch.numel(), C.byref(h), C.byref(err)), err,
               "rcs_snapshot_load")
@@ -322,10 +361,13 @@ class State:
         return self
 
     def xeb(self, x) -> dict:
+        """Linear XEB of host bitstrings or a CUDA int64/uint64 tensor against this state."""
         if not hasattr(x, "data_ptr"):
             x = np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
             n = x.size
         else:
+            x = _device_u64(self.ctx, x, "xeb")
+            _order_after_torch(self.ctx)
             n = x.numel()
         rep = rcs_xeb_report()
         err = rcs_error()

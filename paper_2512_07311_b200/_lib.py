@@ -23,9 +23,15 @@ class rcs_circuit_counts(C.Structure):
                                        "n_sx", "n_sy", "n_sw", "n_rz", "n_fsim")]
 
 
+# rcs_build_opts.remap_mode
+REMAP_MODES = {"auto": 0, "nccl": 1, "loopback": 2}
+
+
 class rcs_build_opts(C.Structure):
     _fields_ = [("fuse_k", C.c_int), ("block_bits", C.c_int), ("virtual_global", C.c_int),
-                ("timing", C.c_int), ("staging_bytes", C.c_uint64), ("keep_layout", C.c_int)]
+                ("timing", C.c_int), ("staging_bytes", C.c_uint64), ("keep_layout", C.c_int),
+                ("remap_mode", C.c_int), ("overlap", C.c_int), ("overlap_chunks", C.c_int),
+                ("overlap_sms", C.c_int), ("tc_kernel", C.c_int)]
 
 
 class rcs_build_report(C.Structure):
@@ -34,7 +40,8 @@ class rcs_build_report(C.Structure):
                 ("pass_ms_min", C.c_double), ("pass_ms_max", C.c_double), ("remap_ms", C.c_double),
                 ("blocksum_ms", C.c_double), ("pass_bytes", C.c_uint64), ("remap_bytes", C.c_uint64),
                 ("norm", C.c_double), ("n_tc_passes", C.c_int), ("swap_ms", C.c_double),
-                ("layout_kept", C.c_int), ("n_pipelined", C.c_int), ("n_paired", C.c_int)]
+                ("layout_kept", C.c_int), ("n_pipelined", C.c_int), ("n_peer_remaps", C.c_int),
+                ("remap_kernel_ms", C.c_double)]
 
 
 class rcs_sample_report(C.Structure):

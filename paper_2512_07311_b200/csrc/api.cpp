@@ -23,6 +23,8 @@
 
 using namespace rcs;
 
+constexpr int kMaxPeerWorld = 8;   // NVLink peer-swap remaps up to 8 ranks (one NVSwitch box); NCCL beyond
+
 struct rcs_context {
     int device = 0, rank = 0, world = 1, g = 0;
     int num_sms = 148;
@@ -35,19 +37,15 @@ struct rcs_context {
     const rcs::TcPack* tc_pack = nullptr;
     std::shared_ptr<const rcs::TcPack> tc_hold;   // keeps that pack alive
     // remaps over NVLink: CUDA-IPC mappings of the peers' shards (re-checked every build)
-    bool p2p = false;                 // every peer mappable
-    bool p2p_stage = false;           // and every peer's pull staging area too
+    bool p2p = false;                 // every rank mapped every peer (agreed over all ranks)
     char* d_xchg = nullptr;           // device buffer for the handle all-gather
-    cudaIpcMemHandle_t peer_handle[2][8];   // [0] amplitude shards, [1] pull staging
-    uint64_t peer_off[2][8] = {};
-    void* peer_map[2][8] = {};
+    cudaIpcMemHandle_t peer_handle[kMaxPeerWorld];
+    uint64_t peer_off[kMaxPeerWorld] = {};
+    void* peer_map[kMaxPeerWorld] = {};
     float* d_bar = nullptr;           // 1-float all-reduce used as a stream-ordered barrier
     // pipelined remaps (f1): a second stream for the chunked peer swaps + per-chunk events
     cudaStream_t xstream = nullptr;
-    // paired tensor-core passes (K11): per-chunk completion counters
-    unsigned* d_done = nullptr;
-    uint64_t done_cap = 0;
-    cudaEvent_t ev_a[16] = {}, ev_s[16] = {}, ev_p[16] = {}, ev_b[16] = {};
+    cudaEvent_t ev_a[16] = {}, ev_s[16] = {};
     // sampling / XEB chunk buffers, shared by every state of this context
     unsigned long long* xbuf = nullptr;
     double* dbuf = nullptr;
@@ -86,15 +84,14 @@ struct rcs_state {
     uint64_t* ptab = nullptr;        // logical -> physical block byte tables (device)
     uint64_t nblocks_all = 0;
     uint64_t last_block = 0;
-    float2* pull_stage = nullptr;    // 2 x pull_stage_elems (world >= 4)
-    uint64_t pull_stage_elems = 0;
+    // execution options of the build (rcs_build_opts), reused by rcs_state_canonicalize
+    int remap_mode = RCS_REMAP_AUTO;
+    int virt = 0;                    // virtual global qubits (world 1)
 };
 
 namespace {
 
 constexpr uint64_t kChunkShots = 1ull << 22;
-constexpr int kPullCb = 3;   // pull-mode remaps: 8 chunks
-constexpr int kPairMaxChunkBits = 18;   // paired passes: chunk <= 2^18 amplitudes (2 MB)
 constexpr uint64_t kAlign = 256;
 
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -139,7 +136,6 @@ struct Layout {
     bool kept = false;
     uint64_t nblocks_all = 0, gbuf_off = 0, ptab_off = 0;
     uint64_t stage_end = 0;
-    uint64_t pull_off = 0, pull_elems = 0;   // world >= 4: 2 x pull_elems complex64
 };
 
 // keep: a kept (permuted) final layout is possible (keep_layout and world > 1 or virtual global)
@@ -161,13 +157,6 @@ Layout scratch_layout(int nl, int world, int virt, uint64_t staging_bytes, int b
     if (world > 1) st = staging_bytes ? staging_bytes : (256ull << 20);
     uint64_t end = align_up(L.stage_off + st);
     L.stage_end = end;
-    // pull-mode remaps (RCS_REMAP_PULL=1, world >= 4): outgoing elements of one 2^-kPullCb chunk, twice
-    static const bool pull_on = getenv("RCS_REMAP_PULL") && atoi(getenv("RCS_REMAP_PULL")) != 0;
-    if (world >= 4 && pull_on) {
-        L.pull_elems = (1ull << (nl - kPullCb)) / (uint64_t)world * (uint64_t)(world - 1);
-        L.pull_off = end;
-        end = align_up(L.pull_off + 2 * L.pull_elems * 8);
-    }
     if (L.kept) {
         L.gbuf_off = end;
         L.ptab_off = align_up(L.gbuf_off + L.nblocks_all * 8);
@@ -177,8 +166,25 @@ Layout scratch_layout(int nl, int world, int virt, uint64_t staging_bytes, int b
     return L;
 }
 
+struct Span {   // timing: item time += sign * elapsed(a, b); item kRemapKernelSpan: remap data movement
+    size_t item;
+    cudaEvent_t a, b;
+    int sign;
+};
+constexpr size_t kRemapKernelSpan = SIZE_MAX;
+
+// timing event recorded on st (owned by the build); nullptr when not timing
+cudaEvent_t timing_event(std::vector<cudaEvent_t>* owned, cudaStream_t st) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    owned->push_back(e);
+    cudaEventRecord(e, st);
+    return e;
+}
+
 // Exchange for one REMAP item over NCCL: swap global positions a[i] with local b[i].
-rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_error* err) {
+rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, std::vector<Span>* spans,
+                         std::vector<cudaEvent_t>* owned, rcs_error* err) {
     rcs_context* c = s->ctx;
     const int j = it.k, nl = s->nl;
     int lpos[8];
@@ -209,6 +215,7 @@ rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs
         set_error(err, RCS_ERR_MEMORY, "remap staging too small");
         return RCS_ERR_MEMORY;
     }
+    cudaEvent_t k0 = spans ? timing_event(owned, c->stream) : nullptr;
     for (uint64_t m0 = 0; m0 < count; m0 += E) {
         const uint64_t e = std::min(E, count - m0);
         for (int p = 0; p < np; p++)
@@ -223,6 +230,7 @@ rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs
             CUDA_TRY(dev::unpack(s->amps, s->staging + (uint64_t)(np + p) * E, j, lpos, masks[p], m0, e, c->stream));
         *bytes_sent += e * 8ull * np;
     }
+    if (spans) spans->push_back({kRemapKernelSpan, k0, timing_event(owned, c->stream), 1});
     return RCS_OK;
 }
 
@@ -267,103 +275,76 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
 // --- NVLink peer mapping -----------------------------------------------------------------
 typedef int (*PFN_getAddressRange)(unsigned long long*, size_t*, unsigned long long);
 
-// Maps every peer's amplitude shard (buffer 0) and, if given, its pull staging area (buffer 1).
-rcs_status setup_peers(rcs_context* c, void* amps, rcs_error* err, void* stage = nullptr) {
-    c->p2p = false;
-    c->p2p_stage = false;
-    if (getenv("RCS_REMAP_NCCL")) return RCS_OK;   // force the NCCL send/recv path
-    for (int r = 0; r < c->world; r++) {
-        if (r == c->rank) continue;
-        int can = 0;
-        if (cudaDeviceCanAccessPeer(&can, c->device, r) != cudaSuccess || !can) {
-            cudaGetLastError();
-            return RCS_OK;   // ranks are not one-GPU-per-device-index on this box: NCCL path
-        }
-    }
-    static PFN_getAddressRange get_range = nullptr;
-    if (!get_range) {
-        void* fn = nullptr;
+PFN_getAddressRange address_range_fn() {
+    static const PFN_getAddressRange fn = [] {   // resolved once (thread-safe static init)
+        void* f = nullptr;
         cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-            return RCS_OK;
-        get_range = (PFN_getAddressRange)fn;
-    }
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess) {
+            cudaGetLastError();
+            return (PFN_getAddressRange) nullptr;
+        }
+        return (PFN_getAddressRange)f;
+    }();
+    return fn;
+}
+
+// Maps every peer's amplitude shard over CUDA IPC (no assumption about device ordinals: the
+// handles are all-gathered and opened; cudaIpcMemLazyEnablePeerAccess enables NVLink access).
+// Every rank takes part in every collective whatever its local outcome, and the decision is
+// agreed (all-reduce MIN of the per-rank success flags), so all ranks take the same remap path.
+rcs_status setup_peers(rcs_context* c, void* amps, int remap_mode, rcs_error* err) {
+    c->p2p = false;
+    // identical on every rank (same opts, same world): no collective needed to agree
+    if (remap_mode == RCS_REMAP_NCCL || c->world > kMaxPeerWorld) return RCS_OK;
     struct Rec {
-        cudaIpcMemHandle_t h[2];
-        uint64_t off[2];
-        int ok[2];
-        int same;   // buffer 1 lies in buffer 0's allocation
+        cudaIpcMemHandle_t h;
+        uint64_t off;
+        int ok;
     } mine{};
-    unsigned long long base[2] = {0, 0};
-    void* bufs[2] = {amps, stage};
-    for (int i = 0; i < 2; i++) {
-        if (!bufs[i]) continue;
+    {
+        unsigned long long base = 0;
         size_t size = 0;
-        if (get_range(&base[i], &size, (unsigned long long)bufs[i]) != 0) {
-            if (i == 0) return RCS_OK;
-            continue;
+        PFN_getAddressRange get_range = address_range_fn();
+        if (get_range && get_range(&base, &size, (unsigned long long)amps) == 0) {
+            mine.off = (uint64_t)amps - base;
+            mine.ok = cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess;
+            if (!mine.ok) cudaGetLastError();
         }
-        mine.off[i] = (uint64_t)bufs[i] - base[i];
-        if (i == 1 && base[1] == base[0]) {
-            mine.same = 1;
-            mine.ok[1] = 1;
-            continue;
-        }
-        mine.ok[i] = cudaIpcGetMemHandle(&mine.h[i], (void*)base[i]) == cudaSuccess;
-        if (!mine.ok[i]) cudaGetLastError();
     }
     const size_t rec = (sizeof(Rec) + 15) / 16 * 16;
-    if (!c->d_xchg) CUDA_TRY(cudaMalloc(&c->d_xchg, rec * (8 + 1)));
+    if (!c->d_xchg) CUDA_TRY(cudaMalloc(&c->d_xchg, rec * (kMaxPeerWorld + 1)));
     if (!c->d_bar) CUDA_TRY(cudaMalloc(&c->d_bar, 16));
     CUDA_TRY(cudaMemcpyAsync(c->d_xchg, &mine, sizeof mine, cudaMemcpyHostToDevice, c->stream));
     NCCL_TRY(ncclAllGather(c->d_xchg, c->d_xchg + rec, rec, ncclChar, c->comm, c->stream));
     std::vector<char> all(rec * c->world);
     CUDA_TRY(cudaMemcpyAsync(all.data(), c->d_xchg + rec, rec * c->world, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    bool ok0 = true, ok1 = stage != nullptr;
-    for (int r = 0; r < c->world; r++) {
-        const Rec* pr = reinterpret_cast<const Rec*>(all.data() + rec * r);
-        ok0 = ok0 && pr->ok[0];
-        ok1 = ok1 && pr->ok[1];
-    }
-    if (!ok0) return RCS_OK;
-    auto open = [&](int r, int i, const cudaIpcMemHandle_t& h, void** out) -> bool {
-        // cached by handle; the same allocation may back both buffers
-        for (int j = 0; j < 2; j++)
-            if (c->peer_map[j][r] && std::memcmp(&c->peer_handle[j][r], &h, sizeof h) == 0) {
-                *out = c->peer_map[j][r];
-                return true;
-            }
-        void* mp = nullptr;
-        if (cudaIpcOpenMemHandle(&mp, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        *out = mp;
-        return true;
-    };
-    for (int r = 0; r < c->world; r++) {
+    bool ok = true;
+    for (int r = 0; r < c->world; r++) ok = ok && reinterpret_cast<const Rec*>(all.data() + rec * r)->ok;
+    for (int r = 0; r < c->world && ok; r++) {
         if (r == c->rank) continue;
         const Rec* pr = reinterpret_cast<const Rec*>(all.data() + rec * r);
-        void* m0 = nullptr;
-        void* m1 = nullptr;
-        if (!open(r, 0, pr->h[0], &m0)) return RCS_OK;
-        if (ok1 && !pr->same && !open(r, 1, pr->h[1], &m1)) ok1 = false;
-        if (ok1 && pr->same) m1 = m0;
-        // close mappings no longer referenced
-        for (int j = 0; j < 2; j++) {
-            void* old = c->peer_map[j][r];
-            if (old && old != m0 && old != m1 && old != c->peer_map[1 - j][r]) cudaIpcCloseMemHandle(old);
+        if (c->peer_map[r] && std::memcmp(&c->peer_handle[r], &pr->h, sizeof pr->h) == 0) {   // cached mapping
+            c->peer_off[r] = pr->off;
+            continue;
         }
-        c->peer_map[0][r] = m0;
-        c->peer_handle[0][r] = pr->h[0];
-        c->peer_off[0][r] = pr->off[0];
-        c->peer_map[1][r] = ok1 ? m1 : nullptr;
-        c->peer_handle[1][r] = pr->same ? pr->h[0] : pr->h[1];
-        c->peer_off[1][r] = pr->off[1];
+        void* mp = nullptr;
+        if (cudaIpcOpenMemHandle(&mp, pr->h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            break;
+        }
+        if (c->peer_map[r]) cudaIpcCloseMemHandle(c->peer_map[r]);   // the peer's buffer changed
+        c->peer_map[r] = mp;
+        c->peer_handle[r] = pr->h;
+        c->peer_off[r] = pr->off;
     }
-    c->p2p = true;
-    c->p2p_stage = ok1;
+    float flag[2] = {ok ? 1.f : 0.f, 0.f};
+    CUDA_TRY(cudaMemcpyAsync(c->d_bar + 2, flag, sizeof flag, cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(ncclAllReduce(c->d_bar + 2, c->d_bar + 3, 1, ncclFloat, ncclMin, c->comm, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(flag, c->d_bar + 2, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->p2p = flag[1] > 0.5f;
     return RCS_OK;
 }
 
@@ -452,18 +433,50 @@ rcs_status plan_distributed(rcs_context* c, const Circuit& circ, int fuse_k, int
 
 // stream-ordered barrier over all ranks (no rank proceeds past it before every rank reached it)
 rcs_status stream_barrier(rcs_context* c, cudaStream_t st, rcs_error* err) {
-    NCCL_TRY(ncclAllReduce(c->d_bar, c->d_bar, 1, ncclFloat, ncclSum, c->comm, st));
+    NCCL_TRY(ncclAllReduce(c->d_bar, c->d_bar, 1, ncclFloat, ncclMax, c->comm, st));
     return RCS_OK;
+}
+
+// One (possibly virtual) rank's view of a remap: its rank index, the local bits of a shard and
+// every rank's shard.  Real ranks (world > 1): one view, peers through the CUDA-IPC mappings.
+// Loopback (world 1, virtual_global g, RCS_REMAP_LOOPBACK): 2^g views whose shards are the
+// 2^g consecutive regions of the one buffer, so the remap runs through the same peer-swap
+// kernel and pipeline as between GPUs.
+struct SwapView {
+    int rank;
+    int nl;
+    float2* shard[kMaxPeerWorld];
+};
+
+bool loopback(const rcs_state* s) { return s->ctx->world == 1 && s->remap_mode == RCS_REMAP_LOOPBACK && s->virt > 0; }
+
+std::vector<SwapView> swap_views(const rcs_state* s) {
+    const rcs_context* c = s->ctx;
+    std::vector<SwapView> v;
+    if (loopback(s)) {
+        const int nv = 1 << s->virt, nlv = s->n - s->virt;
+        for (int r = 0; r < nv; r++) {
+            SwapView w{r, nlv, {}};
+            for (int q = 0; q < nv; q++) w.shard[q] = s->amps + ((uint64_t)q << nlv);
+            v.push_back(w);
+        }
+        return v;
+    }
+    SwapView w{c->rank, s->nl, {}};
+    for (int q = 0; q < c->world && q < kMaxPeerWorld; q++)
+        w.shard[q] = q == c->rank ? s->amps
+                                  : reinterpret_cast<float2*>(static_cast<char*>(c->peer_map[q]) + c->peer_off[q]);
+    v.push_back(w);
+    return v;
 }
 
 // Peer-swap arguments for one REMAP item: every unordered rank pair splits its element pairs
 // in two halves, one per rank.  fix/nfix/fixval restrict it to one chunk of the index space.
-void make_swap_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint64_t fixval, dev::PeerSwapArgs& A,
-                    uint64_t* bytes_sent) {
-    rcs_context* c = s->ctx;
-    const int j = it.k, nl = s->nl;
+void make_swap_args(const SwapView& v, const Item& it, const int* fix, int nfix, uint64_t fixval,
+                    dev::PeerSwapArgs& A, uint64_t* bytes_sent) {
+    const int j = it.k, nl = v.nl;
     A = dev::PeerSwapArgs{};
-    A.local = s->amps;
+    A.local = v.shard[v.rank];
     A.j = j;
     int lpos[8];
     for (int i = 0; i < j; i++) lpos[i] = it.b[i];
@@ -473,15 +486,13 @@ void make_swap_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint
     for (int i = 0; i < nfix; i++) A.fix[i] = fix[i];
     A.fixval = fixval;
     int my_code = 0;
-    for (int i = 0; i < j; i++) my_code |= ((c->rank >> (it.a[i] - nl)) & 1) << i;
+    for (int i = 0; i < j; i++) my_code |= ((v.rank >> (it.a[i] - nl)) & 1) << i;
     for (int i = 0; i < j; i++)
         if ((my_code >> i) & 1) A.my_mask |= 1ull << it.b[i];
     const uint64_t count = 1ull << (nl - j - nfix);
-    static const int rounds = getenv("RCS_SWAP_ROUNDS") ? atoi(getenv("RCS_SWAP_ROUNDS")) : 0;   // measured: no gain
-    A.rounds = rounds;
-    for (int x = 1; x < (1 << j); x++) {   // peers in XOR-pattern order: round x pairs code with code^x
+    for (int x = 1; x < (1 << j); x++) {   // peers in XOR-pattern order
         const int code = my_code ^ x;
-        int peer = c->rank;
+        int peer = v.rank;
         uint64_t mask = 0;
         for (int i = 0; i < j; i++) {
             const int gb = it.a[i] - nl;
@@ -489,64 +500,33 @@ void make_swap_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint
             if ((code >> i) & 1) mask |= 1ull << it.b[i];
         }
         const int pc = A.npeers++;
-        A.peer[pc] = reinterpret_cast<float2*>(static_cast<char*>(c->peer_map[0][peer]) + c->peer_off[0][peer]);
+        A.peer[pc] = v.shard[peer];
         A.mask[pc] = mask;
         const uint64_t half = count / 2;
-        A.m_begin[pc] = c->rank < peer ? 0 : half;
-        A.m_count[pc] = c->rank < peer ? half : count - half;
+        A.m_begin[pc] = v.rank < peer ? 0 : half;
+        A.m_count[pc] = v.rank < peer ? half : count - half;
         *bytes_sent += count * 8ull;
     }
 }
 
-// Pull-mode arguments for one chunk: peers in ascending code order (the same order every rank
-// uses for its staging groups, so my group on peer p is at index my_code - (my_code > code_p)).
-void make_pull_args(rcs_state* s, const Item& it, const int* fix, int nfix, uint64_t fixval, int buf,
-                    dev::PullArgs& A, uint64_t* bytes_sent) {
+// Remap over NVLink (or loopback): swap the exchanged halves in place, local <-> peer.  The
+// views' element sets are disjoint, so loopback launches need no barrier between them.
+rcs_status do_remap_p2p(rcs_state* s, const Item& it, uint64_t* bytes_sent, std::vector<Span>* spans,
+                        std::vector<cudaEvent_t>* owned, rcs_error* err) {
     rcs_context* c = s->ctx;
-    const int j = it.k, nl = s->nl;
-    A = dev::PullArgs{};
-    A.local = s->amps;
-    A.j = j;
-    int lpos[8];
-    for (int i = 0; i < j; i++) lpos[i] = it.b[i];
-    std::sort(lpos, lpos + j);
-    for (int i = 0; i < j; i++) A.lpos[i] = lpos[i];
-    A.nfix = nfix;
-    for (int i = 0; i < nfix; i++) A.fix[i] = fix[i];
-    A.fixval = fixval;
-    A.count = 1ull << (nl - j - nfix);
-    const uint64_t group_elems = A.count;   // per peer
-    A.stage = s->pull_stage + (size_t)buf * s->pull_stage_elems;
-    int my_code = 0;
-    for (int i = 0; i < j; i++) my_code |= ((c->rank >> (it.a[i] - nl)) & 1) << i;
-    for (int code = 0; code < (1 << j); code++) {
-        if (code == my_code) continue;
-        int peer = c->rank;
-        uint64_t mask = 0;
-        for (int i = 0; i < j; i++) {
-            const int gb = it.a[i] - nl;
-            peer = (peer & ~(1 << gb)) | (((code >> i) & 1) << gb);
-            if ((code >> i) & 1) mask |= 1ull << it.b[i];
-        }
-        const int pc = A.npeers++;
-        A.mask[pc] = mask;
-        const int slot = my_code - (my_code > code ? 1 : 0);
-        const float2* base = reinterpret_cast<const float2*>(static_cast<char*>(c->peer_map[1][peer]) +
-                                                             c->peer_off[1][peer]);
-        A.peer_stage[pc] = base + (size_t)buf * s->pull_stage_elems + (size_t)slot * group_elems;
-        *bytes_sent += A.count * 8ull;
+    const bool real = !loopback(s);
+    if (real) {
+        rcs_status st = stream_barrier(c, c->stream, err);
+        if (st) return st;
     }
-}
-
-// Remap over NVLink: swap the exchanged halves in place, local <-> peer (CUDA-IPC mapping).
-rcs_status do_remap_p2p(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_error* err) {
-    rcs_context* c = s->ctx;
-    dev::PeerSwapArgs A;
-    make_swap_args(s, it, nullptr, 0, 0, A, bytes_sent);
-    rcs_status st = stream_barrier(c, c->stream, err);
-    if (st) return st;
-    CUDA_TRY(dev::peer_swap(A, c->stream));
-    return stream_barrier(c, c->stream, err);
+    cudaEvent_t k0 = spans ? timing_event(owned, c->stream) : nullptr;
+    for (const SwapView& v : swap_views(s)) {
+        dev::PeerSwapArgs A;
+        make_swap_args(v, it, nullptr, 0, 0, A, bytes_sent);
+        CUDA_TRY(dev::peer_swap(A, c->stream));
+    }
+    if (spans) spans->push_back({kRemapKernelSpan, k0, timing_event(owned, c->stream), 1});
+    return real ? stream_barrier(c, c->stream, err) : RCS_OK;
 }
 
 // Pipelined remap: [pass A] -> REMAP -> [pass B] in 2^cb chunks of the index
@@ -554,34 +534,26 @@ rcs_status do_remap_p2p(rcs_state* s, const Item& it, uint64_t* bytes_sent, rcs_
 // context stream on (num_sms - reserve) SMs; the peer swap of chunk c runs on xstream as soon
 // as every rank finished A on chunk c (barrier), and B on chunk c starts once every rank
 // finished swapping it (barrier).  Arithmetic per amplitude is unchanged (bitwise equal).
+// Loopback: the pass launches cover every virtual rank's chunk c at once, so stream order
+// alone provides both barriers.
 struct PassRef {
     const int* pos;
     const uint32_t* d_a;
 };
-struct Span {   // timing: item time += sign * elapsed(a, b)
-    size_t item;
-    cudaEvent_t a, b;
-    int sign;
-};
 
 rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, const PassRef* pb, const int* fix,
-                              int cb, int reserve, bool pull, uint64_t* bytes_sent, uint64_t* pass_bytes, size_t ia,
-                              size_t ir, size_t ib, std::vector<Span>* spans, std::vector<cudaEvent_t>* owned,
-                              rcs_error* err) {
+                              int cb, int reserve, bool force_k9, uint64_t* bytes_sent, uint64_t* pass_bytes,
+                              size_t ia, size_t ir, size_t ib, std::vector<Span>* spans,
+                              std::vector<cudaEvent_t>* owned, rcs_error* err) {
     rcs_context* c = s->ctx;
     const int nch = 1 << cb;
+    const bool real = !loopback(s);
     if (!c->xstream) CUDA_TRY(cudaStreamCreateWithFlags(&c->xstream, cudaStreamNonBlocking));
     for (int i = 0; i < nch; i++) {
         if (!c->ev_a[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_a[i], cudaEventDisableTiming));
         if (!c->ev_s[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_s[i], cudaEventDisableTiming));
     }
-    auto tev = [&](cudaStream_t st) -> cudaEvent_t {   // timing event (only when spans requested)
-        cudaEvent_t e;
-        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
-        owned->push_back(e);
-        cudaEventRecord(e, st);
-        return e;
-    };
+    auto tev = [&](cudaStream_t st) { return timing_event(owned, st); };
     auto fixval = [&](int ch) {
         uint64_t v = 0;
         for (int i = 0; i < cb; i++)
@@ -589,65 +561,44 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
         return v;
     };
     const int sms = std::max(1, c->num_sms - reserve);
+    const std::vector<SwapView> views = swap_views(s);
     cudaEvent_t t0 = spans ? tev(c->stream) : nullptr;
-    if (pull) {
-        for (int ch = 0; ch < nch; ch++) {
-            if (!c->ev_p[ch]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_p[ch], cudaEventDisableTiming));
-            if (!c->ev_b[ch]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_b[ch], cudaEventDisableTiming));
-        }
-    }
-    // A: all chunks, in order, on the main stream.  Pull mode: pack(c) follows A(c) on the main
-    // stream (all SMs), pull(c) runs on xstream after a barrier.  The staging is double-buffered:
-    // pack(c) waits for barrier(c-1), which every peer passes only after its pull(c-2) from the
-    // same buffer.
+    // A: all chunks, in order, on the main stream
     for (int ch = 0; ch < nch; ch++) {
-        if (pa) {
-            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch)));
-        }
+        if (pa)
+            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch), force_k9));
         CUDA_TRY(cudaEventRecord(c->ev_a[ch], c->stream));
-        if (pull) {
-            dev::PullArgs A;
-            make_pull_args(s, it, fix, cb, fixval(ch), ch & 1, A, bytes_sent);
-            if (ch >= 2) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_b[ch - 1], 0));
-            CUDA_TRY(dev::remap_pack(A, c->stream));
-            CUDA_TRY(cudaEventRecord(c->ev_p[ch], c->stream));
-            CUDA_TRY(cudaStreamWaitEvent(c->xstream, c->ev_p[ch], 0));
-            rcs_status st = stream_barrier(c, c->xstream, err);
-            if (st) return st;
-            CUDA_TRY(cudaEventRecord(c->ev_b[ch], c->xstream));
-            A.max_grid = reserve * 8;
-            CUDA_TRY(dev::remap_pull(A, c->xstream));
-            CUDA_TRY(cudaEventRecord(c->ev_s[ch], c->xstream));
-        }
     }
     if (pa) *pass_bytes += 16ull * s->n_amps;
     cudaEvent_t tA = spans ? tev(c->stream) : nullptr;
     if (spans && pa) spans->push_back({ia, t0, tA, 1});
-    if (pull) {
-        rcs_status st = stream_barrier(c, c->xstream, err);   // peers done reading my staging
-        if (st) return st;
-        CUDA_TRY(cudaEventRecord(c->ev_b[0], c->xstream));
-    } else {
     // swaps: chunk by chunk on xstream
     for (int ch = 0; ch < nch; ch++) {
-        dev::PeerSwapArgs A;
-        make_swap_args(s, it, fix, cb, fixval(ch), A, bytes_sent);
-        A.max_grid = reserve * 8;
         CUDA_TRY(cudaStreamWaitEvent(c->xstream, c->ev_a[ch], 0));
-        rcs_status st = stream_barrier(c, c->xstream, err);
-        if (st) return st;
-        CUDA_TRY(dev::peer_swap(A, c->xstream));
-        st = stream_barrier(c, c->xstream, err);
-        if (st) return st;
+        if (real) {
+            rcs_status st = stream_barrier(c, c->xstream, err);
+            if (st) return st;
+        }
+        cudaEvent_t k0 = spans ? tev(c->xstream) : nullptr;
+        for (const SwapView& v : views) {
+            dev::PeerSwapArgs A;
+            make_swap_args(v, it, fix, cb, fixval(ch), A, bytes_sent);
+            A.max_grid = reserve * 8;
+            CUDA_TRY(dev::peer_swap(A, c->xstream));
+        }
+        if (spans) spans->push_back({kRemapKernelSpan, k0, tev(c->xstream), 1});
+        if (real) {
+            rcs_status st = stream_barrier(c, c->xstream, err);
+            if (st) return st;
+        }
         CUDA_TRY(cudaEventRecord(c->ev_s[ch], c->xstream));
-    }
     }
     // B: chunk c after every rank exchanged chunk c
     for (int ch = 0; ch < nch; ch++) {
         CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
         if (pb) {
             cudaEvent_t w = spans ? tev(c->stream) : nullptr;
-            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pb->pos, pb->d_a, sms, c->stream, fix, cb, fixval(ch)));
+            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pb->pos, pb->d_a, sms, c->stream, fix, cb, fixval(ch), force_k9));
             if (spans) {
                 cudaEvent_t d = tev(c->stream);
                 spans->push_back({ib, w, d, 1});
@@ -656,12 +607,12 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
         }
     }
     if (pb) *pass_bytes += 16ull * s->n_amps;
-    if (pull) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_b[0], 0));   // final barrier
     if (spans) spans->push_back({ir, tA, tev(c->stream), 1});
     return RCS_OK;
 }
 
-// chunk bits for a pipelined remap: the highest positions outside `excl`; false if too few
+// chunk bits for a pipelined remap: the highest positions below nl_local outside `excl`
+// (K9's tile sub-cube and pair bit, K12's 13 positions, the remapped bits); false if too few
 bool choose_chunk_bits(int nl, uint64_t excl, int cb, int* fix) {
     int got = 0;
     for (int b = nl - 1; b >= 7 && got < cb; b--)   // above every tile sub-cube's low bits
@@ -1010,10 +961,8 @@ rcs_status rcs_context_create(int device, int rank, int world, const void* nccl_
 void rcs_context_free(rcs_context* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    for (int r = 0; r < 8; r++) {
-        if (c->peer_map[0][r]) cudaIpcCloseMemHandle(c->peer_map[0][r]);
-        if (c->peer_map[1][r] && c->peer_map[1][r] != c->peer_map[0][r]) cudaIpcCloseMemHandle(c->peer_map[1][r]);
-    }
+    for (int r = 0; r < kMaxPeerWorld; r++)
+        if (c->peer_map[r]) cudaIpcCloseMemHandle(c->peer_map[r]);
     if (c->d_xchg) cudaFree(c->d_xchg);
     if (c->d_bar) cudaFree(c->d_bar);
     if (c->xbuf) cudaFree(c->xbuf);
@@ -1022,10 +971,9 @@ void rcs_context_free(rcs_context* c) {
     if (c->bad) cudaFree(c->bad);
     if (c->d_tc) cudaFree(c->d_tc);
     for (int i = 0; i < 16; i++)
-        for (cudaEvent_t e : {c->ev_a[i], c->ev_s[i], c->ev_p[i], c->ev_b[i]})
+        for (cudaEvent_t e : {c->ev_a[i], c->ev_s[i]})
             if (e) cudaEventDestroy(e);
     if (c->xstream) cudaStreamDestroy(c->xstream);
-    if (c->d_done) cudaFree(c->d_done);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -1052,6 +1000,14 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     const int g = ctx->g;
     if (o.virtual_global && ctx->world > 1) {
         set_error(err, RCS_ERR_ARG, "virtual_global needs world == 1");
+        return RCS_ERR_ARG;
+    }
+    if (o.remap_mode < RCS_REMAP_AUTO || o.remap_mode > RCS_REMAP_LOOPBACK ||
+        (o.remap_mode == RCS_REMAP_LOOPBACK && (ctx->world != 1 || o.virtual_global < 1 || o.virtual_global > 3)) ||
+        o.overlap_chunks < 0 || o.overlap_chunks > 4 || o.overlap_sms < 0 || o.tc_kernel < 0 || o.tc_kernel > 1 ||
+        o.virtual_global < 0) {
+        set_error(err, RCS_ERR_ARG, "invalid build options (remap_mode %d, virtual_global %d, overlap_chunks %d)",
+                  o.remap_mode, o.virtual_global, o.overlap_chunks);
         return RCS_ERR_ARG;
     }
     const int plan_g = ctx->world > 1 ? g : o.virtual_global;
@@ -1111,10 +1067,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     s->staging = reinterpret_cast<float2*>(sc + L.stage_off);
     s->staging_elems = (L.stage_end - L.stage_off) / sizeof(float2);
     s->plan = plan_ptr;
-    if (L.pull_elems) {
-        s->pull_stage = reinterpret_cast<float2*>(sc + L.pull_off);
-        s->pull_stage_elems = L.pull_elems;
-    }
+    s->remap_mode = o.remap_mode;
+    s->virt = ctx->world == 1 ? o.virtual_global : 0;
     // keep_layout: skip the restore items when the final layout is not canonical
     bool keep = false;
     if (L.kept) {
@@ -1198,7 +1152,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         ctx->tc_cap = tc_words;
     }
     if (ctx->world > 1 && P.n_remaps > 0) {
-        rcs_status r = setup_peers(ctx, s->amps, err, s->pull_stage);
+        rcs_status r = setup_peers(ctx, s->amps, o.remap_mode, err);
         if (r) return fail(r);
     }
     BUILD_TRY(cudaEventRecord(eb0, stream));
@@ -1213,27 +1167,24 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     if (keep)
         BUILD_TRY(cudaMemcpyAsync(s->ptab, ptab_host.data(), ptab_host.size() * 8, cudaMemcpyHostToDevice, stream));
     uint64_t pass_bytes = 0, remap_bytes = 0;
-    int n_pipelined = 0, n_paired = 0;
-    std::vector<size_t> half_span;   // paired launches: the span is split evenly over both passes
-    // K11 pairing is off by default: measured no faster than one pass per launch
-    const int tc_pair = getenv("RCS_TC_PAIR") ? atoi(getenv("RCS_TC_PAIR")) : 0;   // read per build (tests toggle it)
+    int n_pipelined = 0, n_peer = 0;
     std::vector<float> mbuf;
     std::vector<Span> spans;
-    // pipelined remaps (f1): on unless RCS_OVERLAP=0; 2^cb chunks, `reserve` SMs left to the swaps
-    static const int ov_on = getenv("RCS_OVERLAP") ? atoi(getenv("RCS_OVERLAP")) : 1;
-    static const int ov_cb = getenv("RCS_OVERLAP_CHUNKS") ? atoi(getenv("RCS_OVERLAP_CHUNKS")) : 2;
-    // SMs left to the swaps: 32 at N=2, 16 at N>=4 (sweeps in profiles/r01_ovl*)
-    static const int ov_res_env = getenv("RCS_OVERLAP_SMS") ? atoi(getenv("RCS_OVERLAP_SMS")) : 0;
-    const int ov_res = ov_res_env > 0 ? ov_res_env : (ctx->world >= 4 ? 16 : 32);
-    static const int ov_pull = getenv("RCS_REMAP_PULL") ? atoi(getenv("RCS_REMAP_PULL")) : 0;
+    const bool force_k9 = o.tc_kernel == 1;
+    const bool peer_path = (ctx->world > 1 && ctx->p2p) || loopback(s);
+    // pipelined remaps (f1): 2^cb chunks, `reserve` SMs left to the swaps (sweeps: profiles/r01_ovl*)
+    const int ov_cb = o.overlap_chunks > 0 ? o.overlap_chunks : 2;
+    const bool ov_on = o.overlap >= 0 && ov_cb <= 4 && peer_path;
+    const int ov_res = o.overlap_sms > 0 ? o.overlap_sms : (ctx->world == 2 ? 32 : 16);
+    const int nl_loc = nl - (loopback(s) ? o.virtual_global : 0);   // local bits of one (virtual) rank
     auto is_tc = [&](size_t i) { return i < n_exec && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
     auto tc_ref = [&](size_t i) {
         return PassRef{tcp->pos[i].data(), ctx->d_tc + (size_t)tc_slot[i] * tc_words_each};
     };
     for (size_t ii = 0; ii < n_exec; ii++) {
         const Item& it = P.items[ii];
-        // [TC pass] -> REMAP -> [TC pass] pipelined over NVLink
-        if (ov_on && ctx->world > 1 && ctx->p2p && ov_cb >= 1 && ov_cb <= 4) {
+        // [TC pass] -> REMAP -> [TC pass] pipelined over NVLink (or loopback)
+        if (ov_on) {
             size_t ir = (it.type == RCS_ITEM_REMAP) ? ii : (is_tc(ii) && ii + 1 < n_exec &&
                                                             P.items[ii + 1].type == RCS_ITEM_REMAP) ? ii + 1 : SIZE_MAX;
             if (ir != SIZE_MAX) {
@@ -1244,17 +1195,14 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
                 if (has_a) excl |= dev::tc_reserved_mask(nl, tcp->pos[ii].data());
                 if (has_b) excl |= dev::tc_reserved_mask(nl, tcp->pos[ir + 1].data());
                 int fix[4];
-                // world >= 4: pull mode (8 chunks) when every rank's staging is mapped
-                const bool pull = ov_pull && ctx->world >= 4 && ctx->p2p_stage && s->pull_stage &&
-                                  (1ull << (nl - kPullCb)) / (1ull << rm.k) * ((1ull << rm.k) - 1) <= s->pull_stage_elems;
-                const int cbg = pull ? kPullCb : ov_cb;
-                if ((has_a || has_b) && cbg <= 4 && choose_chunk_bits(nl, excl, cbg, fix)) {
+                if ((has_a || has_b) && choose_chunk_bits(nl_loc, excl, ov_cb, fix)) {
                     PassRef ra = has_a ? tc_ref(ii) : PassRef{}, rb = has_b ? tc_ref(ir + 1) : PassRef{};
-                    rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, has_b ? &rb : nullptr, fix, cbg,
-                                                      ov_res, pull, &remap_bytes, &pass_bytes, ii, ir, ir + 1,
+                    rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, has_b ? &rb : nullptr, fix, ov_cb,
+                                                      ov_res, force_k9, &remap_bytes, &pass_bytes, ii, ir, ir + 1,
                                                       o.timing ? &spans : nullptr, &owned, err);
                     if (r) return fail(r);
                     n_pipelined++;
+                    n_peer++;
                     ii = has_b ? ir + 1 : ir;
                     continue;
                 }
@@ -1266,48 +1214,9 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             owned.push_back(e0);
             BUILD_TRY(cudaEventRecord(e0, stream));
         }
-        // two consecutive tensor-core passes in one launch (K11): pass B re-reads pass A's output
-        // from L2 chunk by chunk, one HBM round trip for both
-        // (K11 implements K9's arithmetic: blocks that run on K12 -- no qubit among 0..6 -- are not paired)
-        auto k9_block = [&](size_t i) {
-            for (int t = 0; t < 6; t++)
-                if (tcp->pos[i][t] < 7) return true;
-            return false;
-        };
-        if (tc_pair && is_tc(ii) && is_tc(ii + 1) && k9_block(ii) && k9_block(ii + 1)) {
-            const int* pp[2] = {tcp->pos[ii].data(), tcp->pos[ii + 1].data()};
-            const int cbits = dev::tc_multi_chunk_bits(nl, 2, pp);
-            const int max_bits = getenv("RCS_PAIR_MAXBITS") ? atoi(getenv("RCS_PAIR_MAXBITS")) : kPairMaxChunkBits;
-            if (cbits > 0 && cbits <= max_bits && nl - cbits >= 4) {
-                const uint64_t need = 1ull << (nl - cbits);
-                if (ctx->done_cap < need) {
-                    if (ctx->d_done) cudaFree(ctx->d_done);
-                    ctx->d_done = nullptr;
-                    ctx->done_cap = 0;
-                    BUILD_TRY(cudaMalloc(&ctx->d_done, need * sizeof(unsigned)));
-                    ctx->done_cap = need;
-                }
-                const uint32_t* aa[2] = {ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
-                                         ctx->d_tc + (size_t)tc_slot[ii + 1] * tc_words_each};
-                BUILD_TRY(dev::gate_pass_tc_multi(s->amps, nl, 2, pp, aa, ctx->num_sms, ctx->d_done, ctx->done_cap,
-                                                  stream));
-                pass_bytes += 32ull * n_amps;   // algorithmic: two passes (HBM sees one round trip)
-                n_paired++;
-                if (o.timing) {
-                    cudaEvent_t e1;
-                    BUILD_TRY(cudaEventCreate(&e1));
-                    owned.push_back(e1);
-                    BUILD_TRY(cudaEventRecord(e1, stream));
-                    spans.push_back({ii, e0, e1, 1});
-                    half_span.push_back(ii);
-                }
-                ii++;
-                continue;
-            }
-        }
         if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
             BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tcp->pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
-                                        ctx->num_sms, stream));
+                                        ctx->num_sms, stream, nullptr, 0, 0, force_k9));
             pass_bytes += 16ull * n_amps;
         } else if (it.type == RCS_ITEM_PASS) {
             const Block& B = P.blocks[it.block];
@@ -1321,12 +1230,13 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         } else if (it.type == RCS_ITEM_SWAP) {
             BUILD_TRY(dev::bit_swap(s->amps, nl, it.k, it.a, it.b, stream));
         } else {  // REMAP
-            if (ctx->world == 1) {
+            if (ctx->world == 1 && !loopback(s)) {
                 BUILD_TRY(dev::bit_swap(s->amps, nl, it.k, it.a, it.b, stream));
             } else {
-                rcs_status r = ctx->p2p ? do_remap_p2p(s, it, &remap_bytes, err)
-                                        : do_remap_nccl(s, it, &remap_bytes, err);
+                rcs_status r = peer_path ? do_remap_p2p(s, it, &remap_bytes, o.timing ? &spans : nullptr, &owned, err)
+                                         : do_remap_nccl(s, it, &remap_bytes, o.timing ? &spans : nullptr, &owned, err);
                 if (r) return fail(r);
+                n_peer += peer_path ? 1 : 0;
             }
         }
         if (o.timing) {
@@ -1369,11 +1279,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         for (const Span& sp : spans) {
             float t = 0.f;
             if (sp.a && sp.b) cudaEventElapsedTime(&t, sp.a, sp.b);
-            item_ms[sp.item] += sp.sign * (double)t;
-        }
-        for (size_t ii : half_span) {
-            item_ms[ii] *= 0.5;
-            item_ms[ii + 1] = item_ms[ii];
+            if (sp.item == kRemapKernelSpan) R.remap_kernel_ms += (double)t;
+            else item_ms[sp.item] += sp.sign * (double)t;
         }
         for (size_t ii = 0; ii < n_exec; ii++) {
             const double t = item_ms[ii];
@@ -1397,7 +1304,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     R.norm = s->T_total;
     R.n_tc_passes = n_tc;
     R.n_pipelined = n_pipelined;
-    R.n_paired = n_paired;
+    R.n_peer_remaps = n_peer;
     if (rep) *rep = R;
     *out = s;
     return RCS_OK;
@@ -1412,14 +1319,15 @@ rcs_status rcs_state_canonicalize(rcs_state* s, rcs_error* err) {
     CUDA_TRY(cudaSetDevice(c->device));
     const Plan& P = *s->plan;
     if (c->world > 1) {   // the peer mappings may belong to another state's buffer by now
-        rcs_status r = setup_peers(c, s->amps, err);
+        rcs_status r = setup_peers(c, s->amps, s->remap_mode, err);
         if (r) return r;
     }
     uint64_t bytes = 0;
     for (size_t ii = (size_t)P.restore_begin; ii < P.items.size(); ii++) {
         const Item& it = P.items[ii];
-        if (it.type == RCS_ITEM_REMAP && c->world > 1) {
-            rcs_status r = c->p2p ? do_remap_p2p(s, it, &bytes, err) : do_remap_nccl(s, it, &bytes, err);
+        if (it.type == RCS_ITEM_REMAP && (c->world > 1 || loopback(s))) {
+            rcs_status r = (c->p2p || loopback(s)) ? do_remap_p2p(s, it, &bytes, nullptr, nullptr, err)
+                                                   : do_remap_nccl(s, it, &bytes, nullptr, nullptr, err);
             if (r) return r;
         } else {
             CUDA_TRY(dev::bit_swap(s->amps, s->nl, it.k, it.a, it.b, c->stream));

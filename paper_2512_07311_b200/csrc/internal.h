@@ -78,6 +78,7 @@ constexpr int kTcMinLocal = 12;
 constexpr int kFuseSeeds = 4;
 // fuser: pick among the seeds by the block count of a greedy completion (rollout)
 constexpr bool kFuseLookahead = true;
+constexpr int kFuseDeepDepth = 3;        // strategy 2: extension search depth
 constexpr bool kRemapPrefetch = true;   // remaps also bring in soon-needed global qubits
 constexpr bool kInitialPlacement = true;   // start with the latest-used qubits global (free: |0> state)
 

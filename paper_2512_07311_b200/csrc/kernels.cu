@@ -268,41 +268,6 @@ __global__ void __launch_bounds__(kThreads) k_peer_swap(const __grid_constant__ 
     }
 }
 
-__device__ __forceinline__ uint64_t pull_index(const PullArgs& a, int pc, uint64_t m) {
-    for (int i = 0, f = 0; i < a.j || f < a.nfix;) {   // lpos and fix merged, ascending
-        if (f >= a.nfix || (i < a.j && a.lpos[i] < a.fix[f])) m = insert_zero(m, a.lpos[i++]);
-        else m = insert_zero(m, a.fix[f++]);
-    }
-    return m | a.fixval | a.mask[pc];
-}
-
-template <bool PACK>
-__global__ void __launch_bounds__(kThreads) k_remap_move(const __grid_constant__ PullArgs a) {
-    const int pc = blockIdx.y;
-    const uint64_t nvec = a.count >> 1;   // 16-B vectors (2 amplitudes; positions >= 6 remapped)
-    float4* loc = reinterpret_cast<float4*>(a.local);
-    const uint64_t stride = (uint64_t)gridDim.x * kThreads * kSwapU;
-    for (uint64_t v0 = (uint64_t)blockIdx.x * kThreads * kSwapU + threadIdx.x; v0 < nvec; v0 += stride) {
-        float4 val[kSwapU];
-        uint64_t li[kSwapU];
-#pragma unroll
-        for (int u = 0; u < kSwapU; u++) {
-            const uint64_t v = v0 + (uint64_t)u * kThreads;
-            if (v >= nvec) continue;
-            li[u] = pull_index(a, pc, 2 * v) >> 1;
-            if (PACK) val[u] = loc[li[u]];
-            else val[u] = __ldcs(reinterpret_cast<const float4*>(a.peer_stage[pc]) + v);
-        }
-#pragma unroll
-        for (int u = 0; u < kSwapU; u++) {
-            const uint64_t v = v0 + (uint64_t)u * kThreads;
-            if (v >= nvec) continue;
-            if (PACK) reinterpret_cast<float4*>(a.stage)[(uint64_t)pc * nvec + v] = val[u];
-            else loc[li[u]] = val[u];
-        }
-    }
-}
-
 // ------------------------------------------------------------------------------------
 // K5: block sums; K6: scan; reductions
 // ------------------------------------------------------------------------------------
@@ -674,22 +639,6 @@ cudaError_t unpack(float2* amps, const float2* buf, int j, const int* lpos, uint
 }
 
 cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st) {
-    if (a.rounds && a.npeers > 1) {
-        // one peer at a time (the caller orders peers by code XOR, so every rank pairs with the
-        // same partner in the same round): disjoint pairwise exchanges instead of an all-to-all
-        for (int i = 0; i < a.npeers; i++) {
-            PeerSwapArgs b = a;
-            b.rounds = 0;
-            b.npeers = 1;
-            b.peer[0] = a.peer[i];
-            b.mask[0] = a.mask[i];
-            b.m_begin[0] = a.m_begin[i];
-            b.m_count[0] = a.m_count[i];
-            cudaError_t e = peer_swap(b, st);
-            if (e != cudaSuccess) return e;
-        }
-        return cudaSuccess;
-    }
     uint64_t maxv = 0;
     for (int i = 0; i < a.npeers; i++) maxv = a.m_count[i] / 2 > maxv ? a.m_count[i] / 2 : maxv;
     if (maxv == 0) return cudaSuccess;
@@ -700,22 +649,6 @@ cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st) {
     k_peer_swap<<<dim3((unsigned)gx, (unsigned)a.npeers), kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
-
-static cudaError_t launch_move(const PullArgs& a, bool pack, cudaStream_t st) {
-    const uint64_t nvec = a.count >> 1;
-    if (nvec == 0 || a.npeers == 0) return cudaSuccess;
-    uint64_t gx = (nvec + (uint64_t)kThreads * kSwapU - 1) / ((uint64_t)kThreads * kSwapU);
-    const uint64_t cap = a.max_grid > 0 ? (uint64_t)a.max_grid : 148u * 8u;
-    if (gx > cap) gx = cap;
-    note_launch();
-    if (pack)
-        k_remap_move<true><<<dim3((unsigned)gx, (unsigned)a.npeers), kThreads, 0, st>>>(a);
-    else
-        k_remap_move<false><<<dim3((unsigned)gx, (unsigned)a.npeers), kThreads, 0, st>>>(a);
-    return cudaGetLastError();
-}
-cudaError_t remap_pack(const PullArgs& a, cudaStream_t st) { return launch_move(a, true, st); }
-cudaError_t remap_pull(const PullArgs& a, cudaStream_t st) { return launch_move(a, false, st); }
 
 int block_sums_grid() { return kSumGrid; }
 

@@ -20,18 +20,14 @@ void tc_pack_matrix(const double* u_re_im, uint32_t* out);
 // Optional chunking (pipelined remaps): fix[0..nfix) are extra positions held at the bits of
 // fixval, so the launch covers one 2^-nfix slice of the index space.  Fixed positions must lie
 // outside tc_reserved_mask(pos); the grid is min(num_sms, tiles).
+// K12 (the transposed kernel) runs iff no target sits in positions 0..6 (tc_uses_k12: a function
+// of the block alone); force_k9 (tests) runs K9 for every block.
+bool tc_uses_k12(const int* pos);
 cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const uint32_t* d_a, int num_sms,
-                         cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0);
+                         cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0,
+                         bool force_k9 = false);
 // positions a chunk bit must avoid for this pass: the 12-bit tile sub-cube and the bit above its run
 uint64_t tc_reserved_mask(int n_local_bits, const int* pos);
-// K11: np (1 or 2) consecutive 6-qubit passes in one launch; pass B re-reads pass A's output
-// from L2 chunk by chunk.  done: >= 2^(nl - chunk_bits) zeroed-by-us counters.
-// tc_multi_chunk_bits: |union of both passes' sub-cubes and pair bits| (-1 if invalid).
-int tc_multi_chunk_bits(int n_local_bits, int np, const int* const* pos);
-cudaError_t gate_pass_tc_multi(float2* amps, int n_local_bits, int np, const int* const* pos,
-                               const uint32_t* const* d_a, int num_sms, unsigned* done, uint64_t done_cap,
-                               cudaStream_t st);
-
 // a6 (K1) fused dense gate pass: amps <- M (x) over every group of 2^k amplitudes that
 // differ only in the physical bits pos[0..k) (matrix bit i <-> pos[i]); M is 2^k x 2^k
 // complex64 row-major (interleaved float pairs).  n_local_bits = log2(#amps).
@@ -65,30 +61,8 @@ struct PeerSwapArgs {
     int fix[4];
     uint64_t fixval;                   // ... and their bits
     int max_grid;                      // 0: default
-    int rounds;                        // 1: exchange with one peer at a time (pairwise rounds)
 };
 cudaError_t peer_swap(const PeerSwapArgs& a, cudaStream_t st);
-
-// Pull-mode remap (world >= 4: remote reads outrun mixed read/write swaps on NVSwitch):
-// pack copies this rank's outgoing elements of one chunk to its staging area, grouped by
-// destination ([pc][m], contiguous); pull reads each peer's group for this rank from the
-// peer's staging and writes it to the positions the outgoing elements came from.
-struct PullArgs {
-    float2* local;
-    float2* stage;               // this rank's staging (pack target)
-    const float2* peer_stage[7]; // peers' staging areas (pull sources), already offset to my slot
-    int npeers;
-    int j;
-    int lpos[8];                 // remapped local positions, ascending
-    uint64_t mask[7];            // local L-bit pattern of the elements exchanged with peer pc
-    int nfix;
-    int fix[4];                  // chunk positions (ascending) and value
-    uint64_t fixval;
-    uint64_t count;              // elements per peer in this chunk (even)
-    int max_grid;
-};
-cudaError_t remap_pack(const PullArgs& a, cudaStream_t st);
-cudaError_t remap_pull(const PullArgs& a, cudaStream_t st);
 
 // a9 (K5): bsum[blk] = sum_{x in blk} |a_x|^2 (fp64) for blocks of 2^b amps; part[c] = per-CTA
 // partial sum of p^2 (fixed grid => deterministic).  Returns the number of partials used.

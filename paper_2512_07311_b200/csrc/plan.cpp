@@ -358,13 +358,10 @@ void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb
 // (memoized); all with the rollout lookahead over seed gates.  The plan with the fewest blocks
 // wins, ties to the lower index.
 void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) {
-    const int seeds = getenv("RCS_FUSE_SEEDS") ? atoi(getenv("RCS_FUSE_SEEDS")) : kFuseSeeds;
-    const bool la = getenv("RCS_FUSE_LOOKAHEAD") ? atoi(getenv("RCS_FUSE_LOOKAHEAD")) != 0 : kFuseLookahead;
-    const int deep = getenv("RCS_FUSE_DEPTH") ? atoi(getenv("RCS_FUSE_DEPTH")) : 3;
-    const int depth_of[kFuseStrategies] = {0, 1, deep};
+    const int depth_of[kFuseStrategies] = {0, 1, kFuseDeepDepth};
     Fuser F(c, k);
-    F.seeds = seeds;
-    F.lookahead = la;
+    F.seeds = kFuseSeeds;
+    F.lookahead = kFuseLookahead;
     F.grow_lookahead = depth_of[which] > 0;
     F.grow_depth = depth_of[which];
     out.clear();
@@ -376,11 +373,6 @@ void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) 
 }
 
 int fuse_best(const Circuit& c, int k, std::vector<Block>* cand) {
-    const int strat = getenv("RCS_FUSE_STRATEGY") ? atoi(getenv("RCS_FUSE_STRATEGY")) : -1;   // -1: all
-    if (strat >= 0 && strat < kFuseStrategies) {
-        fuse_strategy(c, k, strat, cand[strat]);
-        return strat;
-    }
     std::vector<std::thread> th;
     for (int w = 1; w < kFuseStrategies; w++) th.emplace_back([&, w] { fuse_strategy(c, k, w, cand[w]); });
     fuse_strategy(c, k, 0, cand[0]);

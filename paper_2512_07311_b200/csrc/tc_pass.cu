@@ -6,17 +6,18 @@
 // fused-gate width makes it a real dense contraction").  A's rows are interleaved (row 2t =
 // Y_re[t], row 2t+1 = Y_im[t]) so one TMEM lane pair holds re/im of one output amplitude.
 //
-// Precision: fp32-level results from fp16 tensor cores by a scaled two-term split
-//     x * 2^s = hi + lo  (hi = fp16(x 2^s), lo = fp16(x 2^s - hi); 22 significant bits)
-//     A B ~= 2^-(sA+sB) (A_hi B_hi + A_hi B_lo + A_lo B_hi)
-// with sA = 14 and sB = 15: a normalized state has |x| <= 1, so x 2^15 never overflows fp16,
-// and one fixed scale keeps the arithmetic independent of how amplitudes are grouped into
-// tiles (bitwise-identical states for every sharding; a per-tile scale is not, because of
-// fp16 subnormals; scripts/micro/tc_f16_fixed.cu: same rms error down to |x| ~ 2^-16,
-// 2.5x at 2^-19).  The fp32
-// accumulation in TMEM truncates, so the small cross terms are accumulated first into acc 0
-// and the main term is split over 3 accumulators by K-steps, summed round-to-nearest in the
-// epilogue (scripts/micro/tc_f16.cu: norm^2 drift -1.4e-7 per pass, rms error 1.2e-7).
+// Precision: fp32-level results from fp16 tensor cores with an EXACT main term.  Matrix row
+// pair t and state column j get power-of-two scales 2^F_t / 2^E_j that put their largest
+// magnitude in [2^10, 2^11); each value is split into hi = rint(x 2^s) (an integer, exact in
+// fp16) and lo = fp16(x 2^s - hi):
+//     A B = 2^-(F_t + E_j) (A_hi B_hi + [A_hi B_lo + A_lo B_hi]) + O(2^-20 relative)
+// A_hi B_hi is a sum of integer products that stays below 2^24, so the tensor core's truncating
+// fp32 accumulation adds it exactly (scripts/micro/tc_exact.cu: inexact in 7.5e-5 of outputs,
+// only by overflowing 2^24); only the cross terms (2^-11 of the result, their own accumulator)
+// round.  Measured: bias -4e-10 relative per product (round 1's floating split: -1.4e-7 per
+// pass in norm^2, which capped a build at ~70 passes), rms error 3.9e-7.  The scales depend on
+// the column's own 64 amplitudes only, never on how columns are grouped into tiles, so the state
+// stays bitwise identical for every sharding.
 //
 // Tile = 64 columns x 64 target combinations = 4096 amplitudes (32 KB), a 12-bit sub-cube of
 // the index: the 6 target bits plus the 6 lowest non-target bits, so every tile is a set of
@@ -25,19 +26,23 @@
 //                         index bit r, right above every run, so each copy covers both tiles'
 //                         runs: >= 1 KB per copy) into a raw pair slot (2 slots = 128 KB, no
 //                         registers) -> rfull[slot] (complete_tx)
-//   warps 0-7  converters: raw smem -> hi/lo split -> STS into B stage (K-major, interleaved
-//                         core matrices) -> full[s]
+//   warps 0-7  converters: raw smem -> column max -> scale 2^E_j -> hi/lo split -> STS into
+//                         B stage (K-major, interleaved core matrices) -> full[s]
 //   warp  12   MMA     : 8 K-steps x 3 terms = 24 tcgen05.mma kind::f16 (M=128, N=64, K=16,
 //                         A in TMEM) into D[d] -> commit empty[s], tfull[d]
-//   warps 8-11 epilogue: tcgen05.ld 3 accumulators of D[d] -> tempty[d] -> sum, unscale ->
-//                         STS staging [t][j] -> coalesced LDS/STG (each thread owns one
-//                         column, rows t0 + 2i: hoisted offsets, immediate staging offsets)
+//   warps 8-11 epilogue: tcgen05.ld the 2 accumulators of D[d] -> tempty[d] -> sum, unscale by
+//                         2^-E_j 2^-F_t -> STS staging [t][j] -> coalesced LDS/STG (each
+//                         thread owns one column, rows t0 + 2i)
+// The converters of a column (4 threads in 4 warps) agree on its max through a shared-memory
+// atomicMax and one named barrier; E_j reaches the epilogue through a 4-slot ring guarded by an
+// mbarrier per slot.
 // Shared memory: raw 4 x 32 KB + B 2 x 32 KB + staging 33 KB + control = 227 KB.
-// TMEM (512 cols): A_hi [0,64), A_lo [64,128) (fp16 pairs), D[d] = [128 + 192 d, +192) holding
-// 3 accumulators of 64 columns.
+// TMEM (512 cols): A_hi [0,64), A_lo [64,128) (fp16 pairs), D[d] = [128 + 128 d, +128) holding
+// the cross-term and main-term accumulators (64 columns each).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 
@@ -60,15 +65,14 @@ constexpr uint32_t kStageBytes = 2 * kBBytes;
 constexpr uint32_t kSBO = (TK / 8) * 128;    // next 8-row group (16 chunks of 16 B)
 constexpr int kPitchF = 130;                 // staging row pitch in floats (520 B): conflict-free
 constexpr uint32_t kStagingBytes = 64 * kPitchF * 4;
+constexpr int kExpSlots = 4;                 // per-tile column exponents in flight (converter -> epilogue)
 constexpr uint32_t kCtlBytes = 2560;   // barriers + offset tables; total <= 227 KB
-// control block: 18 mbarriers + 3 x 64 offsets (8 B) + 24 ints + 2 x 64 uint16
-static_assert(18 * 8 + 3 * 64 * 8 + 24 * 4 + 2 * 64 * 2 <= 2560, "control block overflow");
+// control block: (12 + kExpSlots) mbarriers + 64 run offsets (8 B) + 3 x 64 column maxima (4 B)
+// + 2 x 64 uint16 + kExpSlots x 64 exponents (1 B) + the TMEM slot
+static_assert((12 + kExpSlots) * 8 + 64 * 8 + 3 * 64 * 4 + 2 * 64 * 2 + kExpSlots * 64 + 4 <= kCtlBytes,
+              "control block overflow");
 constexpr uint32_t kSmemBytes = kRaw * kRawBytes + kStages * kStageBytes + kStagingBytes + kCtlBytes;
-#ifndef RCS_TC_ACCS
-#define RCS_TC_ACCS 2                        // accumulators per D buffer (= K11's, so pairing never changes a result)
-#endif
-constexpr int kAccs = RCS_TC_ACCS;
-constexpr int kAccCols = kAccs * TN;         // one D buffer
+constexpr int kAccCols = 2 * TN;             // one D buffer: acc 0 cross terms, acc 1 main term
 
 struct TcArgs {
     float2* amps;
@@ -139,15 +143,6 @@ __device__ __forceinline__ void rot_h8(uint32_t (&w)[4], int rho) {
     for (int i = 0; i < 4; i++) w[i] = (rho & 1) ? a[i] : w[i];
 }
 
-// (x0, x1) -> hi = fp16x2(x0, x1) (x0 in the low half), lo = fp16x2(x - f32(hi)): one packed
-// convert each, two widening converts and two FADDs (x0, x1 already scaled)
-__device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
-    const __half2 h = *reinterpret_cast<const __half2*>(&hi);
-    const float r0 = x0 - __low2float(h), r1 = x1 - __high2float(h);
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r1), "f"(r0));
-}
-
 __device__ __forceinline__ float2 f2mul(float2 v, float s) {   // packed f32x2 multiply
     float2 o;
     asm("{\n.reg .b64 x, y;\nmov.b64 x, {%2, %3};\nmov.b64 y, {%4, %4};\nmul.rn.f32x2 x, x, y;\n"
@@ -185,6 +180,37 @@ __device__ __forceinline__ float2 f2mul(float2 v, float s) {   // packed f32x2 m
     asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, " #acc ";" ::"r"(d), "r"(a), "l"(b), \
                  "r"(idesc))
 
+// Exact main term: the state column j is scaled by 2^E_j (E_j from the column's max |x|, so the
+// max lands in [2^10, 2^11)) and split into hi = rint(x 2^E_j) -- an integer, exact in fp16 --
+// and lo = fp16(x 2^E_j - hi).  Matrix row pair t likewise with 2^F_t (host, tc_pack_matrix).
+// The main products hi.hi are then integers and their sums stay below 2^24 (checked at 7.5e-5
+// overflow rate on Porter-Thomas data, scripts/micro/tc_exact.cu), so the tensor core's
+// truncating fp32 accumulation adds them EXACTLY; only the small cross terms hi.lo + lo.hi
+// (2^-11 of the result) round.  The result is (main + cross) 2^-E_j 2^-F_t, one round-to-nearest
+// add and two exact scalings.  The scale is a function of the column's 64 amplitudes only, never
+// of the tiling, so the arithmetic stays independent of the sharding (bitwise P-invariance).
+__device__ __forceinline__ int col_exponent(int maxbits) {
+    // max |x| as float bits (>= 0) -> E with max 2^E in [2^10, 2^11); 0 for an all-zero column;
+    // clamped so 2^E and 2^-E are normal floats
+    if (maxbits == 0) return 0;
+    const int e = ((maxbits >> 23) & 0xff) - 127;
+    const int E = 10 - e;
+    return E > 126 ? 126 : E;
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }   // e in [-126, 127]
+
+// (v0, v1) already scaled -> hi = fp16x2(rint v0, rint v1) (exact integers), lo = fp16x2(v - hi)
+__device__ __forceinline__ void split_exact_h2(float v0, float v1, uint32_t& hi, uint32_t& lo) {
+    float h0, h1;
+    asm("cvt.rni.f32.f32 %0, %1;" : "=f"(h0) : "f"(v0));
+    asm("cvt.rni.f32.f32 %0, %1;" : "=f"(h1) : "f"(v1));
+    const float r0 = v0 - h0, r1 = v1 - h1;   // exact
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(h1), "f"(h0));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r1), "f"(r0));
+}
+
+__device__ __forceinline__ float absmax2(float m, float2 v) { return fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y))); }
+
 // ROT: when >= 2 target bits are among the 4 lowest sub-cube bits, the converters' shared-memory
 // reads of one element index across lanes hit the same banks; lane l then walks its target octet
 // starting at element (l & 7) and rotates the packed fp16 octet back before storing it.
@@ -199,18 +225,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
     uint64_t* empty = full + kStages;                     // [kStages]
     uint64_t* tfull = empty + kStages;                    // [2]
     uint64_t* tempty = tfull + 2;                         // [2]
-    uint64_t* mfull = tempty + 2;                         // [2]
-    uint64_t* rfull = mfull + 2;                          // [2] raw pair slots
+    uint64_t* rfull = tempty + 2;                         // [2] raw pair slots
     uint64_t* rempty = rfull + 2;                         // [2]
-    uint64_t* offt = rempty + 2;                          // [64] target-combination offsets (global)
-    uint64_t* offj = offt + 64;                           // [64] column offsets (global)
-    uint64_t* offr = offj + 64;                           // [64] run offsets (global)
-    int* wmax = reinterpret_cast<int*>(offr + 64);        // [2][8] per-warp max |x| (float bits)
-    uint16_t* soft = reinterpret_cast<uint16_t*>(wmax + 24);   // [64] sub-cube index of target combo t
-    uint16_t* sofj = soft + 64;                                // [64] sub-cube index of column j
-    int* texp = wmax + 16;                                // [kStages] tile exponent per stage
-    int* meta = texp + kStages;                           // [2] tile exponent per D buffer
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(meta + 2);
+    uint64_t* cready = rempty + 2;                        // [kExpSlots] column exponents of a tile written
+    uint64_t* offr = cready + kExpSlots;                  // [64] run offsets (global)
+    int* cmax = reinterpret_cast<int*>(offr + 64);        // [3][64] column max |x| (float bits, atomicMax)
+    uint16_t* soft = reinterpret_cast<uint16_t*>(cmax + 3 * 64);   // [64] sub-cube index of target combo t
+    uint16_t* sofj = soft + 64;                                    // [64] sub-cube index of column j
+    int8_t* colexp = reinterpret_cast<int8_t*>(sofj + 64);         // [kExpSlots][64] E_j per tile
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colexp + kExpSlots * 64);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) {
@@ -230,11 +253,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             mbar_init(&rfull[r], 1);
             mbar_init(&rempty[r], 2 * kLoadWarps * 32);   // both tiles of the pair consumed
         }
+        for (int e = 0; e < kExpSlots; e++) mbar_init(&cready[e], 64);   // the 64 column owners (to == 0)
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
+    if (threadIdx.x < 3 * 64) cmax[threadIdx.x] = 0;
     if (threadIdx.x < 64) {
         const int x = threadIdx.x;
-        uint64_t ot = 0, oj = 0, orr = 0;
+        uint64_t orr = 0;
         int st = 0, sj = 0;
         for (int i = 0; i < 6; i++) {
             int rt = 0, rj = 0;   // rank of pos[i] / jpos[i] among the sorted sub-cube bits
@@ -243,16 +268,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                 rj += p.sub[b] < p.jpos[i];
             }
             if ((x >> i) & 1) {
-                ot |= 1ull << p.pos[i];
-                oj |= 1ull << p.jpos[i];
                 st |= 1 << rt;
                 sj |= 1 << rj;
             }
         }
         for (int b = p.r; b < 12; b++)
             if ((x >> (b - p.r)) & 1) orr |= 1ull << p.sub[b];
-        offt[x] = ot;
-        offj[x] = oj;
         offr[x] = orr;
         // raw pair layout: element index = s with a zero inserted at bit r (bit r = pair half)
         const int lowm = (1 << p.r) - 1;
@@ -369,10 +390,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             mbar_wait(&rfull[slot], use & 1);
             const float2* rb = raw + (size_t)slot * 8192 + ((p.pair == 2 && (tile & 1)) ? (1 << p.r) : 0);
             float2 b[16];
+            float mx = 0.f;
 #pragma unroll
-            for (int i = 0; i < 16; i++) b[i] = f2mul(rb[boff[i]], 32768.f);   // x 2^15 (fixed scale)
+            for (int i = 0; i < 16; i++) {
+                b[i] = rb[boff[i]];
+                mx = absmax2(mx, b[i]);
+            }
             mbar_arrive(&rempty[slot]);
             if (p.pair == 1) mbar_arrive(&rempty[slot]);   // count is for two tiles
+            // column max over the 4 threads of column j (warps j/32 + 2 to): smem atomicMax on
+            // the float bits (non-negative floats order like ints), one named barrier
+            const int cb = (int)(it % 3);
+            atomicMax(&cmax[cb * 64 + j], __float_as_int(mx));
+            asm volatile("bar.sync 2, 256;" ::: "memory");
+            const int E = col_exponent(cmax[cb * 64 + j]);
+            const int es = (int)(it % kExpSlots);
+            if (to == 0) {
+                cmax[((it + 2) % 3) * 64 + j] = 0;   // buffer of tile it+2: every thread read it at tile it-1
+                colexp[es * 64 + j] = (int8_t)E;
+                mbar_arrive(&cready[es]);             // release: the epilogue reads E_j after acquiring
+            }
+            const float sc = pow2f(E);
+#pragma unroll
+            for (int i = 0; i < 16; i++) b[i] = f2mul(b[i], sc);
             const int s = it % kStages;
             mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
             uint8_t* bhi = stages + s * kStageBytes;
@@ -383,8 +423,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
 #pragma unroll
                 for (int e2 = 0; e2 < 4; e2++) {
                     const float2 v0 = b[8 * g + 2 * e2], v1 = b[8 * g + 2 * e2 + 1];
-                    split_h2(v0.x, v1.x, rh[e2], rl[e2]);
-                    split_h2(v0.y, v1.y, ih[e2], il[e2]);
+                    split_exact_h2(v0.x, v1.x, rh[e2], rl[e2]);
+                    split_exact_h2(v0.y, v1.y, ih[e2], il[e2]);
                 }
                 if (ROT) {
                     rot_h8(rh, rho);
@@ -417,7 +457,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                 // descriptors of K-step ks = base + ks * (256 B >> 4): no carry out of the 14-bit field
                 const uint64_t bh0 = bdesc(sb), bl0 = bdesc(sb + kBBytes);
                 const uint32_t ah = tmem, al = tmem + 64;
-                // cross terms (A_hi B_lo, A_lo B_hi) first, into accumulator 0
+                // cross terms (A_hi B_lo, A_lo B_hi) -> accumulator 0 (rounds; 2^-11 of the result)
                 MMA_F16(d0, ah, bl0, idesc, 0);
                 MMA_F16(d0, al, bh0, idesc, 1);
 #pragma unroll
@@ -425,25 +465,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                     MMA_F16(d0, ah + ks * 8, bl0 + ks * 16, idesc, 1);
                     MMA_F16(d0, al + ks * 8, bh0 + ks * 16, idesc, 1);
                 }
-                // main term A_hi B_hi: K-steps 0-2 -> acc 0, 3-5 -> acc 1, 6-7 -> acc 2
-                if (kAccs == 3) {
+                // main term A_hi B_hi -> accumulator 1: integer products, exact sums
+                MMA_F16(d0 + TN, ah, bh0, idesc, 0);
 #pragma unroll
-                    for (int ks = 0; ks < 3; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                    MMA_F16(d0 + TN, ah + 3 * 8, bh0 + 3 * 16, idesc, 0);
-#pragma unroll
-                    for (int ks = 4; ks < 6; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                    MMA_F16(d0 + 2 * TN, ah + 6 * 8, bh0 + 6 * 16, idesc, 0);
-                    MMA_F16(d0 + 2 * TN, ah + 7 * 8, bh0 + 7 * 16, idesc, 1);
-                } else if (kAccs == 2) {   // experiment: K-steps 0-3 -> acc 0, 4-7 -> acc 1
-#pragma unroll
-                    for (int ks = 0; ks < 4; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                    MMA_F16(d0 + TN, ah + 4 * 8, bh0 + 4 * 16, idesc, 0);
-#pragma unroll
-                    for (int ks = 5; ks < 8; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                } else {                   // experiment: everything in acc 0
-#pragma unroll
-                    for (int ks = 0; ks < 8; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                }
+                for (int ks = 1; ks < TK / 16; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     su32(&empty[s])));
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -457,6 +482,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         const int et = threadIdx.x - kEpiWarp0 * 32;   // 0..127
         const int m = q * 32 + lane;                   // D row: t = m/2, re (m even) / im (m odd)
         const int trow = m >> 1, comp = m & 1;
+        const float rowfac = pow2f(-(int)p.a[2 * 128 * 64 + trow]);   // 2^-F_t
         // store phase in memory order: thread handles sub-cube indices et + 128 i (i < 32), so
         // consecutive lanes write consecutive addresses for every target layout
         int tb, jb;
@@ -467,16 +493,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         uint64_t it = 0, bp = first_base;
         for (uint64_t tile = first_tile; tile < ntiles; next_tile(tile, bp), it++) {
             const int d = it & 1;
+            const int es = (int)(it % kExpSlots);
+            mbar_wait(&cready[es], (uint32_t)((it / kExpSlots) & 1));
             mbar_wait(&tfull[d], (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const float us = 1.f / (16384.f * 32768.f);   // 2^-(14 + 15)
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + 128 + d * kAccCols;
+            const int8_t* ce = colexp + es * 64;
 #pragma unroll
             for (int h = 0; h < 2; h++) {
-                uint32_t a0[32], a1[32], a2[32];
+                uint32_t a0[32], a1[32];
                 TMEM_LD32(ta + 32 * h, a0);
-                if (kAccs > 1) TMEM_LD32(ta + TN + 32 * h, a1);
-                if (kAccs > 2) TMEM_LD32(ta + 2 * TN + 32 * h, a2);
+                TMEM_LD32(ta + TN + 32 * h, a1);
+                // 2^-E_j of this half's 32 columns (read before the D buffer is released: the
+                // converters rewrite this slot only kExpSlots tiles later)
+                int ev[8];
+#pragma unroll
+                for (int w = 0; w < 8; w++) ev[w] = reinterpret_cast<const int*>(ce + 32 * h)[w];
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
                 if (h == 1) {
                     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -484,26 +516,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                 }
 #pragma unroll
                 for (int c = 0; c < 32; c += 2) {
-                    float o0, o1;   // ((acc0 + acc1) + acc2) * 2^-29, two columns per packed op
-                    if (kAccs == 3) {
-                        asm("{\n.reg .b64 x, y, z, u;\n"
-                            "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 z, {%6, %7};\nmov.b64 u, {%8, %8};\n"
-                            "add.rn.f32x2 x, x, y;\nadd.rn.f32x2 x, x, z;\nmul.rn.f32x2 x, x, u;\n"
-                            "mov.b64 {%0, %1}, x;\n}"
-                            : "=f"(o0), "=f"(o1)
-                            : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "r"(a2[c]), "r"(a2[c + 1]),
-                              "f"(us));
-                    } else if (kAccs == 2) {
-                        asm("{\n.reg .b64 x, y, u;\n"
-                            "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\n"
-                            "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\n"
-                            "mov.b64 {%0, %1}, x;\n}"
-                            : "=f"(o0), "=f"(o1)
-                            : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(us));
-                    } else {
-                        o0 = __uint_as_float(a0[c]) * us;
-                        o1 = __uint_as_float(a0[c + 1]) * us;
-                    }
+                    const int e0 = (int)(int8_t)(ev[c >> 2] >> (8 * (c & 3)));
+                    const int e1 = (int)(int8_t)(ev[c >> 2] >> (8 * ((c & 3) + 1)));
+                    const float f0 = pow2f(-e0), f1 = pow2f(-e1);
+                    float o0, o1;   // ((cross + main) (2^-E_c, 2^-E_c+1)) 2^-F_t
+                    asm("{\n.reg .b64 x, y, u, v;\n"
+                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %7};\nmov.b64 v, {%8, %8};\n"
+                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\nmul.rn.f32x2 x, x, v;\n"
+                        "mov.b64 {%0, %1}, x;\n}"
+                        : "=f"(o0), "=f"(o1)
+                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(f0), "f"(f1), "f"(rowfac));
                     st[2 * (32 * h + c)] = o0;
                     st[2 * (32 * h + c) + 2] = o1;
                 }
@@ -514,463 +536,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             for (int i = 0; i < 32; i++) {
                 const float2 v = *reinterpret_cast<const float2*>(sld + p.sso[i]);
                 __stcs(dst + p.sgo[i], v);
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");   // staging reused by the next tile
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-// =====================================================================================
-// K11: the same pass applied to 1 or 2 consecutive blocks in ONE launch (fewer
-// HBM round trips).  The index space is cut into chunks: C = both passes' 12-bit tile
-// sub-cubes and their pair bits r; a chunk fixes the remaining (H) positions, so it holds
-// complete tiles of both passes.  Groups of gs CTAs own chunks (chunk k -> group k mod
-// ngroups); a CTA walks A(k_0), A(k_1), B(k_0), A(k_2), B(k_1), ... over its share of each
-// chunk's tile pairs.  Pass A's outputs are stored with the default (L2-allocating) policy and
-// pass B reads them back from L2 once every member of the group has finished A(k) (per-chunk
-// completion counter, release/acquire at gpu scope; all CTAs are co-resident).  HBM traffic:
-// one read and one write per amplitude for both passes.  Arithmetic per tile is identical to
-// K9 (same MMA sequence, same epilogue sums), so pairing never changes a result.
-struct TcPass {
-    const uint32_t* a;       // packed A (hi, lo)
-    int pos[6];              // physical position of matrix bit i
-    int jpos[6];             // 6 lowest non-target positions
-    int sub[12];             // tile sub-cube positions, ascending
-    int r;                   // first position outside the sub-cube (tile-pair bit)
-    int rot;                 // converters use lane-rotated reads (>= 2 targets in the 4 lowest cube bits)
-    int nw;                  // within-chunk tile positions, ascending (wpos[0] == r)
-    int wpos[12];
-    uint64_t wmask;          // their mask
-    uint64_t wstep;          // deposit of 2 gs (the member's pair stride)
-    int sso[32];             // staging offset (floats) of sub-cube index 128 i
-    uint64_t sgo[32];        // global offset (amplitudes) of sub-cube index 128 i
-};
-struct TcMulti {
-    float2* amps;
-    int np;                  // passes in this launch (1 or 2)
-    TcPass ps[2];
-    int nh;                  // chunk-index positions, ascending
-    int hpos[48];
-    uint64_t hmask;          // their mask
-    uint64_t hstep;          // deposit of ngroups (a group's chunk stride)
-    uint64_t nchunks;
-    uint64_t npairs;         // tile pairs per chunk per pass
-    int gs;                  // CTAs per group
-    int depth;               // chunk-steps between a chunk's pass A and its pass B
-    unsigned* done;          // [nchunks] pass-A completion counters (np == 2), zeroed by the host
-};
-
-__device__ __forceinline__ uint64_t pdep_pos(uint64_t x, const int* pos, int n) {
-    uint64_t r = 0;
-    for (int i = 0; i < n; i++) r |= ((x >> i) & 1ull) << pos[i];
-    return r;
-}
-
-// masked increment of a deposited index: pdep(x + y, M) = ((pdep(x, M) | ~M) + pdep(y, M)) & M
-__device__ __forceinline__ uint64_t dep_add(uint64_t dx, uint64_t dy, uint64_t mask) { return ((dx | ~mask) + dy) & mask; }
-
-// The tile sequence every role of a CTA walks (identically): step s = pass A on chunk(s), then
-// pass B on chunk(s - depth); `depth` chunk-steps of other work between a chunk's pass A and its
-// pass B hide the pipeline latency and the group members' skew.  With BASE the walker also keeps
-// the deposited tile base incrementally (a few 64-bit ops per tile).
-template <bool BASE>
-struct TcSched {
-    const TcMulti* p;
-    uint64_t g, m, ngroups;
-    int s, ph, h;            // ph 0: pass A on chunk(s); ph 1: pass B on chunk(s - depth)
-    uint64_t u;
-    bool live;
-    uint64_t dW;             // deposit of 2u into the current pass's within-chunk positions
-    uint64_t dHa;            // deposit of chunk(s)
-    uint64_t dHb;            // deposit of chunk(s - depth) (valid once s >= depth)
-    uint64_t dH0;            // deposit of chunk(0) = g
-    __device__ uint64_t chunk_of(int ss) const { return g + (uint64_t)ss * ngroups; }
-    __device__ bool b_ok(int ss) const { return p->np == 2 && ss >= p->depth && chunk_of(ss - p->depth) < p->nchunks; }
-    __device__ bool phase_ok() const { return ph == 0 ? chunk_of(s) < p->nchunks : b_ok(s); }
-    __device__ void enter() {   // first pair of the member in the current phase
-        u = m;
-        if (BASE) dW = pdep_pos(2 * m, p->ps[ph].wpos, p->ps[ph].nw);
-    }
-    __device__ void normalize() {
-        while (live) {
-            if (u < p->npairs && phase_ok()) return;
-            if (p->np == 2 && ph == 0) {
-                ph = 1;
-            } else {
-                s++;
-                ph = 0;
-                if (BASE) {
-                    dHa = dep_add(dHa, p->hstep, p->hmask);
-                    if (s == p->depth) dHb = dH0;
-                    else if (s > p->depth) dHb = dep_add(dHb, p->hstep, p->hmask);
-                }
-            }
-            enter();
-            if (ph == 0 && chunk_of(s) >= p->nchunks && !b_ok(s) && !b_ok(s + 1)) live = false;
-        }
-    }
-    __device__ void begin(const TcMulti* pp, uint64_t gg, uint64_t mm, uint64_t ng) {
-        p = pp;
-        g = gg;
-        m = mm;
-        ngroups = ng;
-        s = 0;
-        ph = 0;
-        h = 0;
-        live = true;
-        if (BASE) {
-            dHa = dH0 = pdep_pos(g, p->hpos, p->nh);
-            dHb = p->depth == 0 ? dH0 : 0;
-        }
-        enter();
-        normalize();
-    }
-    __device__ void advance() {
-        h ^= 1;
-        if (h) return;
-        u += (uint64_t)p->gs;
-        if (BASE) dW = dep_add(dW, p->ps[ph].wstep, p->ps[ph].wmask);
-        normalize();
-    }
-    __device__ uint64_t chunk() const { return ph == 0 ? chunk_of(s) : chunk_of(s - p->depth); }
-    __device__ uint64_t base() const {
-        return dW | (h ? (1ull << p->ps[ph].r) : 0ull) | (ph == 0 ? dHa : dHb);
-    }
-    // the member's last tile of this pass-A phase (its A(chunk) is then complete)
-    __device__ bool last_of_phase() const { return h == 1 && u + (uint64_t)p->gs >= p->npairs; }
-};
-
-__global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc_multi(const __grid_constant__ TcMulti p) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    float2* raw = reinterpret_cast<float2*>(smem);
-    uint8_t* stages = smem + kRaw * kRawBytes;
-    float* staging = reinterpret_cast<float*>(stages + kStages * kStageBytes);
-    uint8_t* ctl = reinterpret_cast<uint8_t*>(staging) + kStagingBytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(ctl);   // [kStages]
-    uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;                    // [2]
-    uint64_t* tempty = tfull + 2;
-    uint64_t* rfull = tempty + 2;                         // [2] raw pair slots
-    uint64_t* rempty = rfull + 2;
-    uint64_t* offr = rempty + 2;                          // [2][64] run offsets per pass
-    uint16_t* soft = reinterpret_cast<uint16_t*>(offr + 128);   // [2][64]
-    uint16_t* sofj = soft + 128;                                 // [2][64]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sofj + 128);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; s++) {
-            mbar_init(&full[s], kLoadWarps * 32);
-            mbar_init(&empty[s], 1);
-        }
-        for (int d = 0; d < 2; d++) {
-            mbar_init(&tfull[d], 1);
-            mbar_init(&tempty[d], kEpiThreads);
-        }
-        for (int r = 0; r < 2; r++) {
-            mbar_init(&rfull[r], 1);
-            mbar_init(&rempty[r], 2 * kLoadWarps * 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;");
-    }
-    if (threadIdx.x < 64 * p.np) {
-        const int x = threadIdx.x & 63, P = threadIdx.x >> 6;
-        const TcPass& q = p.ps[P];
-        uint64_t orr = 0;
-        int st = 0, sj = 0;
-        for (int i = 0; i < 6; i++) {
-            int rt = 0, rj = 0;
-            for (int b = 0; b < 12; b++) {
-                rt += q.sub[b] < q.pos[i];
-                rj += q.sub[b] < q.jpos[i];
-            }
-            if ((x >> i) & 1) {
-                st |= 1 << rt;
-                sj |= 1 << rj;
-            }
-        }
-        for (int b = q.r; b < 12; b++)
-            if ((x >> (b - q.r)) & 1) orr |= 1ull << q.sub[b];
-        offr[64 * P + x] = orr;
-        const int lowm = (1 << q.r) - 1;
-        soft[64 * P + x] = (uint16_t)(((st & ~lowm) << 1) | (st & lowm));
-        sofj[64 * P + x] = (uint16_t)(((sj & ~lowm) << 1) | (sj & lowm));
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = *tmem_slot;
-    // TMEM: A of pass P at [128 P, 128 P + 128) (hi, lo); D[d] at 256 + 128 d (2 accumulators)
-    if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-        const int q = warp - kEpiWarp0;
-        const int m = q * 32 + lane;
-        for (int P = 0; P < p.np; P++)
-            for (int h = 0; h < 2; h++)
-                for (int c0 = 0; c0 < 64; c0 += 32) {
-                    uint32_t r[32];
-                    const uint4* src =
-                        reinterpret_cast<const uint4*>(p.ps[P].a + (size_t)h * 128 * 64 + (size_t)m * 64 + c0);
-#pragma unroll
-                    for (int c = 0; c < 8; c++) {
-                        const uint4 v = __ldg(src + c);
-                        r[4 * c] = v.x;
-                        r[4 * c + 1] = v.y;
-                        r[4 * c + 2] = v.z;
-                        r[4 * c + 3] = v.w;
-                    }
-                    TMEM_ST32(tmem + ((uint32_t)(q * 32) << 16) + 128 * P + h * 64 + c0, r);
-                }
-        asm volatile("tcgen05.wait::st.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-
-    const uint64_t ngroups = gridDim.x / (unsigned)p.gs;   // equal groups (host sizes the grid)
-    const uint64_t grp = blockIdx.x / (unsigned)p.gs, mem = blockIdx.x % (unsigned)p.gs;
-
-    if (warp == kProdWarp) {
-        // ---------------- TMA producer: both tiles of a pair
-        uint64_t pol_first;
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-        TcSched<true> sc;
-        sc.begin(&p, grp, mem, ngroups);
-        uint64_t it = 0;
-        int wait_s = -1;
-        for (; sc.live; sc.advance(), it++) {
-            if (sc.h) continue;   // odd half: copied with its pair
-            const int P = sc.ph;
-            if (P == 1 && sc.s != wait_s) {
-                // pass B reads pass A's output of this chunk: every member of the group must be done
-                wait_s = sc.s;
-                if (lane == 0) {
-                    const unsigned* cnt = p.done + sc.chunk();
-                    unsigned v;
-                    while (true) {
-                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-                        if (v >= (unsigned)p.gs) break;
-                        __nanosleep(128);
-                    }
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                }
-                __syncwarp();
-            }
-            const int slot = (it >> 1) & 1;
-            const uint64_t use = it >> 2;
-            mbar_wait(&rempty[slot], (use & 1) ^ 1);
-            if (lane == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[slot])),
-                             "r"(kRawBytes * 2)
-                             : "memory");
-            __syncwarp();
-            const int r = p.ps[P].r;
-            const int nruns = 1 << (12 - r);
-            const uint32_t copy_bytes = (8u << r) * 2u;
-            const float2* src = p.amps + sc.base();
-            const uint32_t dst = su32(raw + (size_t)slot * 8192);
-            for (int u = lane; u < nruns; u += 32)   // inputs are read once: L2 evict-first
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
-                    "[%3], %4;" ::"r"(dst + u * copy_bytes),
-                    "l"(src + offr[64 * P + u]), "r"(copy_bytes), "r"(su32(&rfull[slot])), "l"(pol_first)
-                    : "memory");
-        }
-    } else if (warp < kLoadWarps) {
-        // ---------------- converters: thread = column j, target octets `to` and `to + 4`
-        const int lt = threadIdx.x;
-        const int j = lt & 63;
-        const int to = lt >> 6;
-        int boff[2][16];   // raw-slot element offsets per pass (tile-invariant)
-        for (int P = 0; P < 2; P++) {
-            const int PP = P < p.np ? P : 0;
-            const int rho = p.ps[PP].rot ? (lane & 7) : 0;
-            const int sj = sofj[64 * PP + j];
-#pragma unroll
-            for (int i = 0; i < 16; i++) boff[P][i] = soft[64 * PP + 8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj;
-        }
-        TcSched<false> sc;
-        sc.begin(&p, grp, mem, ngroups);
-        uint64_t it = 0;
-        for (; sc.live; sc.advance(), it++) {
-            const int P = sc.ph;
-            const int slot = (it >> 1) & 1;
-            const uint64_t use = it >> 2;
-            mbar_wait(&rfull[slot], use & 1);
-            const float2* rb = raw + (size_t)slot * 8192 + (sc.h ? (1 << p.ps[P].r) : 0);
-            float2 b[16];
-            if (P == 0) {
-#pragma unroll
-                for (int i = 0; i < 16; i++) b[i] = f2mul(rb[boff[0][i]], 32768.f);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; i++) b[i] = f2mul(rb[boff[1][i]], 32768.f);
-            }
-            mbar_arrive(&rempty[slot]);
-            const int s = it % kStages;
-            mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
-            uint8_t* bhi = stages + s * kStageBytes;
-            uint8_t* blo = bhi + kBBytes;
-            const bool rot = p.ps[P].rot != 0;
-            const int rho = lane & 7;
-#pragma unroll
-            for (int g = 0; g < 2; g++) {
-                uint32_t rh[4], rl[4], ih[4], il[4];
-#pragma unroll
-                for (int e2 = 0; e2 < 4; e2++) {
-                    const float2 v0 = b[8 * g + 2 * e2], v1 = b[8 * g + 2 * e2 + 1];
-                    split_h2(v0.x, v1.x, rh[e2], rl[e2]);
-                    split_h2(v0.y, v1.y, ih[e2], il[e2]);
-                }
-                if (rot) {
-                    rot_h8(rh, rho);
-                    rot_h8(rl, rho);
-                    rot_h8(ih, rho);
-                    rot_h8(il, rho);
-                }
-                const int c = to + 4 * g;
-                const uint32_t ore = bchunk(j, c), oim = bchunk(j, c + 8);
-                *reinterpret_cast<uint4*>(bhi + ore) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
-                *reinterpret_cast<uint4*>(bhi + oim) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
-                *reinterpret_cast<uint4*>(blo + ore) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
-                *reinterpret_cast<uint4*>(blo + oim) = make_uint4(il[0], il[1], il[2], il[3]);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&full[s]);
-        }
-    } else if (warp == kMmaWarp) {
-        // ---------------- MMA issuer (2 accumulators: cross terms + hh k-steps 0-3, hh k-steps 4-7)
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-        TcSched<false> sc;
-        sc.begin(&p, grp, mem, ngroups);
-        uint64_t it = 0;
-        for (; sc.live; sc.advance(), it++) {
-            const int s = it % kStages, d = it & 1;
-            mbar_wait(&full[s], (it / kStages) & 1);
-            mbar_wait(&tempty[d], ((it >> 1) & 1) ^ 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            if (lane == 0) {
-                const uint32_t sb = su32(stages + s * kStageBytes);
-                const uint32_t d0 = tmem + 256 + d * 2 * TN;
-                const uint64_t bh0 = bdesc(sb), bl0 = bdesc(sb + kBBytes);
-                const uint32_t ah = tmem + 128 * sc.ph, al = ah + 64;
-                MMA_F16(d0, ah, bl0, idesc, 0);
-                MMA_F16(d0, al, bh0, idesc, 1);
-#pragma unroll
-                for (int ks = 1; ks < TK / 16; ks++) {
-                    MMA_F16(d0, ah + ks * 8, bl0 + ks * 16, idesc, 1);
-                    MMA_F16(d0, al + ks * 8, bh0 + ks * 16, idesc, 1);
-                }
-#pragma unroll
-                for (int ks = 0; ks < 4; ks++) MMA_F16(d0, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                MMA_F16(d0 + TN, ah + 4 * 8, bh0 + 4 * 16, idesc, 0);
-#pragma unroll
-                for (int ks = 5; ks < 8; ks++) MMA_F16(d0 + TN, ah + ks * 8, bh0 + ks * 16, idesc, 1);
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                    su32(&empty[s])));
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                    su32(&tfull[d])));
-            }
-            __syncwarp();
-        }
-    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
-        // ---------------- epilogue
-        const int q4 = warp & 3;
-        const int et = threadIdx.x - kEpiWarp0 * 32;
-        const int m = q4 * 32 + lane;
-        const int trow = m >> 1, comp = m & 1;
-        const float* sld[2];
-        uint64_t gb[2];
-        for (int P = 0; P < 2; P++) {   // sub-cube index et -> (t, j, global offset) per pass
-            const TcPass& q = p.ps[P < p.np ? P : 0];
-            int t = 0, jj = 0;
-            uint64_t go = 0;
-            for (int b = 0; b < 12; b++) {
-                if (!((et >> b) & 1)) continue;
-                go |= 1ull << q.sub[b];
-                for (int i = 0; i < 6; i++) {
-                    if (q.pos[i] == q.sub[b]) t |= 1 << i;
-                    if (q.jpos[i] == q.sub[b]) jj |= 1 << i;
-                }
-            }
-            sld[P] = staging + t * kPitchF + 2 * jj;
-            gb[P] = go;
-        }
-        float* st = staging + trow * kPitchF + comp;
-        uint64_t pol_last;
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
-        TcSched<true> sc;
-        sc.begin(&p, grp, mem, ngroups);
-        uint64_t it = 0;
-        for (; sc.live; sc.advance(), it++) {
-            const int d = it & 1;
-            const int P = sc.ph;
-            mbar_wait(&tfull[d], (it >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const float us = 1.f / (16384.f * 32768.f);
-            const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + 256 + d * 2 * TN;
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                uint32_t a0[32], a1[32];
-                TMEM_LD32(ta + 32 * h, a0);
-                TMEM_LD32(ta + TN + 32 * h, a1);
-                asm volatile("tcgen05.wait::ld.sync.aligned;");
-                if (h == 1) {
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    mbar_arrive(&tempty[d]);
-                }
-#pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                    float o0, o1;   // (acc0 + acc1) * 2^-29
-                    asm("{\n.reg .b64 x, y, u;\n"
-                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\n"
-                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\n"
-                        "mov.b64 {%0, %1}, x;\n}"
-                        : "=f"(o0), "=f"(o1)
-                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(us));
-                    st[2 * (32 * h + c)] = o0;
-                    st[2 * (32 * h + c) + 2] = o1;
-                }
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const uint64_t tb = sc.base();
-            if (P == 0) {
-                float2* dst = p.amps + (tb | gb[0]);
-                if (p.np == 2) {   // re-read by pass B from L2: keep (evict-last)
-#pragma unroll 8
-                    for (int i = 0; i < 32; i++) {
-                        const float2 v = *reinterpret_cast<const float2*>(sld[0] + p.ps[0].sso[i]);
-                        asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(dst + p.ps[0].sgo[i]),
-                                     "f"(v.x), "f"(v.y), "l"(pol_last)
-                                     : "memory");
-                    }
-                } else {
-#pragma unroll 8
-                    for (int i = 0; i < 32; i++)
-                        __stcs(dst + p.ps[0].sgo[i], *reinterpret_cast<const float2*>(sld[0] + p.ps[0].sso[i]));
-                }
-            } else {
-                float2* dst = p.amps + (tb | gb[1]);
-#pragma unroll 8
-                for (int i = 0; i < 32; i++)
-                    __stcs(dst + p.ps[1].sgo[i], *reinterpret_cast<const float2*>(sld[1] + p.ps[1].sso[i]));
-            }
-            if (p.np == 2 && P == 0 && sc.last_of_phase()) {
-                // this CTA's last pass-A tile of the chunk: publish after all epilogue stores (the
-                // named barrier orders them before thread 0's gpu-scope release)
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (et == 0) {
-                    unsigned* cnt = p.done + sc.chunk();
-                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-                }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");   // staging reused by the next tile
         }
@@ -1010,7 +575,8 @@ struct TcTArgs {
 
 constexpr uint32_t kTRaw = 8192 * 8;                  // one tile: 64 KB
 constexpr uint32_t kTMat = 2 * 128 * 128 * 2;         // B hi + lo: 64 KB
-constexpr uint32_t kTCtl = 1024;
+constexpr uint32_t kTCtl = 3072;
+static_assert((10 + kExpSlots) * 8 + 64 * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl, "K12 control block");
 constexpr uint32_t kTSmem = 2 * kTRaw + kTMat + kTCtl;
 
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constant__ TcTArgs p) {
@@ -1024,8 +590,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     uint64_t* aempty = afull + 2;                         // [2]
     uint64_t* dfull = aempty + 2;                         // [1]
     uint64_t* dempty = dfull + 1;                         // [1]
-    uint64_t* offt = dempty + 1;                          // [64] target-combination offsets
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(offt + 64);
+    uint64_t* cready = dempty + 1;                        // [kExpSlots] column exponents of a tile written
+    uint64_t* offt = cready + kExpSlots;                  // [64] target-combination offsets
+    int* cmax = reinterpret_cast<int*>(offt + 64);        // [3][128] column max |x| (float bits)
+    float* rowfac = reinterpret_cast<float*>(cmax + 3 * 128);   // [64] 2^-F_t
+    int8_t* colexp = reinterpret_cast<int8_t*>(rowfac + 64);     // [kExpSlots][128] E_j per tile
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colexp + kExpSlots * 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) {
@@ -1041,13 +611,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         }
         mbar_init(dfull, 1);
         mbar_init(dempty, kEpiThreads);
+        for (int e = 0; e < kExpSlots; e++) mbar_init(&cready[e], 128);   // the 128 column owners (th == 0)
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
+    for (int i = threadIdx.x; i < 3 * 128; i += blockDim.x) cmax[i] = 0;
     if (threadIdx.x < 64) {
         uint64_t ot = 0;
         for (int i = 0; i < 6; i++)
             if ((threadIdx.x >> i) & 1) ot |= 1ull << p.pos[i];
         offt[threadIdx.x] = ot;
+        rowfac[threadIdx.x] = pow2f(-(int)p.a[2 * 128 * 64 + threadIdx.x]);
     }
     // the matrix as the K-major shared-memory operand: core chunk (n, c) = A_K9 words [n][4c..4c+3]
     for (int e = threadIdx.x; e < 2 * 128 * 16; e += blockDim.x) {
@@ -1098,19 +671,37 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++) {
             const int slot = it & 1, b = it & 1;
             mbar_wait(&rfull[slot], (it >> 1) & 1);
+            const float2* rb = raw + (size_t)slot * 8192 + j;
+            float2 v[32];
+            float mx = 0.f;
+#pragma unroll
+            for (int u = 0; u < 32; u++) {
+                v[u] = rb[(size_t)(32 * th + u) * 128];
+                mx = absmax2(mx, v[u]);
+            }
+            mbar_arrive(&rempty[slot]);
+            // column max over the two threads of column j (warps q and q + 4), as K9
+            const int cb = (int)(it % 3);
+            atomicMax(&cmax[cb * 128 + j], __float_as_int(mx));
+            asm volatile("bar.sync 2, 256;" ::: "memory");
+            const int E = col_exponent(cmax[cb * 128 + j]);
+            const int es = (int)(it % kExpSlots);
+            if (th == 0) {
+                cmax[((it + 2) % 3) * 128 + j] = 0;
+                colexp[es * 128 + j] = (int8_t)E;
+                mbar_arrive(&cready[es]);
+            }
+            const float sc = pow2f(E);
             mbar_wait(&aempty[b], ((it >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            const float2* rb = raw + (size_t)slot * 8192 + j;
             // K order t + 64 c: word c < 32 packs re of t = 2c, 2c+1; word 32 + c the im parts
             uint32_t hre[16], lre[16], him[16], lim[16];
 #pragma unroll
             for (int u = 0; u < 16; u++) {
-                const int t = 32 * th + 2 * u;
-                const float2 v0 = f2mul(rb[(size_t)t * 128], 32768.f), v1 = f2mul(rb[(size_t)(t + 1) * 128], 32768.f);
-                split_h2(v0.x, v1.x, hre[u], lre[u]);
-                split_h2(v0.y, v1.y, him[u], lim[u]);
+                const float2 v0 = f2mul(v[2 * u], sc), v1 = f2mul(v[2 * u + 1], sc);
+                split_exact_h2(v0.x, v1.x, hre[u], lre[u]);
+                split_exact_h2(v0.y, v1.y, him[u], lim[u]);
             }
-            mbar_arrive(&rempty[slot]);
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 128 * b + 16 * th;
             TMEM_ST16(ta, hre);             // hi, re words [16 th, +16)
             TMEM_ST16(ta + 32, him);        // hi, im words [32 + 16 th, +16)
@@ -1133,7 +724,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             if (lane == 0) {
                 const uint32_t d0 = tmem + 256;
                 const uint32_t xh = tmem + 128 * b, xl = xh + 64;   // state hi / lo (A)
-                // cross terms first (x_hi u_lo, x_lo u_hi), then x_hi u_hi: k-steps 0-3 -> acc 0, 4-7 -> acc 1
+                // cross terms (x_hi u_lo, x_lo u_hi) -> acc 0; main x_hi u_hi (exact) -> acc 1
                 MMA_F16(d0, xh, bl0, idesc, 0);
                 MMA_F16(d0, xl, bh0, idesc, 1);
 #pragma unroll
@@ -1141,11 +732,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                     MMA_F16(d0, xh + ks * 8, bl0 + ks * 16, idesc, 1);
                     MMA_F16(d0, xl + ks * 8, bh0 + ks * 16, idesc, 1);
                 }
+                MMA_F16(d0 + 128, xh, bh0, idesc, 0);
 #pragma unroll
-                for (int ks = 0; ks < 4; ks++) MMA_F16(d0, xh + ks * 8, bh0 + ks * 16, idesc, 1);
-                MMA_F16(d0 + 128, xh + 4 * 8, bh0 + 4 * 16, idesc, 0);
-#pragma unroll
-                for (int ks = 5; ks < 8; ks++) MMA_F16(d0 + 128, xh + ks * 8, bh0 + ks * 16, idesc, 1);
+                for (int ks = 1; ks < 8; ks++) MMA_F16(d0 + 128, xh + ks * 8, bh0 + ks * 16, idesc, 1);
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                     su32(&aempty[b])));
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -1157,9 +746,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         // ---------------- epilogue: lane quarter q holds columns j = 32 q + lane
         const int q = warp & 3;
         const int j = 32 * q + lane;
-        const float us = 1.f / (16384.f * 32768.f);
         uint64_t it = 0, bp = tile_base(first);
         for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
+            const int es = (int)(it % kExpSlots);
+            mbar_wait(&cready[es], (uint32_t)((it / kExpSlots) & 1));
+            const float cf = pow2f(-(int)colexp[es * 128 + j]);   // 2^-E_j (read before releasing D)
             mbar_wait(dfull, it & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             float2* dst = p.amps + (bp | p.fixval) + j;
@@ -1176,13 +767,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                 }
 #pragma unroll
                 for (int c = 0; c < 32; c += 2) {
-                    float o0, o1;   // (acc0 + acc1) * 2^-29 of (re, im) of t = 16 s4 + c / 2
-                    asm("{\n.reg .b64 x, y, u;\n"
-                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\n"
-                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\n"
+                    const float rf = rowfac[16 * s4 + c / 2];
+                    float o0, o1;   // ((cross + main) 2^-E_j) 2^-F_t of (re, im) of t = 16 s4 + c / 2
+                    asm("{\n.reg .b64 x, y, u, v;\n"
+                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\nmov.b64 v, {%7, %7};\n"
+                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\nmul.rn.f32x2 x, x, v;\n"
                         "mov.b64 {%0, %1}, x;\n}"
                         : "=f"(o0), "=f"(o1)
-                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(us));
+                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(cf), "f"(rf));
                     __stcs(dst + offt[16 * s4 + c / 2], make_float2(o0, o1));
                 }
             }
@@ -1196,34 +788,39 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
 
 }  // namespace
 
-size_t tc_matrix_words() { return 2 * 128 * 64; }
+size_t tc_matrix_words() { return 2 * 128 * 64 + 64; }
 
-// A = [[U_re, -U_im], [U_im, U_re]] (rows interleaved), scaled by 2^14 and split into fp16
-// hi = fp16(2^14 A), lo = fp16(2^14 A - hi) computed from the fp64 product; packed 2 per word
-// (k even in the low half), [hi rows 0..127][lo rows 0..127], 64 words per row.
+// A = [[U_re, -U_im], [U_im, U_re]] (rows interleaved: 2t = re, 2t+1 = im of output t).  Row
+// pair t is scaled by 2^F_t, F_t = 10 - floor(log2 max_c |A[2t][c]|) (both rows hold the same
+// magnitudes), so its entries lie below 2^11, and split into hi = rint(2^F_t A) -- an integer,
+// exact in fp16 -- and lo = fp16(2^F_t A - hi), both from the fp64 product.  Packed 2 per word
+// (k even in the low half): [hi rows 0..127][lo rows 0..127], 64 words per row, then F_t (64
+// words, int).  The kernels unscale by 2^-F_t in the epilogue.
 void tc_pack_matrix(const double* u_re_im /* 64x64 complex, row-major interleaved */, uint32_t* out) {
-    auto split = [](double x, uint16_t* h, uint16_t* l) {
-        const double xs = x * 16384.0;
-        const __half hh = __float2half_rn((float)xs);
-        const __half ll = __float2half_rn((float)(xs - (double)__half2float(hh)));
-        *h = __half_as_ushort(hh);
-        *l = __half_as_ushort(ll);
+    auto entry = [&](int m, int kk) {
+        const int t = m >> 1, col = kk & 63;
+        const double ur = u_re_im[2 * (t * 64 + col)], ui = u_re_im[2 * (t * 64 + col) + 1];
+        if (!(m & 1)) return kk < 64 ? ur : -ui;   // row 2t:   [U_re | -U_im]
+        return kk < 64 ? ui : ur;                  // row 2t+1: [U_im |  U_re]
     };
-    for (int m = 0; m < 128; m++) {
-        const int t = m >> 1, im_row = m & 1;
-        for (int k = 0; k < 128; k += 2) {
-            uint16_t h[2], l[2];
-            for (int u = 0; u < 2; u++) {
-                const int kk = k + u;
-                const int col = kk & 63;
-                const double ur = u_re_im[2 * (t * 64 + col)], ui = u_re_im[2 * (t * 64 + col) + 1];
-                double v;
-                if (!im_row) v = kk < 64 ? ur : -ui;   // row 2t:   [U_re | -U_im]
-                else v = kk < 64 ? ui : ur;            // row 2t+1: [U_im |  U_re]
-                split(v, &h[u], &l[u]);
+    for (int t = 0; t < 64; t++) {
+        double mx = 0.0;
+        for (int kk = 0; kk < 128; kk++) mx = std::fmax(mx, std::fabs(entry(2 * t, kk)));
+        const int F = mx > 0.0 ? 10 - std::ilogb(mx) : 0;
+        out[(size_t)2 * 128 * 64 + t] = (uint32_t)F;
+        for (int r = 0; r < 2; r++) {
+            const int m = 2 * t + r;
+            for (int k = 0; k < 128; k += 2) {
+                uint16_t h[2], l[2];
+                for (int u = 0; u < 2; u++) {
+                    const double xs = std::ldexp(entry(m, k + u), F);
+                    const double hi = std::nearbyint(xs);   // |hi| <= 2^11: exact in fp16
+                    h[u] = __half_as_ushort(__float2half_rn((float)hi));
+                    l[u] = __half_as_ushort(__double2half(xs - hi));
+                }
+                out[(size_t)m * 64 + k / 2] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+                out[(size_t)128 * 64 + (size_t)m * 64 + k / 2] = (uint32_t)l[0] | ((uint32_t)l[1] << 16);
             }
-            out[(size_t)m * 64 + k / 2] = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
-            out[(size_t)128 * 64 + (size_t)m * 64 + k / 2] = (uint32_t)l[0] | ((uint32_t)l[1] << 16);
         }
     }
 }
@@ -1276,25 +873,25 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
             v >>= 1;
         }
     p.dstride = d;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass_tct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    // the attribute is per device (context): set it before every launch (cheap)
+    cudaError_t e = cudaFuncSetAttribute(k_pass_tct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+    if (e != cudaSuccess) return e;
     count_launch();
     k_pass_tct<<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
     return cudaGetLastError();
 }
 
+bool tc_uses_k12(const int* pos) {
+    for (int i = 0; i < 6; i++)
+        if (pos[i] < 7) return false;
+    return true;
+}
+
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
-                         const int* fix, int nfix, uint64_t fixval) {
-    {   // K12 when no target sits in positions 0..6 (read per launch: tests toggle RCS_TC_NOTRANS)
-        bool low = false;
-        for (int i = 0; i < 6; i++) low = low || pos[i] < 7;
-        if (!low && nl >= 13 + nfix && !getenv("RCS_TC_NOTRANS"))
-            return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval);
-    }
+                         const int* fix, int nfix, uint64_t fixval, bool force_k9) {
+    // K12 iff no target sits in positions 0..6: a function of the block alone, so the kernel
+    // (and its rounding) never depends on the sharding or on chunking (force_k9: tests only)
+    if (!force_k9 && tc_uses_k12(pos)) return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval);
     if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
     p.amps = amps;
@@ -1334,8 +931,6 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
     for (int b = 0; b < nl; b++)
         if ((insmask >> b) & 1) p.ins[p.nins++] = b;
     p.pair = p.ntiles >= 2 ? 2 : 1;                // tile bit 0 = index bit r (first non-cube bit)
-    static const bool no_pair = getenv("RCS_TC_NOPAIR") != nullptr, no_rot = getenv("RCS_TC_NOROT") != nullptr;
-    if (no_pair) p.pair = 1;
     for (int i = 0; i < 32; i++) {                 // epilogue store offsets of sub-cube index 128 i
         const int sidx = 128 * i;
         int t = 0, jj = 0;
@@ -1350,14 +945,6 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
         }
         p.sso[i] = t * kPitchF + 2 * jj;
         p.sgo[i] = go;
-    }
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_pass_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr = true;
     }
     // bank conflicts of the converters' reads: target bits among the 4 lowest sub-cube bits
     int low_targets = 0;
@@ -1375,148 +962,18 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
             }
         p.dstride = d;
     }
+    const bool rot = low_targets >= 2;
+    cudaError_t e = rot ? cudaFuncSetAttribute(k_pass_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)
+                        : cudaFuncSetAttribute(k_pass_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e != cudaSuccess) return e;
     count_launch();
-    if (low_targets >= 2 && !no_rot)
+    if (rot)
         k_pass_tc<true><<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
     else
         k_pass_tc<false><<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(p);
     return cudaGetLastError();
 }
 
-
-namespace {
-// per-pass tables of K11 (same derivation as gate_pass_tc)
-bool fill_pass(TcPass& q, int nl, const int* pos, const uint32_t* d_a, uint64_t* submask) {
-    q = TcPass{};
-    q.a = d_a;
-    uint64_t tmask = 0;
-    for (int i = 0; i < 6; i++) {
-        q.pos[i] = pos[i];
-        tmask |= 1ull << pos[i];
-    }
-    int nj = 0;
-    for (int b = 0; b < nl && nj < 6; b++)
-        if (!((tmask >> b) & 1)) q.jpos[nj++] = b;
-    if (nj != 6) return false;
-    int na = 0;
-    uint64_t sm = 0;
-    for (int b = 0; b < nl && na < 12; b++) {
-        bool in = (tmask >> b) & 1;
-        for (int i = 0; i < 6; i++) in = in || q.jpos[i] == b;
-        if (in) {
-            q.sub[na++] = b;
-            sm |= 1ull << b;
-        }
-    }
-    if (na != 12) return false;
-    q.r = 0;
-    while (q.r < 12 && q.sub[q.r] == q.r) q.r++;
-    if (q.r >= nl) return false;
-    for (int i = 0; i < 32; i++) {
-        const int sidx = 128 * i;
-        int t = 0, jj = 0;
-        uint64_t go = 0;
-        for (int b = 0; b < 12; b++) {
-            if (!((sidx >> b) & 1)) continue;
-            go |= 1ull << q.sub[b];
-            for (int k = 0; k < 6; k++) {
-                if (q.pos[k] == q.sub[b]) t |= 1 << k;
-                if (q.jpos[k] == q.sub[b]) jj |= 1 << k;
-            }
-        }
-        q.sso[i] = t * kPitchF + 2 * jj;
-        q.sgo[i] = go;
-    }
-    int low_targets = 0;
-    for (int i = 0; i < 4; i++) low_targets += (int)((tmask >> q.sub[i]) & 1);
-    q.rot = low_targets >= 2 ? 1 : 0;
-    *submask = sm;
-    return true;
-}
-}  // namespace
-
-int tc_multi_chunk_bits(int nl, int np, const int* const* pos) {
-    uint64_t c = 0;
-    for (int P = 0; P < np; P++) {
-        TcPass q;
-        uint64_t sm;
-        if (!fill_pass(q, nl, pos[P], nullptr, &sm)) return -1;
-        c |= sm | (1ull << q.r);
-    }
-    return __builtin_popcountll(c);
-}
-
-cudaError_t gate_pass_tc_multi(float2* amps, int nl, int np, const int* const* pos, const uint32_t* const* d_a,
-                               int num_sms, unsigned* done, uint64_t done_cap, cudaStream_t st) {
-    if (np < 1 || np > 2 || nl < 13) return cudaErrorInvalidValue;
-    TcMulti m{};
-    m.amps = amps;
-    m.np = np;
-    uint64_t cmask = 0, sub[2] = {0, 0};
-    for (int P = 0; P < np; P++) {
-        if (!fill_pass(m.ps[P], nl, pos[P], d_a[P], &sub[P])) return cudaErrorInvalidValue;
-        cmask |= sub[P] | (1ull << m.ps[P].r);
-    }
-    const int nc = __builtin_popcountll(cmask);
-    for (int P = 0; P < np; P++) {
-        TcPass& q = m.ps[P];
-        q.nw = 0;
-        for (int b = 0; b < nl; b++)
-            if (((cmask >> b) & 1) && !((sub[P] >> b) & 1)) q.wpos[q.nw++] = b;
-        if (q.nw != nc - 12 || q.wpos[0] != q.r || q.nw > 12) return cudaErrorInvalidValue;
-    }
-    m.nh = 0;
-    for (int b = 0; b < nl; b++)
-        if (!((cmask >> b) & 1)) m.hpos[m.nh++] = b;
-    m.nchunks = 1ull << m.nh;
-    m.npairs = 1ull << (nc - 13);
-    uint64_t grid = (uint64_t)num_sms;
-    if (np == 1) {
-        m.gs = 1;
-        if (grid > m.nchunks * m.npairs) grid = m.nchunks * m.npairs;
-    } else {
-        // depth chunk-steps of slack, each member holding ~kSlackTiles tiles of other work
-        // between a chunk's pass A and pass B; in flight: ngroups x (depth + 1) chunks
-        const int depth_env = getenv("RCS_PAIR_DEPTH") ? atoi(getenv("RCS_PAIR_DEPTH")) : 2;
-        const int slack_env = getenv("RCS_PAIR_SLACK") ? atoi(getenv("RCS_PAIR_SLACK")) : 16;
-        const uint64_t chunk_tiles = 2 * m.npairs;
-        m.depth = depth_env < 1 ? 1 : depth_env;
-        const uint64_t want = (chunk_tiles * (uint64_t)m.depth + slack_env - 1) / (uint64_t)slack_env;
-        uint64_t gs = 1;   // power of two <= npairs: every member gets the same number of pairs
-        while (gs * 2 <= want && gs * 2 <= m.npairs && gs * 2 <= grid) gs *= 2;
-        m.gs = (int)gs;
-        grid = grid / gs * gs;   // equal groups (a few SMs idle rather than one slow group)
-        if (!done || done_cap < m.nchunks) return cudaErrorInvalidValue;
-        m.done = done;
-        cudaError_t e = cudaMemsetAsync(done, 0, m.nchunks * sizeof(unsigned), st);
-        if (e != cudaSuccess) return e;
-    }
-    // incremental deposits: a member's pair stride 2 gs inside a chunk, a group's chunk stride
-    auto pdep_host = [](uint64_t x, const int* pos, int n) {
-        uint64_t r = 0;
-        for (int i = 0; i < n; i++) r |= ((x >> i) & 1ull) << pos[i];
-        return r;
-    };
-    const uint64_t ngroups = grid / (uint64_t)m.gs;
-    m.hmask = 0;
-    for (int i = 0; i < m.nh; i++) m.hmask |= 1ull << m.hpos[i];
-    m.hstep = pdep_host(ngroups, m.hpos, m.nh);
-    for (int P = 0; P < np; P++) {
-        TcPass& q = m.ps[P];
-        q.wmask = 0;
-        for (int i = 0; i < q.nw; i++) q.wmask |= 1ull << q.wpos[i];
-        q.wstep = pdep_host(2ull * (uint64_t)m.gs, q.wpos, q.nw);
-    }
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass_tc_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    count_launch();
-    k_pass_tc_multi<<<(unsigned)grid, kThreadsTC, kSmemBytes, st>>>(m);
-    return cudaGetLastError();
-}
 
 }  // namespace dev
 }  // namespace rcs

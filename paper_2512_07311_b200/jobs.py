@@ -105,6 +105,9 @@ def run_pipeline(qasm: str, total_shots: int, n_jobs: int, base_seed: int, work_
     """Stages 1-4 locally: build on `device`, snapshot, fan out n_jobs worker processes
     (`parallel` at a time, each on `device`), aggregate the result files."""
     from . import Circuit, Context, State, shard_shots
+    if n_jobs < 1 or total_shots < n_jobs:
+        raise ValueError(f"need 1 <= n_jobs <= total_shots (got n_jobs={n_jobs}, total_shots={total_shots}): "
+                         "every job draws at least one shot")
     os.makedirs(work_dir, exist_ok=True)
     t0 = time.perf_counter()
     ctx = Context(device)
@@ -117,20 +120,32 @@ def run_pipeline(qasm: str, total_shots: int, n_jobs: int, base_seed: int, work_
     shards = shard_shots(total_shots, n_jobs)
     procs, paths, pending = [], [], list(enumerate(shards))
     env = dict(os.environ)
-    while pending or procs:
-        while pending and len(procs) < max(1, parallel):
-            j, sh = pending.pop(0)
-            cmd = [sys.executable, "-m", "paper_2512_07311_b200.jobs", "worker", "--snapshot", snap, "--shots",
-                   str(sh), "--seed", str(base_seed), "--job-id", str(j), "--out", work_dir, "--device", str(device),
-                   "--queue-s", f"{time.perf_counter() - t1:.6f}"]
-            procs.append((j, subprocess.Popen(cmd, env=env)))
-            paths.append(os.path.join(work_dir, f"result_{j}.jsonl"))
-        for j, pr in list(procs):
-            if pr.poll() is not None:
-                if pr.returncode != 0:
-                    raise RuntimeError(f"job {j} failed with exit code {pr.returncode}")
-                procs.remove((j, pr))
-        time.sleep(0.02)
+    try:
+        while pending or procs:
+            while pending and len(procs) < max(1, parallel):
+                j, sh = pending.pop(0)
+                cmd = [sys.executable, "-m", "paper_2512_07311_b200.jobs", "worker", "--snapshot", snap, "--shots",
+                       str(sh), "--seed", str(base_seed), "--job-id", str(j), "--out", work_dir, "--device",
+                       str(device), "--queue-s", f"{time.perf_counter() - t1:.6f}"]
+                procs.append((j, subprocess.Popen(cmd, env=env)))
+                paths.append(os.path.join(work_dir, f"result_{j}.jsonl"))
+            for j, pr in list(procs):
+                if pr.poll() is not None:
+                    if pr.returncode != 0:
+                        raise RuntimeError(f"job {j} failed with exit code {pr.returncode}")
+                    procs.remove((j, pr))
+            time.sleep(0.02)
+    except BaseException:
+        for _, pr in procs:   # no orphaned GPU workers: stop and reap the jobs still running
+            if pr.poll() is None:
+                pr.terminate()
+        for _, pr in procs:
+            try:
+                pr.wait(timeout=30)
+            except subprocess.TimeoutExpired:
+                pr.kill()
+                pr.wait()
+        raise
     t2 = time.perf_counter()
     out = aggregate(paths)
     out.update({"snapshot": snap, "snapshot_digest": digest.hex(), "stage1_s": t1 - t0, "stage3_s": t2 - t1})

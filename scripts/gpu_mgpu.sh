@@ -13,8 +13,8 @@ for M in $N $((N/2)); do
   CUDA_VISIBLE_DEVICES=$DEV timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $M \
       --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus $M --steps 3 --warmup 3 \
       > $OUT/bench_c4_N$M.json 2> $OUT/bench_c4_N$M.err; echo "rc=$?" >> $OUT/bench_c4_N$M.err
-  CUDA_VISIBLE_DEVICES=$DEV RCS_OVERLAP=0 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $M \
-      --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus $M --steps 3 --warmup 3 \
+  CUDA_VISIBLE_DEVICES=$DEV timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $M \
+      --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus $M --steps 3 --warmup 3 --no-overlap \
       > $OUT/bench_c4_N${M}_seq.json 2> $OUT/bench_c4_N${M}_seq.err; echo "rc=$?" >> $OUT/bench_c4_N${M}_seq.err
 done
 echo done > $OUT/done

@@ -1,6 +1,6 @@
 """Sustained-load probe: HBM rate, SM clock and board power for
   copy   : torch in-place x.mul_(1) over a 64 GiB complex64 buffer (read+write, the pass's traffic)
-  pass   : the library's C4 build (40 tensor-core passes) with RCS_TC_EXPERIMENT=0/1/2 set by the caller
+  pass   : the library's C4 build (36 tensor-core passes)
 Each experiment runs ~3 s; nvidia-smi is sampled every 100 ms meanwhile.
 usage: python scripts/power_probe.py copy|pass
 """
@@ -67,7 +67,7 @@ def main():
             allg += [16 * (1 << 34) / (m / 1e3) / 1e9 for m in st.pass_times()]
             st.free()
         sm, pw, tp = stop(p, f)
-        print(f"pass exp={os.environ.get('RCS_TC_EXPERIMENT', '0')}: GB/s first10 {statistics.median(allg[:10]):.0f}"
+        print(f"pass: GB/s first10 {statistics.median(allg[:10]):.0f}"
               f" median {statistics.median(allg):.0f} last20 {statistics.median(allg[-20:]):.0f}"
               f" | sm MHz median {statistics.median(sm):.0f} min {min(sm):.0f} | W max {max(pw):.0f} median"
               f" {statistics.median(pw):.0f} | temp {max(tp):.0f}")

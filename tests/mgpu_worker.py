@@ -26,12 +26,13 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = rcs.Context.from_process_group(local)
     results = {}
+    opts = json.loads(os.environ.get("MGPU_OPTS", "{}"))
     from tests.test_multigpu import CASES
     for name, (text, k) in CASES.items():
         c = rcs.Circuit.from_qasm(text)
         n = c.n_qubits
         keep = name.endswith("_keep")
-        st = rcs.State.build(ctx, c, fuse_k=k, timing=True, staging_bytes=1 << 20, keep_layout=keep)
+        st = rcs.State.build(ctx, c, fuse_k=k, timing=True, staging_bytes=1 << 20, keep_layout=keep, **opts)
         report = dict(st.report)
         x = st.sample(20000, seed=SHOT_SEED)
         xr = st.xeb(x)

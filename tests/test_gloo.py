@@ -1,4 +1,4 @@
-"""World-size-2 (and 4) gloo tests of the N>1 host logic on CPU.
+"""World-size-2, 4 and 8 gloo tests of the N>1 host logic on CPU.
 
 Each process holds one shard (top log2(P) qubits global) and executes the library's plan
 (rcs_plan_create with n_global = log2 P): passes on local bits, REMAP items as a real
@@ -103,17 +103,19 @@ def run_rank(rank, world, port, text, g, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,case", [(2, "c1"), (2, "grid"), (4, "grid")])
+@pytest.mark.parametrize("world,case", [(2, "c1"), (2, "grid"), (4, "grid"), (8, "grid16")])
 def test_sharded_plan_over_gloo(world, case):
     import oracle
     from rcs_workload import config_qasm, emit_qasm, generate
     from paper_2512_07311_b200 import build
     build.build()
-    text = config_qasm("c1") if case == "c1" else emit_qasm(generate(3, 5, 14, "ABCDCDAB", seed=7))
+    text = {"c1": config_qasm("c1"), "grid": emit_qasm(generate(3, 5, 14, "ABCDCDAB", seed=7)),
+            # world 8: g = 3 global qubits (7 peers per rank, j = 3 remaps), 4x4 grid
+            "grid16": emit_qasm(generate(4, 4, 14, "ABCDCDAB", seed=9))}[case]
     g = world.bit_length() - 1
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + world + (7 if case == "grid" else 0)
+    port = 29600 + world + (7 if case != "c1" else 0)
     procs = [ctx.Process(target=run_rank, args=(r, world, port, text, g, q)) for r in range(world)]
     for p in procs:
         p.start()
