@@ -135,6 +135,27 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def host_info():
+    """Host the oracle baseline runs on (nproc, CPU model/sockets, memory)."""
+    info = {"nproc": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal:"):
+                    info["mem_total_gib"] = round(int(ln.split()[1]) / 2 ** 20, 1)
+    except Exception:
+        pass
+    return info
+
+
 def ncu_traffic(config, world):
     """Per-launch DRAM bytes of the gate-pass kernel from a committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -185,9 +206,13 @@ def oracle_sample(cfg_name: str, cfg: dict, shots: int, budget_s: float, n_small
     n_full = cfg["n_qubits"]
     scale = 2.0 ** (n_full - n_small)
     proj = max(t_build - fixed, 1e-9) / G * full_gates * scale + t_samp * scale
+    host = host_info()
+    need_gib = 16 * 2 ** n_full / 2 ** 30
     desc = (f"oracle fp64, first {G} of {len(circ.gates)} gates of the {cfg_name} circuit at n={n_small} "
             f"({t_build:.2f} s) + sample/XEB of {S} shots ({t_samp:.2f} s); projected linearly in 2^n*gates "
-            f"to n={n_full}, {full_gates} gates, {shots} shots: {proj:.1f} s")
+            f"to n={n_full}, {full_gates} gates, {shots} shots: {proj:.1f} s (projected, not run in full: the "
+            f"fp64 state needs {need_gib:.0f} GiB, host RAM {host.get('mem_total_gib', '?')} GiB, and a full run "
+            f"takes ~{proj / 60:.0f} min)")
     return proj, desc, oracle.num_threads(), t_build + t_samp
 
 
@@ -310,19 +335,30 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             proj, sdesc, cores, spent = oracle_sample(args.config, cfg, shots, args.cpu_budget)
             cpu = {"value": total_pass_bytes / args.steps / proj / 1e9, "unit": "GB/s", "cores": cores,
-                   "kind": "oracle", "sample": sdesc, "projected_step_s": proj, "cpu_seconds_spent": spent}
+                   "kind": "oracle", "sample": sdesc, "projected": True, "projected_step_s": proj,
+                   "cpu_seconds_spent": spent, "host": host_info()}
         X = xebs[-1]
         out = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "dtype_note": "complex64 state, f32 FMA; fp64 block CDF, search and XEB",
+            "dtype_note": ("complex64 state; 6-qubit passes on tcgen05 kind::f16 with an fp16 hi/lo split "
+                           "(hi = integer-valued, per-row/per-column power-of-two scales): exact integer main "
+                           "term + rounded cross terms, fp32 TMEM accumulation, fp32 epilogue; fp64 block CDF, "
+                           "search and XEB"),
             "data": "synthetic: seeded Sycamore-style circuit (rcs_workload, seed 1), shot seed 2512",
             "config": {"workload": desc, "n_qubits": n, "cycles": cfg["cycles"], "pattern": cfg["pattern"],
                        "shots": shots, "fuse_k": R["fuse_k"],
                        "parallelism": (f"state sharded over top {g} qubit(s), remaps = in-place NVLink peer swaps "
                                                "pipelined with the neighbouring passes") if world > 1 else "1 GPU",
-                       "l2": "no flush: state (%d GiB per GPU) >> 126 MB L2" % ((8 << (n - g)) >> 30)},
+                       "l2": "no flush: state (%d GiB per GPU) >> 126 MB L2" % ((8 << (n - g)) >> 30),
+                       "sampler": ("kept layout (no final restore): every rank all-gathers the physical block "
+                                   "sums and scans the logical-order CDF of the whole state (2^(n-6) doubles, "
+                                   "replicated); north_star's per-rank partial CDF + scan of shard totals is the "
+                                   "--canonical path. Same picks at N=1; at N>1 the scan association differs "
+                                   "(G17 band)") if keep and world > 1 else
+                                  ("canonical layout: per-rank block CDF + exclusive scan of shard totals"
+                                   if world > 1 else "block CDF (b=6) + per-shot search")},
             "build_s": statistics.median(r["build_ms"] for r in reports) / 1e3,
             "shots_per_s": shots / (statistics.median(sample_ms) / 1e3),
             "shots_per_s_incl_blocksum": shots / ((statistics.median(sample_ms) + R["blocksum_ms"]) / 1e3),
@@ -332,10 +368,19 @@ def run_ours(args):
             "pass_gbs": {"min": gbs[0], "median": gbs[len(gbs) // 2], "max": gbs[-1]},
             "pass_ms_total": R["pass_ms"], "remap_ms_total": R["remap_ms"], "swap_ms_total": R["swap_ms"],
             "blocksum_ms": R["blocksum_ms"], "n_tc_passes": R["n_tc_passes"],
-            "remap_gbs": (R["remap_bytes"] / (R["remap_ms"] / 1e3) / 1e9) if R["remap_ms"] > 0 else None,
-            "remap_note": "remap_ms_total = exposed remap time (not overlapped with pass chunks)",
+            "remap": {"bytes_per_rank": R["remap_bytes"], "exposed_ms": R["remap_ms"],
+                      "kernel_ms": R["remap_kernel_ms"],
+                      "nvlink_gbs": (R["remap_bytes"] / (R["remap_kernel_ms"] / 1e3) / 1e9)
+                      if R["remap_kernel_ms"] > 0 else None,
+                      "peak_gbs": 900.0,
+                      "frac": (R["remap_bytes"] / (R["remap_kernel_ms"] / 1e3) / 1e9 / 900.0)
+                      if R["remap_kernel_ms"] > 0 else None,
+                      "note": ("bytes this rank moves out per step / device time of the swap kernels "
+                               "(co-running with pass chunks when pipelined) vs NVLink 5's 900 GB/s per "
+                               "direction; exposed_ms = remap time not hidden behind pass chunks")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.config, world),
+                         "frac": achieved / peak, "frac_nominal_8tbs": achieved / 8000.0,
+                         "traffic": ncu_traffic(args.config, world),
                          "kernel": ("k_pass_tc + k_pass_tct (6-qubit tcgen05 passes)" if R["n_tc_passes"] == R["n_passes"]
                                     else "gate passes (k_pass_tc + k_pass_pair/k_pass_bit0)"),
                          "per_launch_bytes": per_launch,
@@ -380,7 +425,8 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": statistics.median(spent) * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeded circuit)",
            "config": {"workload": desc, "n_qubits": n, "shots": shots}, "impl": "reference",
-           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sdesc},
+           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sdesc,
+                            "projected": True, "host": host_info()},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
     return out

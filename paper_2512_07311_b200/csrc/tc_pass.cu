@@ -404,17 +404,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             atomicMax(&cmax[cb * 64 + j], __float_as_int(mx));
             asm volatile("bar.sync 2, 256;" ::: "memory");
             const int E = col_exponent(cmax[cb * 64 + j]);
-            const int es = (int)(it % kExpSlots);
-            if (to == 0) {
-                cmax[((it + 2) % 3) * 64 + j] = 0;   // buffer of tile it+2: every thread read it at tile it-1
-                colexp[es * 64 + j] = (int8_t)E;
-                mbar_arrive(&cready[es]);             // release: the epilogue reads E_j after acquiring
-            }
+            if (to == 0) cmax[((it + 2) % 3) * 64 + j] = 0;   // buffer of tile it+2: all read it at tile it-1
             const float sc = pow2f(E);
 #pragma unroll
             for (int i = 0; i < 16; i++) b[i] = f2mul(b[i], sc);
             const int s = it % kStages;
             mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+            // E_j -> epilogue.  Slot it % 4 was last read by the epilogue of tile it-4, which
+            // released D before the MMA of tile it-2 ran, which freed stage s (waited above): the
+            // write (and the slot mbarrier's next phase) must come after that wait.
+            const int es = (int)(it % kExpSlots);
+            if (to == 0) {
+                colexp[es * 64 + j] = (int8_t)E;
+                mbar_arrive(&cready[es]);             // release: the epilogue reads E_j after acquiring
+            }
             uint8_t* bhi = stages + s * kStageBytes;
             uint8_t* blo = bhi + kBBytes;
 #pragma unroll
@@ -685,15 +688,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             atomicMax(&cmax[cb * 128 + j], __float_as_int(mx));
             asm volatile("bar.sync 2, 256;" ::: "memory");
             const int E = col_exponent(cmax[cb * 128 + j]);
-            const int es = (int)(it % kExpSlots);
-            if (th == 0) {
-                cmax[((it + 2) % 3) * 128 + j] = 0;
-                colexp[es * 128 + j] = (int8_t)E;
-                mbar_arrive(&cready[es]);
-            }
+            if (th == 0) cmax[((it + 2) % 3) * 128 + j] = 0;
             const float sc = pow2f(E);
             mbar_wait(&aempty[b], ((it >> 1) & 1) ^ 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
+            // E_j -> epilogue after the wait: buffer b was freed by the MMA of tile it-2, which
+            // waited for the epilogue of tile it-3, so slot it % 4 (tile it-4) has been read
+            const int es = (int)(it % kExpSlots);
+            if (th == 0) {
+                colexp[es * 128 + j] = (int8_t)E;
+                mbar_arrive(&cready[es]);
+            }
             // K order t + 64 c: word c < 32 packs re of t = 2c, 2c+1; word 32 + c the im parts
             uint32_t hre[16], lre[16], him[16], lim[16];
 #pragma unroll

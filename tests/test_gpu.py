@@ -191,6 +191,56 @@ def test_sampling_and_xeb_parity(rcs, ctx, cfg, shots):
     assert abs(xr["F"] - xr["fstar"]) <= 5 * xr["sigma"]
 
 
+def dyadic_state(n, K, seed, zero_blocks=(), b=6):
+    """K = 4^m non-zero amplitudes of magnitude 2^-m with phases in {1, i, -1, -i}: every
+    probability (1/K), block sum and CDF value is exact in fp32, fp64 and any summation order.
+    The listed 2^b-amplitude blocks and the last block are all zero (trailing zeros)."""
+    rng = np.random.default_rng(seed)
+    N = 1 << n
+    allowed = np.ones(N, bool)
+    for z in list(zero_blocks) + [N // (1 << b) - 1]:
+        allowed[z << b:(z + 1) << b] = False
+    pos = np.sort(rng.choice(np.nonzero(allowed)[0], K, replace=False))
+    psi = np.zeros(N, complex)
+    psi[pos] = np.array([1, 1j, -1, -1j])[rng.integers(0, 4, K)] / math.sqrt(K)
+    return psi
+
+
+@pytest.mark.parametrize("case", ["ties8", "n10", "n12_b3"])
+def test_sampling_edge_uniforms_vs_oracle(rcs, ctx, case, tmp_path):
+    """V13 edge cases on the GPU path, bit-exact against the oracle on states whose CDF is exact:
+    u = 0, u = 1 - 2^-53 (largest generated uniform), u = 1 (t = T: the 'last x with p > 0'
+    fallback, through the uniform hook), t exactly on CDF boundaries (ties: the next x with
+    p > 0), exact zero probabilities, all-zero blocks and a zero tail.  The
+    state enters through the snapshot loader (any state, rounded to complex64 exactly)."""
+    from oracle.artifacts import save_snapshot
+    if case == "ties8":
+        psi = np.zeros(8, complex)
+        psi[0], psi[2], psi[3] = 0.5, 0.5, 0.5 + 0.5j
+        b, K = 6, 4
+    elif case == "n10":
+        psi, b, K = dyadic_state(10, 256, 1, zero_blocks=(0, 3, 7)), 6, 256
+    else:
+        psi, b, K = dyadic_state(12, 1024, 2, zero_blocks=(5, 6, 100), b=3), 3, 1024
+    path = str(tmp_path / "s.rcss")
+    save_snapshot(psi, path)
+    st = rcs.State.load_snapshot(ctx, path, block_bits=b)
+    assert st.norm == 1.0
+    C = np.cumsum(np.abs(psi) ** 2)
+    bounds = np.unique(C[(C > 0) & (C < 1)])              # exact CDF values -> t on a boundary
+    u = np.concatenate([[0.0, 1 - 2.0 ** -53, 1.0, 0.5], bounds, bounds - 2.0 ** -40,
+                        oracle.uniforms(7, 20000)])
+    xg = st.sample_uniforms(u)
+    xo, T = oracle.sample(psi, u)
+    assert T == 1.0
+    np.testing.assert_array_equal(xg, xo)
+    p = np.abs(psi) ** 2
+    assert (p[xg.astype(np.int64)] > 0).all()               # never a zero-probability pick
+    last = np.nonzero(p)[0][-1]
+    assert xg[1] == last and xg[2] == last                  # u = 1 - 2^-53 and the u = 1 fallback
+    st.free()
+
+
 def test_sample_uniforms_hook_and_offsets(rcs, ctx):
     text = config_qasm("c1")
     ref = oracle.build_state(text)

@@ -1,0 +1,238 @@
+"""Oracle-anchored parity at the BENCHMARKED size: n = 34 on one GPU (BASELINE config C4).
+
+A 2^34 fp64 oracle state (256 GiB) does not fit this host, so the oracle is anchored by the
+full-scale pins of SURVEY §8.c.3, each computed from the oracle (or a closed form) on factors
+that it finishes in milliseconds, and compared with the GPU state element by element on the
+device, chunk by chunk:
+
+  pin 2  separable circuit: C4's circuit with every coupler crossing the cut between grid rows
+         2 and 3 dropped.  psi = psi_B (x) psi_A, psi_A = oracle(qubits 0..17), psi_B =
+         oracle(qubits 18..33).  Built with the tensor-core path (fuse_k 6), canonical and with 3
+         virtual global qubits (bit-identical: pin 4, P-invariance), 2.5M shots checked against
+         the exact two-level inverse CDF with the G17 excuse band, same-sample XEB and F*.
+  pin 1  1q-only circuit: psi_x = prod_q v_q[x_q] (closed form), built with 3 virtual global
+         qubits through the NVLink peer-swap kernel (loopback) and its remap pipeline.
+  pin 3  C4 then C4^dagger: psi = e_0.
+
+Tolerances: BASELINE north_star (max |d psi| <= 1e-5, norm within 1e-5, bitstrings identical
+except within 1e-6 of the separating CDF boundary, XEB within 1e-3) and reading G16
+(||d psi||_2 <= 1e-5).  PAPER.md §3.2 l.36: stage 1 "construct[s] the complete quantum state";
+SPEC.md:130/152: the engine must equal the reference state vector.
+"""
+import contextlib
+import gc
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from rcs_workload import SHOT_SEED, CONFIGS, emit_qasm, generate
+from rcs_workload.gen import Circuit as GenCircuit
+
+pytestmark = pytest.mark.gpu
+
+N = 34
+CUT = 18            # qubits 0..17 = grid rows 0..2 (6x6 grid truncated to 34 sites)
+SHOTS = 2_500_000
+
+
+@pytest.fixture(scope="module")
+def rcs(cuda_ok):
+    import torch
+    free, total = torch.cuda.mem_get_info()
+    if free < (8 << N) + (16 << 30):
+        pytest.skip(f"n=34 needs {((8 << N) >> 30) + 16} GiB of device memory ({free >> 30} GiB free)")
+    from paper_2512_07311_b200 import build
+    build.build()
+    import paper_2512_07311_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(rcs):
+    return rcs.Context(0)
+
+
+def release():
+    import torch
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+@contextlib.contextmanager
+def built(rcs, ctx, text, **kw):
+    """A built n=34 state whose 128 GiB are released on every exit path (a failing assertion
+    must not leave the next test without device memory)."""
+    release()
+    st = rcs.State.build(ctx, rcs.Circuit.from_qasm(text), **kw)
+    try:
+        yield st
+    finally:
+        st.free()
+        st.amps = st.scratch = None
+        release()
+
+
+def c4_circuit(two_qubit=True):
+    cfg = CONFIGS["c4"]
+    return generate(cfg["rows"], cfg["cols"], cfg["cycles"], cfg["pattern"], 1, n_qubits=N, jitter=0.05,
+                    two_qubit=two_qubit)
+
+
+def split_circuit():
+    """C4 without the couplers that cross the cut -> (full n=34 QASM, QASM of A, QASM of B)."""
+    full = c4_circuit()
+    cut = GenCircuit(N)
+    a, b = GenCircuit(CUT), GenCircuit(N - CUT)
+    dropped = 0
+    for m in full.moments:
+        keep, ma, mb = [], [], []
+        for g in m:
+            lo = [q < CUT for q in g.qubits]
+            if all(lo):
+                keep.append(g)
+                ma.append(g)
+            elif not any(lo):
+                keep.append(g)
+                mb.append(type(g)(g.kind, tuple(q - CUT for q in g.qubits), g.params))
+            else:
+                dropped += 1
+        cut.moments.append(keep)
+        a.moments.append(ma)
+        b.moments.append(mb)
+    assert dropped > 0
+    return emit_qasm(cut), emit_qasm(a), emit_qasm(b)
+
+
+def compare_kron(amps, f_hi, f_lo):
+    """max |d|, ||d||_2 of the device state against kron(f_hi, f_lo) (index = hi * len(lo) + lo),
+    in complex128, 2^26 amplitudes at a time; plus a positional digest of the raw bits."""
+    import torch
+    dev = amps.device
+    lo = torch.from_numpy(np.ascontiguousarray(f_lo)).to(dev)
+    hi = torch.from_numpy(np.ascontiguousarray(f_hi)).to(dev)
+    nlo = lo.numel()
+    rows = max(1, (1 << 26) // nlo)
+    A = amps.view(-1, nlo)
+    bits = amps.view(torch.int32).view(-1, 2 * nlo)
+    w = (torch.arange(2 * nlo * rows, device=dev, dtype=torch.int64) % 65521 + 1).view(rows, 2 * nlo)
+    maxd, ss, digest = 0.0, 0.0, 0
+    for r0 in range(0, hi.numel(), rows):
+        blk = A[r0:r0 + rows].to(torch.complex128)
+        d = blk - hi[r0:r0 + rows, None] * lo[None, :]
+        maxd = max(maxd, d.abs().max().item())
+        ss += (d.real.square() + d.imag.square()).sum().item()
+        digest = (digest * 1000003 + int((bits[r0:r0 + rows].to(torch.int64) * w[:blk.shape[0]]).sum().item())) % (1 << 61)
+        del blk, d
+    return maxd, math.sqrt(ss), digest
+
+
+@pytest.fixture(scope="module")
+def separable(rcs):
+    text, qa, qb = split_circuit()
+    psi_a = oracle.build_state(qa)
+    psi_b = oracle.build_state(qb)
+    return text, psi_a, psi_b
+
+
+def test_separable_c4_state_sampling_xeb(rcs, ctx, separable):
+    text, psi_a, psi_b = separable
+    with built(rcs, ctx, text, fuse_k=6) as st:
+        rep = st.report
+        assert rep["n_tc_passes"] > 0 and abs(st.norm - 1) <= 1e-5
+        maxd, eps, dig0 = compare_kron(st.amps, psi_b, psi_a)
+        assert maxd <= 1e-5 and eps <= 1e-5, (maxd, eps)
+        x = st.sample(SHOTS, seed=SHOT_SEED)
+        xr = st.xeb(x)
+        T_gpu = st.norm
+
+    # 2.5M shots against the exact two-level inverse CDF (V12/V13): logical x = x_B 2^18 + x_A,
+    # C(x) = C_B(x_B - 1) T_A + p_B(x_B) C_A(x_A).  G17: the GPU pick x_g is right iff
+    # t_s = u_s T lies in [C(x_g - 1) - 1e-6, C(x_g) + 1e-6].
+    u = oracle.uniforms(SHOT_SEED, SHOTS)
+    p_a, p_b = np.abs(psi_a) ** 2, np.abs(psi_b) ** 2
+    CA, CB = np.cumsum(p_a), np.cumsum(p_b)
+    TA, TB = CA[-1], CB[-1]
+    T = TA * TB
+    t = u * T
+    xa = (x & np.uint64((1 << CUT) - 1)).astype(np.int64)
+    xb = (x >> np.uint64(CUT)).astype(np.int64)
+    CBm = np.where(xb > 0, CB[np.maximum(xb - 1, 0)], 0.0)
+    CAm = np.where(xa > 0, CA[np.maximum(xa - 1, 0)], 0.0)
+    hi = CBm * TA + p_b[xb] * CA[xa]                 # C(x_g)
+    lo = CBm * TA + p_b[xb] * CAm                    # C(x_g - 1)
+    bad = ~((t >= lo - 1e-6) & (t <= hi + 1e-6))
+    assert int(bad.sum()) == 0, f"{int(bad.sum())} unexcused shots of {SHOTS}"
+    # Tighter than G17 (whose 1e-6 spans ~17000 CDF steps at n = 34): in normalised CDF
+    # coordinates (the sampler scales u by its own total) the pick may differ from the exact one
+    # only by the CDF drift the state error causes, a random walk of std ~ 2 eps / sqrt(2^n)
+    # (SURVEY §8.c.4); allow 50x that.
+    excess = np.maximum(lo / T - u, 0.0) + np.maximum(u - hi / T, 0.0)
+    band = max(2e-9, 50 * eps / 2 ** (N / 2))
+    assert excess.max() <= band, (excess.max(), band)
+    xb_o = np.minimum(np.searchsorted(CB * TA, t, side="right"), len(CB) - 1)
+    base = np.where(xb_o > 0, CB[np.maximum(xb_o - 1, 0)] * TA, 0.0)
+    xa_o = np.minimum(np.searchsorted(CA, (t - base) / np.maximum(p_b[xb_o], 1e-300), side="right"), len(CA) - 1)
+    x_o = (xb_o.astype(np.uint64) << np.uint64(CUT)) | xa_o.astype(np.uint64)
+    print(f"n=34 separable: eps={eps:.3e} max|d|={maxd:.3e} T_gpu-1={T_gpu - 1:+.2e} "
+          f"shots differing from the exact pick: {int((x_o != x).sum())} of {SHOTS}, max excess {excess.max():.2e}")
+
+    # XEB: same-sample against the exact p(x) = p_A(x_A) p_B(x_B); F* against its closed form
+    F_exact = 2.0 ** N * np.mean(p_a[xa] * p_b[xb]) - 1
+    assert abs(xr["F"] - F_exact) <= 1e-3, (xr["F"], F_exact)
+    fstar = (2.0 ** CUT * np.sum(p_a ** 2)) * (2.0 ** (N - CUT) * np.sum(p_b ** 2)) - 1
+    assert abs(xr["fstar"] - fstar) <= 1e-4, (xr["fstar"], fstar)
+    assert abs(xr["F"] - fstar) <= 5 * xr["sigma"]
+
+    # pin 4: 3 virtual global qubits (remaps between the 8 virtual shards) -> bit-identical
+    with built(rcs, ctx, text, fuse_k=6, virtual_global=3) as st:
+        assert st.report["n_remaps"] > 0
+        maxd3, eps3, dig3 = compare_kron(st.amps, psi_b, psi_a)
+        assert dig3 == dig0 and maxd3 == maxd and eps3 == eps
+        assert np.array_equal(st.sample(SHOTS, seed=SHOT_SEED), x)
+
+
+def product_factors():
+    """1q-only C4 circuit: psi_x = prod_q v_q[x_q]; v_q from the oracle's own 2x2 matrices."""
+    circ = c4_circuit(two_qubit=False)
+    v = [np.array([1, 0], complex) for _ in range(N)]
+    for g in circ.gates:
+        v[g.qubits[0]] = oracle.gate_matrix(g.kind) @ v[g.qubits[0]]
+    half = N // 2
+
+    def kron(qs):   # qubit qs[0] = least significant
+        out = np.array([1.0 + 0j])
+        for q in qs:
+            out = np.kron(v[q], out)
+        return out
+    return emit_qasm(circ), kron(range(half, N)), kron(range(half))
+
+
+@pytest.mark.parametrize("mode", ["loopback", "bitswap"])
+def test_product_state_n34_through_remaps(rcs, ctx, mode):
+    text, f_hi, f_lo = product_factors()
+    kw = {"virtual_global": 3, "timing": True}
+    if mode == "loopback":
+        kw["remap_mode"] = "loopback"
+    with built(rcs, ctx, text, fuse_k=6, **kw) as st:
+        rep = st.report
+        assert rep["n_remaps"] > 0, rep
+        if mode == "loopback":
+            assert rep["n_peer_remaps"] > 0 and rep["remap_kernel_ms"] > 0, rep
+        maxd, eps, _ = compare_kron(st.amps, f_hi, f_lo)
+        assert maxd <= 1e-5 and eps <= 1e-5, (maxd, eps)
+        assert abs(st.norm - 1) <= 1e-5
+
+
+def test_c4_then_inverse_is_e0(rcs, ctx):
+    from tests.test_oracle_pins import inverse_qasm
+    text = emit_qasm(c4_circuit())
+    both = text + inverse_qasm(oracle.parse(text))
+    with built(rcs, ctx, both, fuse_k=6) as st:
+        assert st.report["n_passes"] >= 60
+        a0 = complex(st.copy_out(0, 1)[0])
+        assert abs(a0 - 1) <= 1e-5, a0
+        assert abs(st.norm - 1) <= 1e-5
+        assert st.norm - abs(a0) ** 2 <= 1e-10           # ||psi - e_0||_2 <= 1e-5

@@ -251,6 +251,36 @@ def test_sampler_chi_square_and_tv():
     assert tv <= 3 * math.sqrt(64 / S)
 
 
+def test_inverse_cdf_ties_and_zero_probabilities():
+    """V13 on hand-computed cases: x_s = min{x : C(x) > t_s} with C the INCLUSIVE
+    CDF, so a t_s that lands exactly on C(x) picks the next x with p > 0 (a `>=` comparison
+    would pick x itself, or a zero-probability x)."""
+    psi = np.zeros(8, complex)
+    psi[0], psi[2], psi[3] = 0.5, 0.5, 0.5 + 0.5j       # p = [1/4, 0, 1/4, 1/2, 0, 0, 0, 0] exactly
+    u = np.array([0.0, 0.2, 0.25, 0.4, 0.5, 0.75, 1 - 2.0 ** -53])
+    x, T = oracle.sample(psi, u)
+    assert T == 1.0
+    assert x.tolist() == [0, 0, 2, 2, 3, 3, 3]
+
+
+def test_inverse_cdf_fallback_is_last_nonzero():
+    """V13's fallback: when no x has C(x) > t_s, the pick is the last x WITH p > 0 -- not the last
+    index 2^n - 1 (a plain searchsorted would return 2^n and clip to a zero-probability index).
+    The oracle's T is the CDF's own end C(2^n - 1), so fl(u T) < T for every u < 1 and the branch
+    is reached through the uniform hook with u = 1 (t = T), on states with trailing zeros."""
+    psi = np.zeros(8, complex)
+    psi[0], psi[2], psi[3] = 0.5, 0.5, 0.5 + 0.5j       # p = [1/4, 0, 1/4, 1/2, 0, 0, 0, 0]
+    x, T = oracle.sample(psi, np.array([1.0, 1 - 2.0 ** -53]))
+    assert x.tolist() == [3, 3]
+    psi = np.zeros(16, complex)
+    psi[[1, 4, 5]] = [0.5, 0.5j, 0.5 + 0.5j]             # p = 1/4, 1/4, 1/2; last non-zero at 5
+    x, T = oracle.sample(psi, np.array([1.0, 0.0, 0.25, 0.5]))
+    assert x.tolist() == [5, 1, 4, 5]
+    # fl(u T) < T for the largest uniform: the branch is unreachable from generated uniforms
+    for T in (1.0, 1 - 2.0 ** -52, 1 + 2.0 ** -52, 0.9999995, 1.0000003):
+        assert (1 - 2.0 ** -53) * T < T
+
+
 def test_sampler_refuses_bad_norm():
     psi = np.zeros(4, complex)
     psi[0] = 1.01
