@@ -234,8 +234,10 @@ rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, std
     return RCS_OK;
 }
 
-// Tensor-core items of a plan (6-qubit blocks; 5-qubit blocks padded to 6 with the identity on
-// one more local qubit as the highest matrix bit: same arithmetic for every choice of it).
+// Tensor-core items of a plan (6-qubit blocks; 5-qubit blocks padded to 6 with the identity on a
+// pinned qubit not in the block -- the lowest one, so the choice is a function of the block --
+// placed as matrix bit 0: then a block's highest qubit, the transposed kernel's converter-half
+// bit, never sits at one of the lowest cube ranks).
 void make_tc_pack(const Plan& P, int nl, TcPack& out) {
     out.slot.assign(P.items.size(), -1);
     out.pos.assign(P.items.size(), std::array<int, 6>{});
@@ -243,7 +245,6 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
     for (size_t ii = 0; ii < P.items.size(); ii++) {
         const Item& it = P.items[ii];
         if (it.type != RCS_ITEM_PASS || nl < kTcMinLocal || it.k < 5) continue;
-        for (int i = 0; i < it.k; i++) out.pos[ii][i] = it.pos[i];
         if (it.k == 5) {   // pad qubit: lowest of the pinned qubits 0..5 not in the block
             int pad = -1;
             for (int b = 0; b < P.pinned && pad < 0; b++) {
@@ -251,7 +252,10 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
                 for (int i = 0; i < 5; i++) used = used || it.pos[i] == b;
                 if (!used) pad = b;
             }
-            out.pos[ii][5] = pad;
+            out.pos[ii][0] = pad;
+            for (int i = 0; i < 5; i++) out.pos[ii][i + 1] = it.pos[i];
+        } else {
+            for (int i = 0; i < 6; i++) out.pos[ii][i] = it.pos[i];
         }
         out.slot[ii] = out.n_tc++;
     }
@@ -262,10 +266,10 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
         if (out.slot[ii] < 0) continue;
         const Block& B = P.blocks[P.items[ii].block];
         const cplx* m = B.matrix.data();
-        if (P.items[ii].k == 5) {
+        if (P.items[ii].k == 5) {   // I (x) M with the pad as the lowest matrix bit
             for (int r = 0; r < 64; r++)
                 for (int c = 0; c < 64; c++)
-                    padded[r * 64 + c] = ((r ^ c) & 32) ? cplx{0.0, 0.0} : B.matrix[(r & 31) * 32 + (c & 31)];
+                    padded[r * 64 + c] = ((r ^ c) & 1) ? cplx{0.0, 0.0} : B.matrix[(r >> 1) * 32 + (c >> 1)];
             m = padded.data();
         }
         dev::tc_pack_matrix(reinterpret_cast<const double*>(m), out.words.data() + (size_t)out.slot[ii] * each);

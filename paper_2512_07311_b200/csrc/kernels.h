@@ -20,9 +20,10 @@ void tc_pack_matrix(const double* u_re_im, uint32_t* out);
 // Optional chunking (pipelined remaps): fix[0..nfix) are extra positions held at the bits of
 // fixval, so the launch covers one 2^-nfix slice of the index space.  Fixed positions must lie
 // outside tc_reserved_mask(pos); the grid is min(num_sms, tiles).
-// K12 (the transposed kernel) runs iff no target sits in positions 0..6 (tc_uses_k12: a function
-// of the block alone); force_k9 (tests) runs K9 for every block.
-bool tc_uses_k12(const int* pos);
+// K12 (the transposed kernel, any target layout) runs when n_local >= 13 and at most one target
+// sits in positions 0..3 (tc_uses_k12: a function of the block, positions 0..6 being pinned);
+// K9 otherwise, or for every block with force_k9 (tests, comparisons).
+bool tc_uses_k12(int n_local_bits, const int* pos);
 cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const uint32_t* d_a, int num_sms,
                          cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0,
                          bool force_k9 = false);

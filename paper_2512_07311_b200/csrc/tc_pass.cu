@@ -550,27 +550,46 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
 }
 
 // =====================================================================================
-// K12: the transposed product for layouts with no target among positions 0..6.
+// K12: the transposed product, for ANY target layout (n_local >= 13).
 //     Y^T (128 j x 128 n) = X^T (128 j x 128 k) . B (128 k x 128 n),  B[k][n] = A_K9[n][k]
-// The state tile (64 target combinations t x 128 columns j = index bits 0..6, 8192 amplitudes)
-// is the TMEM operand A: converter thread j packs its row (fp16 hi/lo of re/im for every t)
-// with tcgen05.st -- no B-stage round trip through shared memory -- and the constant matrix is
-// the shared-memory operand.  D rows are columns j, so an epilogue warp stores 32 consecutive
-// amplitudes (256 B) per target combination straight from registers -- no staging.  Shared
-// memory per 8192 amplitudes: TMA 64 KB + converter reads 64 KB + MMA matrix reads 96 KB (K9:
-// ~2x that per amplitude).  K order (t + 64 c), k-steps and accumulators are K9's, so each output
-// element is the same sum of the same products.
-//   warp  13   producer: TMA of the 64 runs (1 KB each) of a tile into a raw slot
+// Tile = a 13-bit sub-cube of the index: the 6 target positions plus the 7 lowest non-target
+// positions (the columns j).  Positions 0..6 always lie in the cube, so the tile is 2^(13-r)
+// runs of 2^r >= 128 contiguous amplitudes (TMA copies >= 1 KB).  In shared memory an element
+// sits at its cube index (bit b = the b-th lowest cube position).  The state tile (64 target
+// combinations t x 128 columns j) is the TMEM operand A: converter thread j packs its row (fp16
+// hi/lo of re/im for every t) with tcgen05.st -- no B-stage round trip through shared memory --
+// and the constant matrix is the shared-memory operand.  D rows are columns j, so the epilogue
+// stores straight from registers (no staging): a warp writes 32 columns of one t, i.e. 256
+// contiguous bytes when no target sits below position 5.
+// Bank conflicts: the 16 lanes of a half-warp read 16 columns of one t; when a targets occupy
+// cube ranks 0..3, only 4-a column bits vary the bank.  K12 takes a <= 1 (more: K9): the lanes
+// whose displaced column bit (j bit 3) is set read t XOR (the low target's bit) instead, which
+// makes the 16 reads hit 16 distinct bank pairs; after the fp16 split the packed words are put
+// back in t order (a byte permute for t bit 0, selects for t bits 1..4).  t bit 5 selects the
+// thread's half and must not be flipped: the planner pins qubits 0..6 to positions 0..6 and pads
+// 5-qubit blocks with a pinned qubit as matrix bit 0, so a block's highest qubit (t bit 5)
+// never sits below cube rank 4.
+// K order (t + 64 c), k-steps and accumulators are K9's: the main term is exact, so K9 and K12
+// differ only in how the cross terms round.
+//   warp  13   producer: TMA of the runs of a tile into a raw slot
 //   warps 0-7  converters: warp w -> TMEM lanes 32 (w & 3).., t half w >> 2 -> A buffer
 //   warp  12   MMA: 24 x tcgen05.mma (M=128, N=128, K=16), A = state (TMEM), B = matrix (smem)
-//   warps 8-11 epilogue: D (2 accumulators) -> registers -> global, memory order per warp
+//   warps 8-11 epilogue: D (2 accumulators) -> registers -> global
 // TMEM: A buffers [0,128) and [128,256) (hi at +0, lo at +64); D acc 0 at 256, acc 1 at 384.
 struct TcTArgs {
     float2* amps;
-    const uint32_t* a;       // K9-packed A (hi, lo): row n, word c = k pair (2c, 2c+1)
+    const uint32_t* a;       // K9-packed A (hi, lo): row n, word c = k pair (2c, 2c+1); F_t after
     uint64_t ntiles;
-    int pos[6];              // physical position of matrix bit i (all >= 7)
-    int nins;                // 13 sub-cube positions (0..6 and the targets) + chunk bits, ascending
+    int pos[6];              // physical position of matrix (target) bit i
+    int tcube[6];            // cube rank of pos[i]
+    int jpos[7];             // physical position of column bit k (the 7 lowest non-targets)
+    int jcube[7];            // cube rank of jpos[k]
+    int r;                   // cube ranks 0..r-1 are positions 0..r-1 (runs of 2^r amplitudes)
+    int nrun_pos;            // 13 - r: cube positions above the runs ...
+    int run_pos[6];          // ... (the TMA run index is deposited into them)
+    int phi_lane;            // lanes with this bit set read t XOR (1 << phi_t) (bank-conflict-free),
+    int phi_t;               // -1 if no target sits in cube ranks 0..3
+    int nins;                // 13 cube positions + chunk bits, ascending
     int ins[17];
     uint64_t fixval;         // chunk bits (pipelined remaps), as K9
     uint64_t fmask, dstride; // tile-index deposit (as K9)
@@ -578,13 +597,47 @@ struct TcTArgs {
 
 constexpr uint32_t kTRaw = 8192 * 8;                  // one tile: 64 KB
 constexpr uint32_t kTMat = 2 * 128 * 128 * 2;         // B hi + lo: 64 KB
-constexpr uint32_t kTCtl = 3072;
-static_assert((10 + kExpSlots) * 8 + 64 * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl, "K12 control block");
+constexpr uint32_t kTCtl = 3584;
+static_assert((10 + kExpSlots) * 8 + 64 * 8 + 64 * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl,
+              "K12 control block");
 constexpr uint32_t kTSmem = 2 * kTRaw + kTMat + kTCtl;
 
+// 32-bit conditional swap (select) of a and b
+__device__ __forceinline__ void cswap(bool f, uint32_t& a, uint32_t& b) {
+    const uint32_t x = f ? b : a, y = f ? a : b;
+    a = x;
+    b = y;
+}
+
+// Undo t ^= (f << tb) on the 16 packed words of one converter thread (word i packs t = 2i,
+// 2i+1 of its 32): t bit 0 is a half swap inside every word, t bit tb >= 1 a swap of words
+// i <-> i ^ 2^(tb-1).  tb is uniform over the launch, f per lane.
+template <int B>
+__device__ __forceinline__ void swap_words(uint32_t (&w)[16], bool f) {
+#pragma unroll
+    for (int i = 0; i < 16; i++)
+        if (!((i >> B) & 1)) cswap(f, w[i], w[i | (1 << B)]);
+}
+__device__ __forceinline__ void unpermute16(uint32_t (&w)[16], bool f, int tb) {
+    if (tb == 0) {
+        const uint32_t sel = f ? 0x1032u : 0x3210u;
+#pragma unroll
+        for (int i = 0; i < 16; i++) w[i] = __byte_perm(w[i], 0, sel);
+    } else if (tb == 1) {
+        swap_words<0>(w, f);
+    } else if (tb == 2) {
+        swap_words<1>(w, f);
+    } else if (tb == 3) {
+        swap_words<2>(w, f);
+    } else {
+        swap_words<3>(w, f);
+    }
+}
+
+template <bool PERM>
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constant__ TcTArgs p) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    float2* raw = reinterpret_cast<float2*>(smem);                       // [2][64 t][128 j]
+    float2* raw = reinterpret_cast<float2*>(smem);                       // [2][8192] by cube index
     uint8_t* mat = smem + 2 * kTRaw;                                      // B hi | B lo (K-major)
     uint8_t* ctl = mat + kTMat;
     uint64_t* rfull = reinterpret_cast<uint64_t*>(ctl);   // [2]
@@ -594,8 +647,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     uint64_t* dfull = aempty + 2;                         // [1]
     uint64_t* dempty = dfull + 1;                         // [1]
     uint64_t* cready = dempty + 1;                        // [kExpSlots] column exponents of a tile written
-    uint64_t* offt = cready + kExpSlots;                  // [64] target-combination offsets
-    int* cmax = reinterpret_cast<int*>(offt + 64);        // [3][128] column max |x| (float bits)
+    uint64_t* offt = cready + kExpSlots;                  // [64] physical offset of target combination t
+    uint64_t* offr = offt + 64;                           // [64] physical offset of TMA run u
+    int* cmax = reinterpret_cast<int*>(offr + 64);        // [3][128] column max |x| (float bits)
     float* rowfac = reinterpret_cast<float*>(cmax + 3 * 128);   // [64] 2^-F_t
     int8_t* colexp = reinterpret_cast<int8_t*>(rowfac + 64);     // [kExpSlots][128] E_j per tile
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colexp + kExpSlots * 128);
@@ -619,11 +673,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     }
     for (int i = threadIdx.x; i < 3 * 128; i += blockDim.x) cmax[i] = 0;
     if (threadIdx.x < 64) {
-        uint64_t ot = 0;
-        for (int i = 0; i < 6; i++)
-            if ((threadIdx.x >> i) & 1) ot |= 1ull << p.pos[i];
-        offt[threadIdx.x] = ot;
-        rowfac[threadIdx.x] = pow2f(-(int)p.a[2 * 128 * 64 + threadIdx.x]);
+        const int x = threadIdx.x;
+        uint64_t ot = 0, orr = 0;
+        for (int i = 0; i < 6; i++) {
+            if ((x >> i) & 1) ot |= 1ull << p.pos[i];
+            if (i < p.nrun_pos && ((x >> i) & 1)) orr |= 1ull << p.run_pos[i];
+        }
+        offt[x] = ot;
+        offr[x] = orr;
+        rowfac[x] = pow2f(-(int)p.a[2 * 128 * 64 + x]);
     }
     // the matrix as the K-major shared-memory operand: core chunk (n, c) = A_K9 words [n][4c..4c+3]
     for (int e = threadIdx.x; e < 2 * 128 * 16; e += blockDim.x) {
@@ -648,6 +706,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     const uint64_t first = blockIdx.x;
 
     if (warp == kProdWarp) {
+        const int nruns = 1 << p.nrun_pos;
+        const uint32_t run_bytes = 8u << p.r;
         uint64_t it = 0, bp = tile_base(first);
         for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
             const int slot = it & 1;
@@ -659,27 +719,43 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             __syncwarp();
             const float2* src = p.amps + (bp | p.fixval);
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
-            for (int t = lane; t < 64; t += 32)
+            for (int u = lane; u < nruns; u += 32)
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        dst + t * 1024u),
-                    "l"(src + offt[t]), "r"(1024u), "r"(su32(&rfull[slot]))
+                        dst + u * run_bytes),
+                    "l"(src + offr[u]), "r"(run_bytes), "r"(su32(&rfull[slot]))
                     : "memory");
         }
     } else if (warp < kLoadWarps) {
         // ---------------- converters: thread j = 32 (w & 3) + lane, t in [32 (w >> 2), +32)
         const int q = warp & 3, th = warp >> 2;
         const int j = 32 * q + lane;
+        const bool pf = PERM && ((lane >> p.phi_lane) & 1);   // this lane reads t ^ (1 << phi_t)
+        const uint32_t phi = pf ? 1u << p.phi_t : 0u;
+        // cube index of (t = 32 th + (u ^ phi), j) = base ^ cube_t(u) with cube_t linear in u
+        uint32_t base = 0;
+        for (int k = 0; k < 7; k++)
+            if ((j >> k) & 1) base |= 1u << p.jcube[k];
+        if (th) base |= 1u << p.tcube[5];
+        uint32_t R[5];
+#pragma unroll
+        for (int i = 0; i < 5; i++) {
+            R[i] = 1u << p.tcube[i];
+            if (PERM && ((phi >> i) & 1)) base ^= R[i];
+        }
         uint64_t it = 0;
         for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++) {
             const int slot = it & 1, b = it & 1;
             mbar_wait(&rfull[slot], (it >> 1) & 1);
-            const float2* rb = raw + (size_t)slot * 8192 + j;
-            float2 v[32];
+            const float2* rb = raw + (size_t)slot * 8192;
+            float2 v[32];   // v[u] = x(32 th + (u ^ phi), j)
             float mx = 0.f;
+            uint32_t ci = base;
 #pragma unroll
-            for (int u = 0; u < 32; u++) {
-                v[u] = rb[(size_t)(32 * th + u) * 128];
+            for (int g = 0; g < 32; g++) {   // Gray-code walk of u: one XOR per element
+                const int u = g ^ (g >> 1);
+                if (g) ci ^= R[(g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4];
+                v[u] = rb[ci];
                 mx = absmax2(mx, v[u]);
             }
             mbar_arrive(&rempty[slot]);
@@ -706,6 +782,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                 const float2 v0 = f2mul(v[2 * u], sc), v1 = f2mul(v[2 * u + 1], sc);
                 split_exact_h2(v0.x, v1.x, hre[u], lre[u]);
                 split_exact_h2(v0.y, v1.y, him[u], lim[u]);
+            }
+            if (PERM) {
+                unpermute16(hre, pf, p.phi_t);
+                unpermute16(him, pf, p.phi_t);
+                unpermute16(lre, pf, p.phi_t);
+                unpermute16(lim, pf, p.phi_t);
             }
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 128 * b + 16 * th;
             TMEM_ST16(ta, hre);             // hi, re words [16 th, +16)
@@ -751,6 +833,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         // ---------------- epilogue: lane quarter q holds columns j = 32 q + lane
         const int q = warp & 3;
         const int j = 32 * q + lane;
+        uint64_t offj = 0;
+        for (int k = 0; k < 7; k++)
+            if ((j >> k) & 1) offj |= 1ull << p.jpos[k];
         uint64_t it = 0, bp = tile_base(first);
         for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
             const int es = (int)(it % kExpSlots);
@@ -758,7 +843,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             const float cf = pow2f(-(int)colexp[es * 128 + j]);   // 2^-E_j (read before releasing D)
             mbar_wait(dfull, it & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            float2* dst = p.amps + (bp | p.fixval) + j;
+            float2* dst = p.amps + (bp | p.fixval | offj);
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256;
 #pragma unroll
             for (int s4 = 0; s4 < 4; s4++) {   // 32 columns n = 16 target combinations (re, im)
@@ -845,19 +930,53 @@ uint64_t tc_reserved_mask(int nl, const int* pos) {
     return m;
 }
 
-// K12 launcher (no target among positions 0..6; whole index space, no chunk bits)
+// K12 launcher: any target layout, n_local >= 13 (+ chunk bits)
 static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms,
                                  cudaStream_t st, const int* fix, int nfix, uint64_t fixval) {
     TcTArgs p{};
     p.amps = amps;
     p.a = d_a;
-    if (nl < 13 + nfix) return cudaErrorInvalidValue;
+    if (nl < 13 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     p.ntiles = 1ull << (nl - 13 - nfix);
-    uint64_t insmask = 0x7f, fixmask = 0;
+    uint64_t tmask = 0;
     for (int i = 0; i < 6; i++) {
+        if (pos[i] < 0 || pos[i] >= nl || ((tmask >> pos[i]) & 1)) return cudaErrorInvalidValue;
         p.pos[i] = pos[i];
-        insmask |= 1ull << pos[i];
+        tmask |= 1ull << pos[i];
     }
+    uint64_t cube = tmask;
+    for (int b = 0, k = 0; b < nl && k < 7; b++)
+        if (!((tmask >> b) & 1)) {
+            p.jpos[k++] = b;
+            cube |= 1ull << b;
+        }
+    int rank[64];
+    int nc = 0;
+    for (int b = 0; b < nl; b++)
+        if ((cube >> b) & 1) rank[b] = nc++;
+    if (nc != 13) return cudaErrorInvalidValue;
+    for (int i = 0; i < 6; i++) p.tcube[i] = rank[pos[i]];
+    for (int k = 0; k < 7; k++) p.jcube[k] = rank[p.jpos[k]];
+    p.r = 0;
+    while (p.r < 13 && ((cube >> p.r) & 1)) p.r++;
+    if (p.r < 7) return cudaErrorInvalidValue;
+    p.nrun_pos = 0;
+    for (int b = p.r; b < nl; b++)
+        if ((cube >> b) & 1) p.run_pos[p.nrun_pos++] = b;
+    if (p.nrun_pos != 13 - p.r) return cudaErrorInvalidValue;
+    // bank-conflict-free converter reads: with one target at cube rank < 4, column bit 3 is
+    // displaced to rank 4 and the lanes with it set read t ^ (that target's bit); t bit 5 (the
+    // converter half) must not be it.  More low targets: K9 (tc_uses_k12).
+    p.phi_lane = 3;
+    p.phi_t = -1;
+    for (int i = 0; i < 6; i++)
+        if (p.tcube[i] < 4) {
+            if (p.phi_t >= 0 || i >= 5) return cudaErrorInvalidValue;
+            p.phi_t = i;
+        }
+    const bool perm = p.phi_t >= 0;
+    if (perm && p.jcube[3] < 4) return cudaErrorInvalidValue;
+    uint64_t insmask = cube, fixmask = 0;
     for (int i = 0; i < nfix; i++) {
         if (fix[i] < 0 || fix[i] >= nl || ((insmask >> fix[i]) & 1)) return cudaErrorInvalidValue;
         fixmask |= 1ull << fix[i];
@@ -879,24 +998,33 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
         }
     p.dstride = d;
     // the attribute is per device (context): set it before every launch (cheap)
-    cudaError_t e = cudaFuncSetAttribute(k_pass_tct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+    cudaError_t e = perm ? cudaFuncSetAttribute(k_pass_tct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem)
+                         : cudaFuncSetAttribute(k_pass_tct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
     if (e != cudaSuccess) return e;
     count_launch();
-    k_pass_tct<<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
+    if (perm)
+        k_pass_tct<true><<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
+    else
+        k_pass_tct<false><<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
     return cudaGetLastError();
 }
 
-bool tc_uses_k12(const int* pos) {
-    for (int i = 0; i < 6; i++)
-        if (pos[i] < 7) return false;
-    return true;
+// K12 (transposed) for n_local >= 13 unless two or more targets sit in positions 0..3: there the
+// converters' lane-dependent t permutation (bank-conflict-free reads) costs 2-2.5x a pass
+// (measured C4: 82-118 ms vs ~60 ms on K9, profiles/r02/pass_report_c4_k12all.txt), and K9's
+// B-stage path is faster.  Positions 0..6 hold qubits 0..6 in every sharding (planner pinning),
+// so the choice is a function of the block: the rounding of the cross terms is
+// sharding-independent.
+bool tc_uses_k12(int nl, const int* pos) {
+    if (nl < 13) return false;
+    int low = 0;
+    for (int i = 0; i < 6; i++) low += pos[i] < 4;
+    return low <= 1;
 }
 
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
                          const int* fix, int nfix, uint64_t fixval, bool force_k9) {
-    // K12 iff no target sits in positions 0..6: a function of the block alone, so the kernel
-    // (and its rounding) never depends on the sharding or on chunking (force_k9: tests only)
-    if (!force_k9 && tc_uses_k12(pos)) return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval);
+    if (!force_k9 && tc_uses_k12(nl, pos)) return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval);
     if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
     p.amps = amps;
