@@ -199,12 +199,17 @@ __device__ __forceinline__ int col_exponent(int maxbits) {
 }
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }   // e in [-126, 127]
 
-// (v0, v1) already scaled -> hi = fp16x2(rint v0, rint v1) (exact integers), lo = fp16x2(v - hi)
+// (v0, v1) already scaled -> hi = fp16x2(rint v0, rint v1) (exact integers), lo = fp16x2(v - hi).
+// rint by the magic constant 1.5 2^23 (|v| <= 2^11: v + M has an ulp of 1, round-half-even like
+// cvt.rni), all three steps as packed f32x2 operations; v - hi is exact.
 __device__ __forceinline__ void split_exact_h2(float v0, float v1, uint32_t& hi, uint32_t& lo) {
-    float h0, h1;
-    asm("cvt.rni.f32.f32 %0, %1;" : "=f"(h0) : "f"(v0));
-    asm("cvt.rni.f32.f32 %0, %1;" : "=f"(h1) : "f"(v1));
-    const float r0 = v0 - h0, r1 = v1 - h1;   // exact
+    float h0, h1, r0, r1;
+    asm("{\n.reg .b64 x, m, t, h, r;\n"
+        "mov.b64 x, {%4, %5};\nmov.b64 m, {%6, %6};\n"
+        "add.rn.f32x2 t, x, m;\nsub.rn.f32x2 h, t, m;\nsub.rn.f32x2 r, x, h;\n"
+        "mov.b64 {%0, %1}, h;\nmov.b64 {%2, %3}, r;\n}"
+        : "=f"(h0), "=f"(h1), "=f"(r0), "=f"(r1)
+        : "f"(v0), "f"(v1), "f"(12582912.0f));
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(h1), "f"(h0));
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(r1), "f"(r0));
 }
@@ -587,8 +592,8 @@ struct TcTArgs {
     int r;                   // cube ranks 0..r-1 are positions 0..r-1 (runs of 2^r amplitudes)
     int nrun_pos;            // 13 - r: cube positions above the runs ...
     int run_pos[6];          // ... (the TMA run index is deposited into them)
-    int phi_lane;            // lanes with this bit set read t XOR (1 << phi_t) (bank-conflict-free),
-    int phi_t;               // -1 if no target sits in cube ranks 0..3
+    int phi_t;               // lanes with column bit 3 set read t XOR (1 << phi_t) (bank-conflict
+                             // free); -1 if no target sits in cube ranks 0..3
     int nins;                // 13 cube positions + chunk bits, ascending
     int ins[17];
     uint64_t fixval;         // chunk bits (pipelined remaps), as K9
@@ -618,24 +623,21 @@ __device__ __forceinline__ void swap_words(uint32_t (&w)[16], bool f) {
     for (int i = 0; i < 16; i++)
         if (!((i >> B) & 1)) cswap(f, w[i], w[i | (1 << B)]);
 }
-__device__ __forceinline__ void unpermute16(uint32_t (&w)[16], bool f, int tb) {
-    if (tb == 0) {
+template <int TB>
+__device__ __forceinline__ void unpermute16(uint32_t (&w)[16], bool f) {
+    if (TB == 0) {
         const uint32_t sel = f ? 0x1032u : 0x3210u;
 #pragma unroll
         for (int i = 0; i < 16; i++) w[i] = __byte_perm(w[i], 0, sel);
-    } else if (tb == 1) {
-        swap_words<0>(w, f);
-    } else if (tb == 2) {
-        swap_words<1>(w, f);
-    } else if (tb == 3) {
-        swap_words<2>(w, f);
-    } else {
-        swap_words<3>(w, f);
+    } else if (TB > 0) {
+        swap_words<(TB > 0 ? TB - 1 : 0)>(w, f);
     }
 }
 
-template <bool PERM>
+// PT: the t bit the lanes with column bit 3 set flip (-1: none, no permutation)
+template <int PT>
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constant__ TcTArgs p) {
+    constexpr bool PERM = PT >= 0;
     extern __shared__ __align__(1024) uint8_t smem[];
     float2* raw = reinterpret_cast<float2*>(smem);                       // [2][8192] by cube index
     uint8_t* mat = smem + 2 * kTRaw;                                      // B hi | B lo (K-major)
@@ -730,8 +732,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         // ---------------- converters: thread j = 32 (w & 3) + lane, t in [32 (w >> 2), +32)
         const int q = warp & 3, th = warp >> 2;
         const int j = 32 * q + lane;
-        const bool pf = PERM && ((lane >> p.phi_lane) & 1);   // this lane reads t ^ (1 << phi_t)
-        const uint32_t phi = pf ? 1u << p.phi_t : 0u;
+        const bool pf = PERM && ((lane >> 3) & 1);   // this lane reads t ^ (1 << PT)
+        const uint32_t phi = pf ? 1u << (PERM ? PT : 0) : 0u;
         // cube index of (t = 32 th + (u ^ phi), j) = base ^ cube_t(u) with cube_t linear in u
         uint32_t base = 0;
         for (int k = 0; k < 7; k++)
@@ -751,6 +753,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             float2 v[32];   // v[u] = x(32 th + (u ^ phi), j)
             float mx = 0.f;
             uint32_t ci = base;
+            // keep the 32 addresses out of registers across tiles: recomputing them costs one XOR
+            // each, hoisting them out of the loop spills (local-memory traffic every tile)
+            asm volatile("" : "+r"(ci));
 #pragma unroll
             for (int g = 0; g < 32; g++) {   // Gray-code walk of u: one XOR per element
                 const int u = g ^ (g >> 1);
@@ -775,25 +780,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                 colexp[es * 128 + j] = (int8_t)E;
                 mbar_arrive(&cready[es]);
             }
-            // K order t + 64 c: word c < 32 packs re of t = 2c, 2c+1; word 32 + c the im parts
-            uint32_t hre[16], lre[16], him[16], lim[16];
-#pragma unroll
-            for (int u = 0; u < 16; u++) {
-                const float2 v0 = f2mul(v[2 * u], sc), v1 = f2mul(v[2 * u + 1], sc);
-                split_exact_h2(v0.x, v1.x, hre[u], lre[u]);
-                split_exact_h2(v0.y, v1.y, him[u], lim[u]);
-            }
-            if (PERM) {
-                unpermute16(hre, pf, p.phi_t);
-                unpermute16(him, pf, p.phi_t);
-                unpermute16(lre, pf, p.phi_t);
-                unpermute16(lim, pf, p.phi_t);
-            }
+            // K order t + 64 c: word c < 32 packs re of t = 2c, 2c+1; word 32 + c the im parts.
+            // Real parts first, then imaginary parts (keeps 32 packed words live, not 64).
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 128 * b + 16 * th;
-            TMEM_ST16(ta, hre);             // hi, re words [16 th, +16)
-            TMEM_ST16(ta + 32, him);        // hi, im words [32 + 16 th, +16)
-            TMEM_ST16(ta + 64, lre);        // lo
-            TMEM_ST16(ta + 96, lim);
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                uint32_t hw[16], lw[16];
+#pragma unroll
+                for (int u = 0; u < 16; u++) {
+                    const float x0 = (c ? v[2 * u].y : v[2 * u].x) * sc, x1 = (c ? v[2 * u + 1].y : v[2 * u + 1].x) * sc;
+                    split_exact_h2(x0, x1, hw[u], lw[u]);
+                }
+                if (PERM) {
+                    unpermute16<PT>(hw, pf);
+                    unpermute16<PT>(lw, pf);
+                }
+                TMEM_ST16(ta + 32 * c, hw);        // hi: re words [16 th, +16), im words [32 + 16 th, +16)
+                TMEM_ST16(ta + 64 + 32 * c, lw);   // lo
+            }
             asm volatile("tcgen05.wait::st.sync.aligned;");
             asm volatile("tcgen05.fence::before_thread_sync;");
             mbar_arrive(&afull[b]);
@@ -967,7 +971,6 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
     // bank-conflict-free converter reads: with one target at cube rank < 4, column bit 3 is
     // displaced to rank 4 and the lanes with it set read t ^ (that target's bit); t bit 5 (the
     // converter half) must not be it.  More low targets: K9 (tc_uses_k12).
-    p.phi_lane = 3;
     p.phi_t = -1;
     for (int i = 0; i < 6; i++)
         if (p.tcube[i] < 4) {
@@ -998,23 +1001,24 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
         }
     p.dstride = d;
     // the attribute is per device (context): set it before every launch (cheap)
-    cudaError_t e = perm ? cudaFuncSetAttribute(k_pass_tct<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem)
-                         : cudaFuncSetAttribute(k_pass_tct<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+    void (*kern)(TcTArgs) = nullptr;
+    switch (p.phi_t) {
+        case -1: kern = k_pass_tct<-1>; break;
+        case 0: kern = k_pass_tct<0>; break;
+        case 1: kern = k_pass_tct<1>; break;
+        case 2: kern = k_pass_tct<2>; break;
+        case 3: kern = k_pass_tct<3>; break;
+        case 4: kern = k_pass_tct<4>; break;
+        default: return cudaErrorInvalidValue;
+    }
+    (void)perm;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
     if (e != cudaSuccess) return e;
     count_launch();
-    if (perm)
-        k_pass_tct<true><<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
-    else
-        k_pass_tct<false><<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
+    kern<<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
     return cudaGetLastError();
 }
 
-// K12 (transposed) for n_local >= 13 unless two or more targets sit in positions 0..3: there the
-// converters' lane-dependent t permutation (bank-conflict-free reads) costs 2-2.5x a pass
-// (measured C4: 82-118 ms vs ~60 ms on K9, profiles/r02/pass_report_c4_k12all.txt), and K9's
-// B-stage path is faster.  Positions 0..6 hold qubits 0..6 in every sharding (planner pinning),
-// so the choice is a function of the block: the rounding of the cross terms is
-// sharding-independent.
 bool tc_uses_k12(int nl, const int* pos) {
     if (nl < 13) return false;
     int low = 0;
