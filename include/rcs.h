@@ -108,8 +108,11 @@ typedef struct {
     int overlap_chunks;      /* log2 chunks, 1..4 (0 -> 2)                                         */
     int overlap_sms;         /* SMs left to the swaps while passes run (0 -> 32 at world 2, 16 at
                                 world >= 4 and in loopback)                                        */
-    int tc_kernel;           /* 0: K12 for blocks with no target among positions 0..6, K9 otherwise
-                                (a function of the block: P-invariant); 1: K9 only (tests)         */
+    int tc_kernel;           /* 0: the transposed kernel K12 (any layout) when n_local >= 13 and at
+                                most one target sits in positions 0..3, K9 otherwise (a function of
+                                the block: P-invariant); 1: K9 only (tests, comparisons)           */
+    int overlap_passes;      /* pipelined remaps: how many tensor-core passes after the remap run
+                                chunk by chunk behind its swaps (0 -> 3; 1 = the next pass only)  */
 } rcs_build_opts;
 
 typedef struct {

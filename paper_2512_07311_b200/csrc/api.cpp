@@ -93,6 +93,7 @@ namespace {
 
 constexpr uint64_t kChunkShots = 1ull << 22;
 constexpr uint64_t kAlign = 256;
+constexpr int kOverlapPasses = 3;   // default passes after a remap pipelined behind its swaps
 
 uint64_t align_up(uint64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -545,9 +546,9 @@ struct PassRef {
     const uint32_t* d_a;
 };
 
-rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, const PassRef* pb, const int* fix,
-                              int cb, int reserve, bool force_k9, uint64_t* bytes_sent, uint64_t* pass_bytes,
-                              size_t ia, size_t ir, size_t ib, std::vector<Span>* spans,
+rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, const PassRef* pbs, int nb,
+                              const int* fix, int cb, int reserve, bool force_k9, uint64_t* bytes_sent,
+                              uint64_t* pass_bytes, size_t ia, size_t ir, const size_t* ibs, std::vector<Span>* spans,
                               std::vector<cudaEvent_t>* owned, rcs_error* err) {
     rcs_context* c = s->ctx;
     const int nch = 1 << cb;
@@ -597,20 +598,26 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
         }
         CUDA_TRY(cudaEventRecord(c->ev_s[ch], c->xstream));
     }
-    // B: chunk c after every rank exchanged chunk c
-    for (int ch = 0; ch < nch; ch++) {
-        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
-        if (pb) {
+    // B chain (nb passes after the remap), chunk c of the first one after every rank exchanged
+    // chunk c.  Anti-diagonal order (pass i of chunk c at step i + c): while the swap of chunk c
+    // is still on NVLink the main stream works on later passes of earlier chunks.
+    for (int d = 0; d < nb + nch - 1; d++)
+        for (int ch = 0; ch < nch; ch++) {
+            const int i = d - ch;
+            if (i < 0 || i >= nb) continue;
+            if (i == 0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
             cudaEvent_t w = spans ? tev(c->stream) : nullptr;
-            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pb->pos, pb->d_a, sms, c->stream, fix, cb, fixval(ch), force_k9));
+            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pbs[i].pos, pbs[i].d_a, sms, c->stream, fix, cb, fixval(ch),
+                                       force_k9));
             if (spans) {
-                cudaEvent_t d = tev(c->stream);
-                spans->push_back({ib, w, d, 1});
-                spans->push_back({ir, w, d, -1});
+                cudaEvent_t e = tev(c->stream);
+                spans->push_back({ibs[i], w, e, 1});
+                spans->push_back({ir, w, e, -1});
             }
         }
-    }
-    if (pb) *pass_bytes += 16ull * s->n_amps;
+    if (nb == 0)   // no pass after the remap: the main stream still waits for every chunk's swap
+        for (int ch = 0; ch < nch; ch++) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
+    *pass_bytes += 16ull * s->n_amps * (uint64_t)nb;
     if (spans) spans->push_back({ir, tA, tev(c->stream), 1});
     return RCS_OK;
 }
@@ -1009,6 +1016,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     if (o.remap_mode < RCS_REMAP_AUTO || o.remap_mode > RCS_REMAP_LOOPBACK ||
         (o.remap_mode == RCS_REMAP_LOOPBACK && (ctx->world != 1 || o.virtual_global < 1 || o.virtual_global > 3)) ||
         o.overlap_chunks < 0 || o.overlap_chunks > 4 || o.overlap_sms < 0 || o.tc_kernel < 0 || o.tc_kernel > 1 ||
+        o.overlap_passes < 0 || o.overlap_passes > 8 ||
         o.virtual_global < 0) {
         set_error(err, RCS_ERR_ARG, "invalid build options (remap_mode %d, virtual_global %d, overlap_chunks %d)",
                   o.remap_mode, o.virtual_global, o.overlap_chunks);
@@ -1180,6 +1188,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     const int ov_cb = o.overlap_chunks > 0 ? o.overlap_chunks : 2;
     const bool ov_on = o.overlap >= 0 && ov_cb <= 4 && peer_path;
     const int ov_res = o.overlap_sms > 0 ? o.overlap_sms : (ctx->world == 2 ? 32 : 16);
+    const int ov_chain = o.overlap_passes > 0 ? o.overlap_passes : kOverlapPasses;
     const int nl_loc = nl - (loopback(s) ? o.virtual_global : 0);   // local bits of one (virtual) rank
     auto is_tc = [&](size_t i) { return i < n_exec && P.items[i].type == RCS_ITEM_PASS && tc_slot[i] >= 0; };
     auto tc_ref = [&](size_t i) {
@@ -1193,21 +1202,34 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
                                                             P.items[ii + 1].type == RCS_ITEM_REMAP) ? ii + 1 : SIZE_MAX;
             if (ir != SIZE_MAX) {
                 const Item& rm = P.items[ir];
-                const bool has_a = ir != ii, has_b = is_tc(ir + 1);
+                const bool has_a = ir != ii;
                 uint64_t excl = 0;
                 for (int i = 0; i < rm.k; i++) excl |= 1ull << rm.b[i];
                 if (has_a) excl |= dev::tc_reserved_mask(nl, tcp->pos[ii].data());
-                if (has_b) excl |= dev::tc_reserved_mask(nl, tcp->pos[ir + 1].data());
                 int fix[4];
-                if ((has_a || has_b) && choose_chunk_bits(nl_loc, excl, ov_cb, fix)) {
-                    PassRef ra = has_a ? tc_ref(ii) : PassRef{}, rb = has_b ? tc_ref(ir + 1) : PassRef{};
-                    rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, has_b ? &rb : nullptr, fix, ov_cb,
-                                                      ov_res, force_k9, &remap_bytes, &pass_bytes, ii, ir, ir + 1,
-                                                      o.timing ? &spans : nullptr, &owned, err);
+                // the passes after the remap that run chunk by chunk behind the swaps: up to
+                // ov_chain consecutive tensor-core passes whose tile cubes leave ov_cb chunk bits,
+                // stopping before a pass that feeds the next remap (that one is the next group's A)
+                std::vector<PassRef> rb;
+                std::vector<size_t> ib;
+                for (size_t k = ir + 1; k < n_exec && (int)rb.size() < ov_chain && is_tc(k); k++) {
+                    if (!rb.empty() && k + 1 < n_exec && P.items[k + 1].type == RCS_ITEM_REMAP) break;
+                    const uint64_t ex = excl | dev::tc_reserved_mask(nl, tcp->pos[k].data());
+                    int f2[4];
+                    if (!choose_chunk_bits(nl_loc, ex, ov_cb, f2)) break;
+                    excl = ex;
+                    rb.push_back(tc_ref(k));
+                    ib.push_back(k);
+                }
+                if ((has_a || !rb.empty()) && choose_chunk_bits(nl_loc, excl, ov_cb, fix)) {
+                    PassRef ra = has_a ? tc_ref(ii) : PassRef{};
+                    rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, rb.data(), (int)rb.size(), fix,
+                                                      ov_cb, ov_res, force_k9, &remap_bytes, &pass_bytes, ii, ir,
+                                                      ib.data(), o.timing ? &spans : nullptr, &owned, err);
                     if (r) return fail(r);
                     n_pipelined++;
                     n_peer++;
-                    ii = has_b ? ir + 1 : ir;
+                    ii = rb.empty() ? ir : ib.back();
                     continue;
                 }
             }

@@ -63,7 +63,7 @@ constexpr uint32_t kRawBytes = 4096 * 8;
 constexpr uint32_t kBBytes = TN * TK * 2;    // 16 KB per fp16 hi or lo tile
 constexpr uint32_t kStageBytes = 2 * kBBytes;
 constexpr uint32_t kSBO = (TK / 8) * 128;    // next 8-row group (16 chunks of 16 B)
-constexpr int kPitchF = 130;                 // staging row pitch in floats (520 B): conflict-free
+constexpr int kPitchF = 128;                 // staging row t: 64 float2, column j at j ^ g(t) (swizzle)
 constexpr uint32_t kStagingBytes = 64 * kPitchF * 4;
 constexpr int kExpSlots = 4;                 // per-tile column exponents in flight (converter -> epilogue)
 constexpr uint32_t kCtlBytes = 2560;   // barriers + offset tables; total <= 227 KB
@@ -83,13 +83,17 @@ struct TcArgs {
     int sub[12];             // all 12 sub-cube positions, ascending (for the tile base deposit)
     int r;                   // sub[0..r) == 0..r-1: runs of 2^r contiguous amplitudes
     int pair;                // 2: tiles processed in adjacent pairs (ntiles >= 2), else 1
-    int sso[32];             // staging offset (floats) of sub-cube index 128 i
+    int sto[32];             // staging row offset (floats) of sub-cube index 128 i: t_i * 128
+    int sxj[32];             // ... and its swizzled column part j_i ^ g(t_i)
     uint64_t sgo[32];        // global offset (amplitudes) of sub-cube index 128 i
+    int gsh;                 // staging swizzle g(t) = rotate-left of t's 4 low bits by gsh
     int nins;                // 12 + number of fixed (chunk) bits
     int ins[16];             // sub-cube and fixed positions, ascending (tile base deposit)
     uint64_t fixval;         // value of the fixed bits (one chunk of the index space)
     uint64_t fmask;          // positions the tile index is deposited into (below n_local)
     uint64_t dstride;        // deposit of the per-CTA tile-pair stride (gridDim.x * pair)
+    int rot_lane[3];         // ROT: lane bit driving rotation bit m (t bits 0..2), -1: none
+    int to_lane;             // ROT: lane bit XORed into the octet index (t bit 3), -1: none
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -384,10 +388,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         const int j = lt & 63;
         const int to = lt >> 6;               // 0..3
         const int sj = sofj[j];
-        const int rho = ROT ? (lane & 7) : 0;
+        // ROT: the lane bits whose column ranks do not reach the banks (displaced by low targets)
+        // rotate the t octet (t bits 0..2) and flip t bit 3, so a half-warp reads 16 bank pairs
+        int rho = 0, tox = to;
+        if (ROT) {
+#pragma unroll
+            for (int m = 0; m < 3; m++)
+                if (p.rot_lane[m] >= 0) rho |= ((lane >> p.rot_lane[m]) & 1) << m;
+            if (p.to_lane >= 0) tox ^= (lane >> p.to_lane) & 1;
+        }
         int boff[16];   // raw-slot element offsets of this thread's 16 amplitudes (tile-invariant)
 #pragma unroll
-        for (int i = 0; i < 16; i++) boff[i] = soft[8 * (to + 4 * (i >> 3)) + ((i + rho) & 7)] | sj;
+        for (int i = 0; i < 16; i++) boff[i] = soft[8 * (tox + 4 * (i >> 3)) + ((i + rho) & 7)] | sj;
         uint64_t it = 0, bp = first_base;
         for (uint64_t tile = first_tile; tile < ntiles; next_tile(tile, bp), it++) {
             const int slot = (it >> (p.pair - 1)) & 1;
@@ -440,7 +452,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                     rot_h8(ih, rho);
                     rot_h8(il, rho);
                 }
-                const int c = to + 4 * g;                 // t octet -> K chunk (re); +8 (im)
+                const int c = tox + 4 * g;                // t octet -> K chunk (re); +8 (im)
                 const uint32_t ore = bchunk(j, c), oim = bchunk(j, c + 8);
                 *reinterpret_cast<uint4*>(bhi + ore) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
                 *reinterpret_cast<uint4*>(bhi + oim) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
@@ -496,8 +508,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
         int tb, jb;
         uint64_t gb;
         decomp(et, tb, jb, gb);
-        const float* sld = staging + tb * kPitchF + 2 * jb;
+        // staging swizzle: element (t, j) at float2 (64 t + (j ^ g(t))), g = a rotation of t's low
+        // 4 bits chosen on the host so that both the row-wise writes (16 rows per warp) and the
+        // memory-order reads (the 4 lowest cube ranks per half-warp: low targets + low columns)
+        // hit 16 distinct bank pairs
+        auto gsw = [&](int t) { const int x = t & 15; return ((x << p.gsh) | (x >> (4 - p.gsh))) & 15; };
+        const float* sld = staging + tb * kPitchF;
+        const int jbs = jb ^ gsw(tb);
         float* st = staging + trow * kPitchF + comp;
+        const int gw = gsw(trow);
         uint64_t it = 0, bp = first_base;
         for (uint64_t tile = first_tile; tile < ntiles; next_tile(tile, bp), it++) {
             const int d = it & 1;
@@ -507,6 +526,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + 128 + d * kAccCols;
             const int8_t* ce = colexp + es * 64;
+            // per-tile copies of the swizzle terms: hoisting the 64 + 32 swizzled offsets out of
+            // the tile loop would hold them in registers (spills)
+            int gwt = gw, jbt = jbs;
+            asm volatile("" : "+r"(gwt), "+r"(jbt));
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 uint32_t a0[32], a1[32];
@@ -534,15 +557,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                         "mov.b64 {%0, %1}, x;\n}"
                         : "=f"(o0), "=f"(o1)
                         : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(f0), "f"(f1), "f"(rowfac));
-                    st[2 * (32 * h + c)] = o0;
-                    st[2 * (32 * h + c) + 2] = o1;
+                    st[2 * ((32 * h + c) ^ gwt)] = o0;
+                    st[2 * ((32 * h + c + 1) ^ gwt)] = o1;
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
             float2* dst = p.amps + (base_of(tile, bp) | gb);
 #pragma unroll 8
             for (int i = 0; i < 32; i++) {
-                const float2 v = *reinterpret_cast<const float2*>(sld + p.sso[i]);
+                const float2 v = *reinterpret_cast<const float2*>(sld + p.sto[i] + 2 * (jbt ^ p.sxj[i]));
                 __stcs(dst + p.sgo[i], v);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");   // staging reused by the next tile
@@ -1080,12 +1103,38 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
                 if (p.jpos[k] == p.sub[b]) jj |= 1 << k;
             }
         }
-        p.sso[i] = t * kPitchF + 2 * jj;
+        p.sto[i] = t * kPitchF;
+        p.sxj[i] = jj;              // XORed with g(t) below, once the swizzle is known
         p.sgo[i] = go;
     }
-    // bank conflicts of the converters' reads: target bits among the 4 lowest sub-cube bits
-    int low_targets = 0;
-    for (int i = 0; i < 4; i++) low_targets += (int)((tmask >> p.sub[i]) & 1);
+    // bank conflicts of the converters' reads: with a targets among the 4 lowest sub-cube ranks,
+    // a lane bits (column bits 0..3) land on ranks >= 4; those lane bits drive the octet
+    // rotation (t bits 0..2) and t bit 3.  Pinning makes the low targets t bits 0..a-1; any
+    // other case keeps the plain lane & 7 rotation.
+    int low_targets = 0, lowt[6], disp[4], nd = 0;
+    for (int i = 0; i < 6; i++) {
+        int rk = 0;
+        while (p.sub[rk] != p.pos[i]) rk++;
+        if (rk < 4) lowt[low_targets++] = i;
+    }
+    for (int k = 0; k < 4; k++) {
+        int rk = 0;
+        while (p.sub[rk] != p.jpos[k]) rk++;
+        if (rk >= 4) disp[nd++] = k;
+    }
+    bool lowest = nd == low_targets;
+    for (int m = 0; m < low_targets; m++) lowest = lowest && lowt[m] == m;
+    for (int m = 0; m < 3; m++) p.rot_lane[m] = lowest ? (m < low_targets ? disp[m] : -1) : m;
+    p.to_lane = (lowest && low_targets == 4) ? disp[3] : -1;
+    // staging swizzle: the half-warp's memory-order reads vary the a low targets (t bits 0..a-1)
+    // and the 4-a lowest columns (j bits 0..3-a); rotating t's low 4 bits left by 4-a puts the
+    // targets on the column bits the reads do not vary (and keeps the 16 rows of a warp's writes
+    // on 16 distinct column slots)
+    p.gsh = lowest ? (4 - (low_targets < 4 ? low_targets : 4)) & 3 : 0;
+    for (int i = 0; i < 32; i++) {
+        const int t = p.sto[i] / kPitchF, x = t & 15;
+        p.sxj[i] ^= ((x << p.gsh) | (x >> (4 - p.gsh))) & 15;
+    }
     const uint64_t units = p.ntiles / p.pair;
     const uint64_t grid = units < (uint64_t)num_sms ? units : (uint64_t)num_sms;
     if (grid == 0) return cudaSuccess;
@@ -1099,7 +1148,7 @@ cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d
             }
         p.dstride = d;
     }
-    const bool rot = low_targets >= 2;
+    const bool rot = lowest ? low_targets >= 1 : low_targets >= 2;
     cudaError_t e = rot ? cudaFuncSetAttribute(k_pass_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)
                         : cudaFuncSetAttribute(k_pass_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     if (e != cudaSuccess) return e;

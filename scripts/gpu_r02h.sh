@@ -16,8 +16,9 @@ for name, t in (("c2", config_qasm("c2")), ("rand20", random_qasm(20, 400, 3)), 
             print(name, kern, st.report["n_passes"], np.abs(d).max(), np.linalg.norm(d), st.norm - 1, flush=True)
 PY
 rc=$?; cat gpurun_out/quick.log; [ $rc -eq 0 ] || { echo QUICK FAILED rc=$rc; exit 1; }
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r02e_bench.json 2> gpurun_out/r02e_bench.err; echo "bench rc=$?"
-python -c "import json;d=json.load(open('gpurun_out/r02e_bench.json'));print(d['ms_per_step'],d['value'],d['pass_gbs'],d['roofline']['frac'],d['clocks'],d['norm'])"
-timeout 300 python scripts/pass_report.py c4 6 > gpurun_out/r02e_pass_report.txt 2>&1; tail -45 gpurun_out/r02e_pass_report.txt
-timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r02e_gputests.log 2>&1; echo "pytest rc=$?"
-grep -E "^(FAILED|ERROR)|passed|failed" gpurun_out/r02e_gputests.log | tail -30
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r02h_bench.json 2> gpurun_out/r02h_bench.err; echo "bench rc=$?"
+python -c "import json;d=json.load(open('gpurun_out/r02h_bench.json'));print(d['ms_per_step'],d['value'],d['pass_gbs'],d['roofline']['frac'],d['clocks'],d['norm'])"
+timeout 300 python scripts/pass_report.py c4 6 > gpurun_out/r02h_pass_report.txt 2>&1; tail -45 gpurun_out/r02h_pass_report.txt
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r02h_gputests.log 2>&1; echo "pytest rc=$?"
+grep -E "^(FAILED|ERROR)|passed|failed" gpurun_out/r02h_gputests.log | tail -30
+NCU_SKIP_LIST=1 ./scripts/gpu_r02_ncu.sh

@@ -42,23 +42,30 @@ def check_amps(psi, ref):
     assert np.abs(d).max() <= 1e-5 and np.linalg.norm(d) <= 1e-5
 
 
-@pytest.mark.parametrize("overlap", [True, False])
+# pipelining: "chain" = the default (up to 3 passes after a remap run chunk by chunk behind its
+# swaps), "next" = only the pass right after the remap, "off" = sequential remaps
+OVERLAP = {"chain": {}, "next": {"overlap_passes": 1}, "off": {"overlap": False}}
+
+
+@pytest.mark.parametrize("mode", list(OVERLAP))
 @pytest.mark.parametrize("g", [1, 2, 3])
 @pytest.mark.parametrize("case", list(CASES))
-def test_loopback_remaps_bitwise(rcs, ctx, case, g, overlap):
+def test_loopback_remaps_bitwise(rcs, ctx, case, g, mode):
     text, k = CASES[case]
+    overlap = mode != "off"
     c = rcs.Circuit.from_qasm(text)
     single = rcs.State.build(ctx, c, fuse_k=k)
     psi1 = single.copy_out()
     x1 = single.sample(50_000, seed=SHOT_SEED)
     single.free()
-    st = rcs.State.build(ctx, c, fuse_k=k, virtual_global=g, remap_mode="loopback", overlap=overlap, timing=True)
+    st = rcs.State.build(ctx, c, fuse_k=k, virtual_global=g, remap_mode="loopback", timing=True, **OVERLAP[mode])
     rep = st.report
     assert rep["n_remaps"] > 0 and rep["n_peer_remaps"] > 0, rep
     if k == 6 and overlap:
         assert rep["n_pipelined"] > 0, rep          # chunked swaps overlapped with pass chunks
     if not overlap or k == 4:
         assert rep["n_pipelined"] == 0, rep
+    assert rep["n_passes"] == len(st.pass_times())
     assert rep["remap_bytes"] > 0 and rep["remap_kernel_ms"] > 0, rep
     psi = st.copy_out()
     assert np.array_equal(psi, psi1), case        # P-invariance through the peer-swap path

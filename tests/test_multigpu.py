@@ -37,9 +37,11 @@ def ngpus():
 
 
 # build options per mode (rcs_build_opts): p2p = NVLink peer swaps pipelined with the neighbouring
-# tensor-core passes (default); p2p_seq = not pipelined; p2p_c8 = 8 pipeline chunks; nccl =
+# tensor-core passes (default: up to 3 passes after each remap); p2p_seq = not pipelined; p2p_c8 =
+# 8 pipeline chunks, only the next pass behind the swaps; nccl =
 # grouped send/recv remaps through the staging area
-MODES = {"p2p": {}, "p2p_seq": {"overlap": False}, "p2p_c8": {"overlap_chunks": 3}, "nccl": {"remap_mode": "nccl"}}
+MODES = {"p2p": {}, "p2p_seq": {"overlap": False}, "p2p_c8": {"overlap_chunks": 3, "overlap_passes": 1},
+         "nccl": {"remap_mode": "nccl"}}
 
 
 @pytest.mark.parametrize("mode", list(MODES))
