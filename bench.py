@@ -62,6 +62,8 @@ def parse_args():
     ap.add_argument("--canonical", action="store_true", help="restore the canonical layout after every build")
     ap.add_argument("--no-overlap", action="store_true", help="sequential remaps (no pipelining with the passes)")
     ap.add_argument("--overlap-passes", type=int, default=0, help="passes after a remap pipelined behind it (0: default)")
+    ap.add_argument("--dynamic-tiles", action="store_true", help="K12 dynamic tile scheduler (default: static)")
+    ap.add_argument("--overlap-sms", type=int, default=0, help="SMs left to the pipelined swaps (0: default)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     return ap.parse_args()
 
@@ -247,7 +249,8 @@ def run_ours(args):
     mat_bytes = sum(8 * (1 << it["k"]) ** 2 for it in plan.items() if it["type"] == "pass")
     amps = torch.empty(1 << (n - g), dtype=torch.complex64, device=dev)
     keep = not args.canonical   # skip the final layout restore: samples/XEB are layout-independent
-    bopts = {"overlap": not args.no_overlap, "overlap_passes": args.overlap_passes}
+    bopts = {"overlap": not args.no_overlap, "overlap_passes": args.overlap_passes,
+             "overlap_sms": args.overlap_sms, "tc_schedule": "dynamic" if args.dynamic_tiles else "static"}
     st0 = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, amps=amps, keep_layout=keep, **bopts)   # sizes scratch
     scratch = st0.scratch
     st0.free()

@@ -113,6 +113,9 @@ typedef struct {
                                 the block: P-invariant); 1: K9 only (tests, comparisons)           */
     int overlap_passes;      /* pipelined remaps: how many tensor-core passes after the remap run
                                 chunk by chunk behind its swaps (0 -> 3; 1 = the next pass only)  */
+    int tc_schedule;         /* K12 tiles: 0 = static round robin (blockIdx + k gridDim), 1 = dynamic
+                                (a device counter hands tiles to the SMs as they free up; measured
+                                5 % slower at C4, profiles/r02/tiles_ab.txt)                      */
 } rcs_build_opts;
 
 typedef struct {

@@ -215,7 +215,8 @@ class State:
     def build(cls, ctx: Context, circuit: Circuit, fuse_k: int = 0, block_bits: int = 0, virtual_global: int = 0,
               timing: bool = False, staging_bytes: int = 0, amps=None, scratch=None,
               keep_layout: bool = False, remap_mode: str = "auto", overlap: bool = True, overlap_chunks: int = 0,
-              overlap_sms: int = 0, tc_kernel: str = "auto", overlap_passes: int = 0) -> "State":
+              overlap_sms: int = 0, tc_kernel: str = "auto", overlap_passes: int = 0,
+              tc_schedule: str = "static") -> "State":
         """rcs_state_build.  remap_mode: "auto" | "nccl" | "loopback" (world 1 + virtual_global: remaps
         through the NVLink peer-swap kernel between regions of this GPU); tc_kernel: "auto" | "k9"."""
         import torch
@@ -223,7 +224,8 @@ class State:
         g = ctx.world.bit_length() - 1
         opts = rcs_build_opts(fuse_k, block_bits, virtual_global, 1 if timing else 0, staging_bytes,
                               1 if keep_layout else 0, REMAP_MODES[remap_mode], 0 if overlap else -1,
-                              overlap_chunks, overlap_sms, {"auto": 0, "k9": 1}[tc_kernel], overlap_passes)
+                              overlap_chunks, overlap_sms, {"auto": 0, "k9": 1}[tc_kernel], overlap_passes,
+                              {"static": 0, "dynamic": 1}[tc_schedule])
         sb = C.c_uint64()
         check(lib().rcs_state_scratch_bytes(ctx._h, circuit._h, C.byref(opts), C.byref(sb)), None,
               "rcs_state_scratch_bytes")

@@ -46,6 +46,7 @@ struct rcs_context {
     // pipelined remaps (f1): a second stream for the chunked peer swaps + per-chunk events
     cudaStream_t xstream = nullptr;
     cudaEvent_t ev_a[16] = {}, ev_s[16] = {};
+    unsigned* d_tiles = nullptr;      // dynamic tile counter of the tensor-core passes (K12)
     // sampling / XEB chunk buffers, shared by every state of this context
     unsigned long long* xbuf = nullptr;
     double* dbuf = nullptr;
@@ -87,6 +88,7 @@ struct rcs_state {
     // execution options of the build (rcs_build_opts), reused by rcs_state_canonicalize
     int remap_mode = RCS_REMAP_AUTO;
     int virt = 0;                    // virtual global qubits (world 1)
+    unsigned* tiles = nullptr;       // K12 dynamic tile counter (the context's), nullptr: static tiles
 };
 
 namespace {
@@ -571,7 +573,8 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
     // A: all chunks, in order, on the main stream
     for (int ch = 0; ch < nch; ch++) {
         if (pa)
-            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch), force_k9));
+            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch), force_k9,
+                                       s->tiles));
         CUDA_TRY(cudaEventRecord(c->ev_a[ch], c->stream));
     }
     if (pa) *pass_bytes += 16ull * s->n_amps;
@@ -608,7 +611,7 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
             if (i == 0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
             cudaEvent_t w = spans ? tev(c->stream) : nullptr;
             CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pbs[i].pos, pbs[i].d_a, sms, c->stream, fix, cb, fixval(ch),
-                                       force_k9));
+                                       force_k9, s->tiles));
             if (spans) {
                 cudaEvent_t e = tev(c->stream);
                 spans->push_back({ibs[i], w, e, 1});
@@ -981,6 +984,7 @@ void rcs_context_free(rcs_context* c) {
     if (c->xeb_part) cudaFree(c->xeb_part);
     if (c->bad) cudaFree(c->bad);
     if (c->d_tc) cudaFree(c->d_tc);
+    if (c->d_tiles) cudaFree(c->d_tiles);
     for (int i = 0; i < 16; i++)
         for (cudaEvent_t e : {c->ev_a[i], c->ev_s[i]})
             if (e) cudaEventDestroy(e);
@@ -1016,7 +1020,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     if (o.remap_mode < RCS_REMAP_AUTO || o.remap_mode > RCS_REMAP_LOOPBACK ||
         (o.remap_mode == RCS_REMAP_LOOPBACK && (ctx->world != 1 || o.virtual_global < 1 || o.virtual_global > 3)) ||
         o.overlap_chunks < 0 || o.overlap_chunks > 4 || o.overlap_sms < 0 || o.tc_kernel < 0 || o.tc_kernel > 1 ||
-        o.overlap_passes < 0 || o.overlap_passes > 8 ||
+        o.overlap_passes < 0 || o.overlap_passes > 8 || o.tc_schedule < 0 || o.tc_schedule > 1 ||
         o.virtual_global < 0) {
         set_error(err, RCS_ERR_ARG, "invalid build options (remap_mode %d, virtual_global %d, overlap_chunks %d)",
                   o.remap_mode, o.virtual_global, o.overlap_chunks);
@@ -1167,6 +1171,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         rcs_status r = setup_peers(ctx, s->amps, o.remap_mode, err);
         if (r) return fail(r);
     }
+    if (n_tc > 0 && !ctx->d_tiles && o.tc_schedule == 1) BUILD_TRY(cudaMalloc(&ctx->d_tiles, 64));
+    s->tiles = o.tc_schedule == 1 ? ctx->d_tiles : nullptr;
     BUILD_TRY(cudaEventRecord(eb0, stream));
     if (tc_upload) {
         BUILD_TRY(cudaMemcpyAsync(ctx->d_tc, tcp->words.data(), tc_words * sizeof(uint32_t), cudaMemcpyHostToDevice,
@@ -1242,7 +1248,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         }
         if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
             BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tcp->pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
-                                        ctx->num_sms, stream, nullptr, 0, 0, force_k9));
+                                        ctx->num_sms, stream, nullptr, 0, 0, force_k9, s->tiles));
             pass_bytes += 16ull * n_amps;
         } else if (it.type == RCS_ITEM_PASS) {
             const Block& B = P.blocks[it.block];

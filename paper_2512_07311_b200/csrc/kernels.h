@@ -24,9 +24,11 @@ void tc_pack_matrix(const double* u_re_im, uint32_t* out);
 // sits in positions 0..3 (tc_uses_k12: a function of the block, positions 0..6 being pinned);
 // K9 otherwise, or for every block with force_k9 (tests, comparisons).
 bool tc_uses_k12(int n_local_bits, const int* pos);
+// tile_counter (one device word, may be nullptr): K12 hands tiles out through it (zeroed here,
+// stream-ordered) instead of the static blockIdx.x + k gridDim.x assignment.
 cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const uint32_t* d_a, int num_sms,
                          cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0,
-                         bool force_k9 = false);
+                         bool force_k9 = false, unsigned* tile_counter = nullptr);
 // positions a chunk bit must avoid for this pass: the 12-bit tile sub-cube and the bit above its run
 uint64_t tc_reserved_mask(int n_local_bits, const int* pos);
 // a6 (K1) fused dense gate pass: amps <- M (x) over every group of 2^k amplitudes that

@@ -621,12 +621,15 @@ struct TcTArgs {
     int ins[17];
     uint64_t fixval;         // chunk bits (pipelined remaps), as K9
     uint64_t fmask, dstride; // tile-index deposit (as K9)
+    unsigned* counter;       // dynamic tile scheduler (zeroed before the launch), nullptr: static
 };
 
-constexpr uint32_t kTRaw = 8192 * 8;                  // one tile: 64 KB
+constexpr uint32_t kTRaw = 8192 * 8;
+constexpr int kTRing = 8;                             // tile bases in flight (producer -> all roles)
+constexpr uint64_t kTileEnd = ~0ull;                  // ring sentinel: no more tiles                  // one tile: 64 KB
 constexpr uint32_t kTMat = 2 * 128 * 128 * 2;         // B hi + lo: 64 KB
 constexpr uint32_t kTCtl = 3584;
-static_assert((10 + kExpSlots) * 8 + 64 * 8 + 64 * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl,
+static_assert((10 + kExpSlots) * 8 + 64 * 8 + 64 * 8 + kTRing * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl,
               "K12 control block");
 constexpr uint32_t kTSmem = 2 * kTRaw + kTMat + kTCtl;
 
@@ -674,7 +677,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     uint64_t* cready = dempty + 1;                        // [kExpSlots] column exponents of a tile written
     uint64_t* offt = cready + kExpSlots;                  // [64] physical offset of target combination t
     uint64_t* offr = offt + 64;                           // [64] physical offset of TMA run u
-    int* cmax = reinterpret_cast<int*>(offr + 64);        // [3][128] column max |x| (float bits)
+    uint64_t* tring = offr + 64;                          // [kTRing] tile base of iteration it (or kTileEnd)
+    int* cmax = reinterpret_cast<int*>(tring + kTRing);   // [3][128] column max |x| (float bits)
     float* rowfac = reinterpret_cast<float*>(cmax + 3 * 128);   // [64] 2^-F_t
     int8_t* colexp = reinterpret_cast<int8_t*>(rowfac + 64);     // [kExpSlots][128] E_j per tile
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colexp + kExpSlots * 128);
@@ -731,16 +735,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     const uint64_t first = blockIdx.x;
 
     if (warp == kProdWarp) {
+        // The producer decides the tile sequence and publishes each tile's base in tring (read by
+        // the other roles after the mbarrier chain rfull -> afull -> cready/dfull); kTileEnd ends
+        // every role's loop.  Dynamic mode: tiles from a global atomic counter, so SMs that run
+        // faster (HBM placement, die) take more tiles; static: blockIdx.x + k gridDim.x.
         const int nruns = 1 << p.nrun_pos;
         const uint32_t run_bytes = 8u << p.r;
-        uint64_t it = 0, bp = tile_base(first);
-        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
+        uint64_t it = 0, bp = tile_base(first), tile = first;
+        unsigned nxt = 0;
+        if (p.counter) {
+            if (lane == 0) nxt = atomicAdd(p.counter, 1u);
+            tile = __shfl_sync(0xffffffffu, nxt, 0);
+        }
+        for (;; it++) {
             const int slot = it & 1;
             mbar_wait(&rempty[slot], ((it >> 1) & 1) ^ 1);
-            if (lane == 0)
+            if (tile >= ntiles) {
+                if (lane == 0) {
+                    tring[it % kTRing] = kTileEnd;
+                    mbar_arrive(&rfull[slot]);   // completes the phase without data
+                }
+                break;
+            }
+            if (p.counter) {
+                bp = tile_base(tile);
+                if (lane == 0) nxt = atomicAdd(p.counter, 1u);   // next tile, in flight during this copy
+            }
+            if (lane == 0) {
+                tring[it % kTRing] = bp | p.fixval;
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[slot])),
                              "r"(kTRaw)
                              : "memory");
+            }
             __syncwarp();
             const float2* src = p.amps + (bp | p.fixval);
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
@@ -750,6 +776,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                         dst + u * run_bytes),
                     "l"(src + offr[u]), "r"(run_bytes), "r"(su32(&rfull[slot]))
                     : "memory");
+            if (p.counter) {
+                tile = __shfl_sync(0xffffffffu, nxt, 0);
+            } else {
+                tile += gridDim.x;
+                bp = ((bp | ~p.fmask) + p.dstride) & p.fmask;
+            }
         }
     } else if (warp < kLoadWarps) {
         // ---------------- converters: thread j = 32 (w & 3) + lane, t in [32 (w >> 2), +32)
@@ -768,10 +800,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             R[i] = 1u << p.tcube[i];
             if (PERM && ((phi >> i) & 1)) base ^= R[i];
         }
-        uint64_t it = 0;
-        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++) {
+        for (uint64_t it = 0;; it++) {
             const int slot = it & 1, b = it & 1;
             mbar_wait(&rfull[slot], (it >> 1) & 1);
+            if (tring[it % kTRing] == kTileEnd) {   // end: hand the MMA warp its last phase
+                mbar_wait(&aempty[b], ((it >> 1) & 1) ^ 1);
+                mbar_arrive(&afull[b]);
+                break;
+            }
             const float2* rb = raw + (size_t)slot * 8192;
             float2 v[32];   // v[u] = x(32 th + (u ^ phi), j)
             float mx = 0.f;
@@ -829,11 +865,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         // ---------------- MMA issuer: M = 128 (j), N = 128 (n = 2 t_o + c_o), K = 16 per step
         const uint32_t idesc = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         const uint64_t bh0 = bdesc(su32(mat)), bl0 = bdesc(su32(mat + kTMat / 2));
-        uint64_t it = 0;
-        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++) {
+        for (uint64_t it = 0;; it++) {
             const int b = it & 1;
             mbar_wait(&afull[b], (it >> 1) & 1);
             mbar_wait(dempty, (it & 1) ^ 1);
+            if (tring[it % kTRing] == kTileEnd) {   // end: hand the epilogue its last phase
+                if (lane == 0) mbar_arrive(dfull);
+                break;
+            }
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
                 const uint32_t d0 = tmem + 256;
@@ -863,14 +902,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         uint64_t offj = 0;
         for (int k = 0; k < 7; k++)
             if ((j >> k) & 1) offj |= 1ull << p.jpos[k];
-        uint64_t it = 0, bp = tile_base(first);
-        for (uint64_t tile = first; tile < ntiles; tile += gridDim.x, it++, bp = ((bp | ~p.fmask) + p.dstride) & p.fmask) {
+        for (uint64_t it = 0;; it++) {
             const int es = (int)(it % kExpSlots);
-            mbar_wait(&cready[es], (uint32_t)((it / kExpSlots) & 1));
-            const float cf = pow2f(-(int)colexp[es * 128 + j]);   // 2^-E_j (read before releasing D)
             mbar_wait(dfull, it & 1);
+            // the end marker is visible here (the MMA warp's plain arrive releases it); a tile's
+            // base is guaranteed visible after cready (the converters read it after rfull)
+            if (tring[it % kTRing] == kTileEnd) break;
+            mbar_wait(&cready[es], (uint32_t)((it / kExpSlots) & 1));
+            const uint64_t tb = tring[it % kTRing];
+            const float cf = pow2f(-(int)colexp[es * 128 + j]);   // 2^-E_j (read before releasing D)
             asm volatile("tcgen05.fence::after_thread_sync;");
-            float2* dst = p.amps + (bp | p.fixval | offj);
+            float2* dst = p.amps + (tb | offj);
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256;
 #pragma unroll
             for (int s4 = 0; s4 < 4; s4++) {   // 32 columns n = 16 target combinations (re, im)
@@ -959,10 +1001,11 @@ uint64_t tc_reserved_mask(int nl, const int* pos) {
 
 // K12 launcher: any target layout, n_local >= 13 (+ chunk bits)
 static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms,
-                                 cudaStream_t st, const int* fix, int nfix, uint64_t fixval) {
+                                 cudaStream_t st, const int* fix, int nfix, uint64_t fixval, unsigned* counter) {
     TcTArgs p{};
     p.amps = amps;
     p.a = d_a;
+    p.counter = counter;
     if (nl < 13 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     p.ntiles = 1ull << (nl - 13 - nfix);
     uint64_t tmask = 0;
@@ -1037,6 +1080,7 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
     (void)perm;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
     if (e != cudaSuccess) return e;
+    if (counter && (e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     count_launch();
     kern<<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
     return cudaGetLastError();
@@ -1050,8 +1094,9 @@ bool tc_uses_k12(int nl, const int* pos) {
 }
 
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
-                         const int* fix, int nfix, uint64_t fixval, bool force_k9) {
-    if (!force_k9 && tc_uses_k12(nl, pos)) return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval);
+                         const int* fix, int nfix, uint64_t fixval, bool force_k9, unsigned* tile_counter) {
+    if (!force_k9 && tc_uses_k12(nl, pos))
+        return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval, tile_counter);
     if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
     p.amps = amps;

@@ -109,6 +109,25 @@ def test_transposed_pass_matches_k9(rcs, ctx, n):
         check_amps(pa, oracle.build_state(text))
 
 
+@pytest.mark.parametrize("case", ["c2", "c3"])
+def test_dynamic_tile_schedule_bitwise(rcs, ctx, case):
+    """K12's optional dynamic scheduler hands tiles to the SMs through a device counter; the
+    arithmetic of a tile does not depend on the SM that runs it, so the state equals the static
+    round-robin schedule (the default) bit for bit (C3: n = 32, the first and last 4M amplitudes)."""
+    c = rcs.Circuit.from_qasm(config_qasm(case))
+    a = rcs.State.build(ctx, c, fuse_k=6, tc_schedule="dynamic")
+    if case == "c3":
+        pa = (a.copy_out(0, 1 << 22), a.copy_out((1 << 32) - (1 << 22), 1 << 22))
+    else:
+        pa = (a.copy_out(),)
+    na = a.norm
+    a.free()
+    b = rcs.State.build(ctx, c, fuse_k=6, tc_schedule="static")
+    pb = (b.copy_out(0, 1 << 22), b.copy_out((1 << 32) - (1 << 22), 1 << 22)) if case == "c3" else (b.copy_out(),)
+    assert all(np.array_equal(x, y) for x, y in zip(pa, pb))
+    assert na == b.norm
+
+
 @pytest.mark.parametrize("g", [1, 2, 3])
 def test_keep_layout_matches_canonical(rcs, ctx, g):
     """keep_layout skips the final restore; the logical-order CDF over the permuted layout gives
