@@ -39,6 +39,15 @@ METRIC = "fused gate-pass HBM GB/s (whole RCS step: state build + shots + XEB)"
 # Fused passes per config and fuse_k of the library's planner (P-independent).  The reference
 # arm converts oracle time into the same unit with this table instead of calling our engine;
 # tests/test_bench.py keeps it equal to rcs_plan_create's output.
+# leading blocks written as a product state (rcs_plan_prefix: one write-only kernel replaces the
+# state initialisation and these passes), likewise kept equal to the planner
+PLAN_PREFIX = {'c1': {3: 4, 4: 2, 5: 2, 6: 2},
+               'c2': {3: 2, 4: 5, 5: 1, 6: 1},
+               'c3': {3: 4, 4: 8, 5: 2, 6: 4},
+               'c4': {3: 3, 4: 2, 5: 1, 6: 5},
+               'c5': {3: 3, 4: 2, 5: 1, 6: 6},
+               'w33': {3: 3, 4: 6, 5: 4, 6: 2},
+               'w35': {3: 5, 4: 6, 5: 5, 6: 2}}
 PLAN_PASSES = {'c1': {3: 32, 4: 19, 5: 14, 6: 8},
                'c2': {3: 97, 4: 47, 5: 37, 6: 27},
                'c3': {3: 99, 4: 56, 5: 43, 6: 31},
@@ -64,6 +73,7 @@ def parse_args():
     ap.add_argument("--overlap-passes", type=int, default=0, help="passes after a remap pipelined behind it (0: default)")
     ap.add_argument("--dynamic-tiles", action="store_true", help="K12 dynamic tile scheduler (default: static)")
     ap.add_argument("--overlap-sms", type=int, default=0, help="SMs left to the pipelined swaps (0: default)")
+    ap.add_argument("--no-prefix", action="store_true", help="run the product-state prefix blocks as passes")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     return ap.parse_args()
 
@@ -246,11 +256,11 @@ def run_ours(args):
     n = cfg["n_qubits"]
     g = world.bit_length() - 1
     plan = rcs.Plan(circuit, args.fuse_k, g)
-    mat_bytes = sum(8 * (1 << it["k"]) ** 2 for it in plan.items() if it["type"] == "pass")
     amps = torch.empty(1 << (n - g), dtype=torch.complex64, device=dev)
     keep = not args.canonical   # skip the final layout restore: samples/XEB are layout-independent
     bopts = {"overlap": not args.no_overlap, "overlap_passes": args.overlap_passes,
-             "overlap_sms": args.overlap_sms, "tc_schedule": "dynamic" if args.dynamic_tiles else "static"}
+             "overlap_sms": args.overlap_sms, "tc_schedule": "dynamic" if args.dynamic_tiles else "static",
+             "product_prefix": not args.no_prefix}
     st0 = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, amps=amps, keep_layout=keep, **bopts)   # sizes scratch
     scratch = st0.scratch
     st0.free()
@@ -311,9 +321,11 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
+    up_bytes = 0
     for _ in range(e2e_steps):
         c2 = rcs.Circuit.from_qasm(text)                       # host QASM in
         st = rcs.State.build(ctx, c2, fuse_k=args.fuse_k, amps=amps, scratch=scratch, keep_layout=keep, **bopts)
+        up_bytes = st.report["upload_bytes"]                   # plan operands copied by this build
         xh = st.sample(shots, seed=SHOT_SEED)                  # bitstrings to host
         xr_h = st.xeb(xh)                                      # XEB from the host array
         st.free()
@@ -367,7 +379,8 @@ def run_ours(args):
             "shots_per_s": shots / (statistics.median(sample_ms) / 1e3),
             "shots_per_s_incl_blocksum": shots / ((statistics.median(sample_ms) + R["blocksum_ms"]) / 1e3),
             "xeb": X["F"], "xeb_sigma": X["sigma"], "fstar": X["fstar"], "norm": R["norm"],
-            "n_passes": R["n_passes"], "n_remaps": R["n_remaps"], "n_swaps": R["n_swaps"],
+            "n_passes": R["n_passes"], "n_prefix": R["n_prefix"], "prefix_ms": R["prefix_ms"],
+            "n_remaps": R["n_remaps"], "n_swaps": R["n_swaps"],
             "layout_kept": R["layout_kept"],
             "pass_gbs": {"min": gbs[0], "median": gbs[len(gbs) // 2], "max": gbs[-1]},
             "pass_ms_total": R["pass_ms"], "remap_ms_total": R["remap_ms"], "swap_ms_total": R["swap_ms"],
@@ -391,7 +404,7 @@ def run_ours(args):
                          "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "steps": e2e_steps, "ms_per_step": e2e_ms / max(1, e2e_steps),
-                    "h2d_bytes_per_step": mat_bytes + 8 * shots, "d2h_bytes_per_step": 8 * shots + 8,
+                    "h2d_bytes_per_step": up_bytes + 8 * shots, "d2h_bytes_per_step": 8 * shots + 8,
                     "xeb": xr_h["F"] if e2e_steps else None},
             "gpu_launches": launches,
             "clocks": clk,
@@ -414,7 +427,10 @@ def run_reference(args):
     cfg, shots, desc = workload(args)
     n = cfg["n_qubits"]
     world = args.gpus
-    step_bytes = PLAN_PASSES[args.config][args.fuse_k] * 16.0 * (1 << n)
+    # the step's algorithmic bytes as the library counts them: 16 B per amplitude per executed pass
+    # + 8 B per amplitude for the product-state prefix kernel (write only)
+    npf = PLAN_PREFIX[args.config][args.fuse_k]
+    step_bytes = ((PLAN_PASSES[args.config][args.fuse_k] - npf) * 16.0 + (8.0 if npf else 0.0)) * (1 << n)
     budget = max(2.0, min(args.cpu_budget, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_sample(args.config, cfg, shots, budget)

@@ -113,6 +113,9 @@ typedef struct {
                                 the block: P-invariant); 1: K9 only (tests, comparisons)           */
     int overlap_passes;      /* pipelined remaps: how many tensor-core passes after the remap run
                                 chunk by chunk behind its swaps (0 -> 3; 1 = the next pass only)  */
+    int product_prefix;      /* 0: the leading fused blocks on pairwise disjoint qubits (they act on
+                                |0...0>) are written as one product state by a write-only kernel
+                                (init + those passes replaced); -1: run them as passes            */
     int tc_schedule;         /* K12 tiles: 0 = static round robin (blockIdx + k gridDim), 1 = dynamic
                                 (a device counter hands tiles to the SMs as they free up; measured
                                 5 % slower at C4, profiles/r02/tiles_ab.txt)                      */
@@ -142,6 +145,12 @@ typedef struct {
     double remap_kernel_ms;  /* timing=1: device time of the remap data movement alone (peer-swap
                                 kernels / NCCL send-recv, first start to last end per remap, also
                                 when hidden behind pass chunks): NVLink GB/s = remap_bytes / it  */
+    int n_prefix;            /* fused blocks written as a product state (not counted in n_passes;
+                                pass_bytes counts their kernel as 8 B per amplitude, write only)  */
+    double prefix_ms;        /* timing=1: device time of the product-state kernel                */
+    uint64_t upload_bytes;   /* host -> device bytes this build copied (tensor-core operands and
+                                product-state tables when not cached for this circuit, layout
+                                tables)                                                          */
 } rcs_build_report;
 
 typedef struct {
@@ -191,6 +200,10 @@ void rcs_circuit_free(rcs_circuit *c);
  * independent of n_global. */
 rcs_status rcs_plan_create(const rcs_circuit *c, int fuse_k, int n_global, rcs_plan **out, rcs_error *err);
 rcs_status rcs_plan_summary(const rcs_plan *p, int *n_items, int *n_passes, int *n_remaps, int *n_swaps);
+/* Product-state prefix: items [0, *n_prefix) are passes on pairwise disjoint qubits applied to
+ * |0...0>; rcs_state_build writes their product state with one kernel (rcs_build_opts
+ * product_prefix) -- a function of the fused blocks, independent of n_global. */
+rcs_status rcs_plan_prefix(const rcs_plan *p, int *n_prefix);
 /* matrix_out (may be NULL): 2 * 4^k doubles, row-major interleaved complex, fp64 product. */
 rcs_status rcs_plan_item_get(const rcs_plan *p, int i, rcs_plan_item *out, double *matrix_out);
 /* Layout bookkeeping of the plan (host): items [*restore_begin, n_items) only restore the

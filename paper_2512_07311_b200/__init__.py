@@ -114,9 +114,11 @@ class Plan:
         err = rcs_error()
         check(lib().rcs_plan_create(circuit._h, fuse_k, n_global, C.byref(h), C.byref(err)), err, "rcs_plan_create")
         self._h = h
-        ni, npa, nr, ns = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        ni, npa, nr, ns, npf = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int()
         lib().rcs_plan_summary(h, C.byref(ni), C.byref(npa), C.byref(nr), C.byref(ns))
+        lib().rcs_plan_prefix(h, C.byref(npf))
         self.n_items, self.n_passes, self.n_remaps, self.n_swaps = ni.value, npa.value, nr.value, ns.value
+        self.prefix = npf.value   # items [0, prefix): product-state prefix (disjoint blocks on |0...0>)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -216,7 +218,7 @@ class State:
               timing: bool = False, staging_bytes: int = 0, amps=None, scratch=None,
               keep_layout: bool = False, remap_mode: str = "auto", overlap: bool = True, overlap_chunks: int = 0,
               overlap_sms: int = 0, tc_kernel: str = "auto", overlap_passes: int = 0,
-              tc_schedule: str = "static") -> "State":
+              tc_schedule: str = "static", product_prefix: bool = True) -> "State":
         """rcs_state_build.  remap_mode: "auto" | "nccl" | "loopback" (world 1 + virtual_global: remaps
         through the NVLink peer-swap kernel between regions of this GPU); tc_kernel: "auto" | "k9"."""
         import torch
@@ -225,7 +227,7 @@ class State:
         opts = rcs_build_opts(fuse_k, block_bits, virtual_global, 1 if timing else 0, staging_bytes,
                               1 if keep_layout else 0, REMAP_MODES[remap_mode], 0 if overlap else -1,
                               overlap_chunks, overlap_sms, {"auto": 0, "k9": 1}[tc_kernel], overlap_passes,
-                              {"static": 0, "dynamic": 1}[tc_schedule])
+                              0 if product_prefix else -1, {"static": 0, "dynamic": 1}[tc_schedule])
         sb = C.c_uint64()
         check(lib().rcs_state_scratch_bytes(ctx._h, circuit._h, C.byref(opts), C.byref(sb)), None,
               "rcs_state_scratch_bytes")

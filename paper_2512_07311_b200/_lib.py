@@ -32,7 +32,7 @@ class rcs_build_opts(C.Structure):
                 ("timing", C.c_int), ("staging_bytes", C.c_uint64), ("keep_layout", C.c_int),
                 ("remap_mode", C.c_int), ("overlap", C.c_int), ("overlap_chunks", C.c_int),
                 ("overlap_sms", C.c_int), ("tc_kernel", C.c_int), ("overlap_passes", C.c_int),
-                ("tc_schedule", C.c_int)]
+                ("product_prefix", C.c_int), ("tc_schedule", C.c_int)]
 
 
 class rcs_build_report(C.Structure):
@@ -42,7 +42,8 @@ class rcs_build_report(C.Structure):
                 ("blocksum_ms", C.c_double), ("pass_bytes", C.c_uint64), ("remap_bytes", C.c_uint64),
                 ("norm", C.c_double), ("n_tc_passes", C.c_int), ("swap_ms", C.c_double),
                 ("layout_kept", C.c_int), ("n_pipelined", C.c_int), ("n_peer_remaps", C.c_int),
-                ("remap_kernel_ms", C.c_double)]
+                ("remap_kernel_ms", C.c_double), ("n_prefix", C.c_int), ("prefix_ms", C.c_double),
+                ("upload_bytes", C.c_uint64)]
 
 
 class rcs_sample_report(C.Structure):
@@ -75,6 +76,7 @@ SIGNATURES = {
     "rcs_circuit_free": (None, [VP]),
     "rcs_plan_create": (C.c_int, [VP, C.c_int, C.c_int, PP, E]),
     "rcs_plan_summary": (C.c_int, [VP, IP, IP, IP, IP]),
+    "rcs_plan_prefix": (C.c_int, [VP, IP]),
     "rcs_plan_item_get": (C.c_int, [VP, C.c_int, C.POINTER(rcs_plan_item), DP]),
     "rcs_plan_free": (None, [VP]),
     "rcs_plan_layout": (C.c_int, [VP, IP, IP, IP]),

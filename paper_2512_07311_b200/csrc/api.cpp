@@ -36,6 +36,11 @@ struct rcs_context {
     uint64_t tc_uid = 0;                          // circuit / pack whose matrices d_tc holds
     const rcs::TcPack* tc_pack = nullptr;
     std::shared_ptr<const rcs::TcPack> tc_hold;   // keeps that pack alive
+    // product-state prefix operands (device copy of a PrefixPack: tab A | tab B | byte tables)
+    char* d_pf = nullptr;
+    size_t pf_cap = 0;
+    const rcs::PrefixPack* pf_pack = nullptr;
+    std::shared_ptr<const rcs::PrefixPack> pf_hold;
     // remaps over NVLink: CUDA-IPC mappings of the peers' shards (re-checked every build)
     bool p2p = false;                 // every rank mapped every peer (agreed over all ranks)
     char* d_xchg = nullptr;           // device buffer for the handle all-gather
@@ -276,6 +281,40 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
             m = padded.data();
         }
         dev::tc_pack_matrix(reinterpret_cast<const double*>(m), out.words.data() + (size_t)out.slot[ii] * each);
+    }
+}
+
+// Product-state prefix operands for a plan at n physical bits: the group tables and, for every
+// byte of the physical index, which group-table bits its bits hold (initial layout).
+void make_prefix_pack(const Plan& P, PrefixPack& out) {
+    const int n = P.n;
+    std::vector<int> occ(n);
+    for (int q = 0; q < n; q++) occ[P.initial_pos.empty() ? q : P.initial_pos[q]] = q;
+    out.nbytes = (n + 7) / 8;
+    out.byt.assign((size_t)2 * out.nbytes * 256, 0u);
+    out.zmask = 0;
+    std::vector<int> gidx(n, -1), grp(n, -1);
+    for (int G = 0; G < 2; G++)
+        for (size_t i = 0; i < P.pq[G].size(); i++) {
+            gidx[P.pq[G][i]] = (int)i;
+            grp[P.pq[G][i]] = G;
+        }
+    for (int p = 0; p < n; p++) {
+        const int q = occ[p];
+        if (grp[q] < 0) {
+            out.zmask |= 1ull << p;
+            continue;
+        }
+        const int c = p >> 3, b = p & 7;
+        for (int v = 0; v < 256; v++)
+            if ((v >> b) & 1) out.byt[((size_t)grp[q] * out.nbytes + c) * 256 + v] |= 1u << gidx[q];
+    }
+    for (int G = 0; G < 2; G++) {
+        out.tab[G].resize(2 * P.tab[G].size());
+        for (size_t i = 0; i < P.tab[G].size(); i++) {
+            out.tab[G][2 * i] = P.tab[G][i].re;
+            out.tab[G][2 * i + 1] = P.tab[G][i].im;
+        }
     }
 }
 
@@ -895,6 +934,12 @@ rcs_status rcs_plan_layout(const rcs_plan* p, int* restore_begin, int* final_pos
     return RCS_OK;
 }
 
+rcs_status rcs_plan_prefix(const rcs_plan* p, int* n_prefix) {
+    if (!p || !n_prefix) return RCS_ERR_ARG;
+    *n_prefix = p->p.prefix;
+    return RCS_OK;
+}
+
 rcs_status rcs_plan_summary(const rcs_plan* p, int* n_items, int* n_passes, int* n_remaps, int* n_swaps) {
     if (!p) return RCS_ERR_ARG;
     if (n_items) *n_items = (int)p->p.items.size();
@@ -985,6 +1030,7 @@ void rcs_context_free(rcs_context* c) {
     if (c->bad) cudaFree(c->bad);
     if (c->d_tc) cudaFree(c->d_tc);
     if (c->d_tiles) cudaFree(c->d_tiles);
+    if (c->d_pf) cudaFree(c->d_pf);
     for (int i = 0; i < 16; i++)
         for (cudaEvent_t e : {c->ev_a[i], c->ev_s[i]})
             if (e) cudaEventDestroy(e);
@@ -1021,6 +1067,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         (o.remap_mode == RCS_REMAP_LOOPBACK && (ctx->world != 1 || o.virtual_global < 1 || o.virtual_global > 3)) ||
         o.overlap_chunks < 0 || o.overlap_chunks > 4 || o.overlap_sms < 0 || o.tc_kernel < 0 || o.tc_kernel > 1 ||
         o.overlap_passes < 0 || o.overlap_passes > 8 || o.tc_schedule < 0 || o.tc_schedule > 1 ||
+        o.product_prefix < -1 || o.product_prefix > 0 ||
         o.virtual_global < 0) {
         set_error(err, RCS_ERR_ARG, "invalid build options (remap_mode %d, virtual_global %d, overlap_chunks %d)",
                   o.remap_mode, o.virtual_global, o.overlap_chunks);
@@ -1167,6 +1214,37 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         BUILD_TRY(cudaMalloc(&ctx->d_tc, tc_words * sizeof(uint32_t)));
         ctx->tc_cap = tc_words;
     }
+    // product-state prefix: cached per (circuit, plan), device copy per context
+    const int n_prefix = o.product_prefix >= 0 ? P.prefix : 0;
+    std::shared_ptr<const PrefixPack> pfp;
+    size_t pf_bytes[3] = {0, 0, 0};
+    bool pf_upload = false;
+    if (n_prefix > 0) {
+        rcs_circuit* cc = const_cast<rcs_circuit*>(circ);
+        std::lock_guard<std::mutex> lk(cc->mu);
+        auto key = std::make_pair(o.fuse_k, plan_g);
+        auto f = cc->prefix_packs.find(key);
+        if (f != cc->prefix_packs.end()) {
+            pfp = f->second;
+        } else {
+            auto np = std::make_shared<PrefixPack>();
+            make_prefix_pack(P, *np);
+            pfp = np;
+            cc->prefix_packs[key] = pfp;
+        }
+        pf_bytes[0] = pfp->tab[0].size() * sizeof(double);
+        pf_bytes[1] = pfp->tab[1].size() * sizeof(double);
+        pf_bytes[2] = pfp->byt.size() * sizeof(uint32_t);
+        const size_t need = pf_bytes[0] + pf_bytes[1] + pf_bytes[2];
+        pf_upload = !(ctx->pf_pack == pfp.get());
+        if (pf_upload && ctx->pf_cap < need) {
+            if (ctx->d_pf) cudaFree(ctx->d_pf);
+            ctx->d_pf = nullptr;
+            ctx->pf_cap = 0;
+            BUILD_TRY(cudaMalloc(&ctx->d_pf, need));
+            ctx->pf_cap = need;
+        }
+    }
     if (ctx->world > 1 && P.n_remaps > 0) {
         rcs_status r = setup_peers(ctx, s->amps, o.remap_mode, err);
         if (r) return fail(r);
@@ -1174,6 +1252,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     if (n_tc > 0 && !ctx->d_tiles && o.tc_schedule == 1) BUILD_TRY(cudaMalloc(&ctx->d_tiles, 64));
     s->tiles = o.tc_schedule == 1 ? ctx->d_tiles : nullptr;
     BUILD_TRY(cudaEventRecord(eb0, stream));
+    cudaEvent_t epf0 = nullptr;
     if (tc_upload) {
         BUILD_TRY(cudaMemcpyAsync(ctx->d_tc, tcp->words.data(), tc_words * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                   stream));
@@ -1181,7 +1260,34 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         ctx->tc_pack = tcp.get();
         ctx->tc_hold = tcp;
     }
-    BUILD_TRY(dev::init_basis(s->amps, n_amps, ctx->rank == 0, stream));
+    if (n_prefix > 0) {
+        if (pf_upload) {
+            BUILD_TRY(cudaMemcpyAsync(ctx->d_pf, pfp->tab[0].data(), pf_bytes[0], cudaMemcpyHostToDevice, stream));
+            BUILD_TRY(cudaMemcpyAsync(ctx->d_pf + pf_bytes[0], pfp->tab[1].data(), pf_bytes[1], cudaMemcpyHostToDevice,
+                                      stream));
+            BUILD_TRY(cudaMemcpyAsync(ctx->d_pf + pf_bytes[0] + pf_bytes[1], pfp->byt.data(), pf_bytes[2],
+                                      cudaMemcpyHostToDevice, stream));
+            ctx->pf_pack = pfp.get();
+            ctx->pf_hold = pfp;
+        }
+        if (o.timing) {
+            BUILD_TRY(cudaEventCreate(&epf0));
+            owned.push_back(epf0);
+            BUILD_TRY(cudaEventRecord(epf0, stream));
+        }
+        dev::PrefixArgs pa{};
+        pa.amps = s->amps;
+        pa.n_amps = n_amps;
+        pa.base = (uint64_t)ctx->rank << nl;
+        pa.tab[0] = reinterpret_cast<const double2*>(ctx->d_pf);
+        pa.tab[1] = reinterpret_cast<const double2*>(ctx->d_pf + pf_bytes[0]);
+        pa.byt = reinterpret_cast<const uint32_t*>(ctx->d_pf + pf_bytes[0] + pf_bytes[1]);
+        pa.nbytes = pfp->nbytes;
+        pa.zmask = pfp->zmask;
+        BUILD_TRY(dev::product_init(pa, stream));
+    } else {
+        BUILD_TRY(dev::init_basis(s->amps, n_amps, ctx->rank == 0, stream));
+    }
     if (keep)
         BUILD_TRY(cudaMemcpyAsync(s->ptab, ptab_host.data(), ptab_host.size() * 8, cudaMemcpyHostToDevice, stream));
     uint64_t pass_bytes = 0, remap_bytes = 0;
@@ -1200,7 +1306,14 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     auto tc_ref = [&](size_t i) {
         return PassRef{tcp->pos[i].data(), ctx->d_tc + (size_t)tc_slot[i] * tc_words_each};
     };
-    for (size_t ii = 0; ii < n_exec; ii++) {
+    if (n_prefix > 0) pass_bytes += 8ull * n_amps;   // the prefix kernel only writes the state
+    cudaEvent_t epf = nullptr;
+    if (o.timing) {
+        BUILD_TRY(cudaEventCreate(&epf));
+        owned.push_back(epf);
+        BUILD_TRY(cudaEventRecord(epf, stream));
+    }
+    for (size_t ii = (size_t)n_prefix; ii < n_exec; ii++) {
         const Item& it = P.items[ii];
         // [TC pass] -> REMAP -> [TC pass] pipelined over NVLink (or loopback)
         if (ov_on) {
@@ -1287,7 +1400,10 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     BUILD_TRY(cudaStreamSynchronize(stream));
 
     rcs_build_report R{};
-    R.n_passes = P.n_passes;
+    R.n_passes = P.n_passes - n_prefix;
+    R.n_prefix = n_prefix;
+    R.upload_bytes = (tc_upload ? tc_words * sizeof(uint32_t) : 0) +
+                     (pf_upload ? pf_bytes[0] + pf_bytes[1] + pf_bytes[2] : 0) + (keep ? ptab_host.size() * 8 : 0);
     R.n_remaps = 0;
     R.n_swaps = 0;
     for (size_t ii = 0; ii < n_exec; ii++) {   // executed items (a kept layout skips the restore)
@@ -1314,7 +1430,12 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             if (sp.item == kRemapKernelSpan) R.remap_kernel_ms += (double)t;
             else item_ms[sp.item] += sp.sign * (double)t;
         }
-        for (size_t ii = 0; ii < n_exec; ii++) {
+        if (epf0 && epf) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, epf0, epf);
+            R.prefix_ms = t;
+        }
+        for (size_t ii = (size_t)n_prefix; ii < n_exec; ii++) {
             const double t = item_ms[ii];
             if (P.items[ii].type == RCS_ITEM_PASS) {
                 R.pass_ms += t;
@@ -1334,7 +1455,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     R.pass_bytes = pass_bytes;
     R.remap_bytes = remap_bytes;
     R.norm = s->T_total;
-    R.n_tc_passes = n_tc;
+    R.n_tc_passes = 0;
+    for (size_t ii = (size_t)n_prefix; ii < n_exec; ii++) R.n_tc_passes += tc_slot[ii] >= 0;
     R.n_pipelined = n_pipelined;
     R.n_peer_remaps = n_peer;
     if (rep) *rep = R;

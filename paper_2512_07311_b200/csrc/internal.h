@@ -62,6 +62,16 @@ struct Plan {
     int restore_begin = 0;
     std::vector<int> final_pos;
     std::vector<int> initial_pos;   // empty: canonical start (qubit q at position q)
+    // Product-state prefix: items [0, prefix) are the leading fused blocks with pairwise disjoint
+    // qubit sets.  They act on |0...0>, so the state after them is the product of their first
+    // columns (and |0> on every other qubit): one write-only kernel replaces init + these passes.
+    // The set is chosen on the fusion result alone (P-independent), split into two groups of
+    // consecutive blocks (A, B); tab[G][v] = product over the group's blocks (fusion order, fp64)
+    // of their first-column entries, v's bit i <-> pq[G][i] (ascending qubits); an amplitude is
+    // tab[A][vA] * tab[B][vB] in fp64, rounded once -- the same arithmetic for every sharding.
+    int prefix = 0;
+    std::vector<int> pq[2];
+    std::vector<cplx> tab[2];
 };
 
 // low physical positions never moved by remaps: keeps qubit 0 at bit 0 (the CUDA-core pass
@@ -81,6 +91,7 @@ constexpr bool kFuseLookahead = true;
 constexpr int kFuseDeepDepth = 3;        // strategy 2: extension search depth
 constexpr bool kRemapPrefetch = true;   // remaps also bring in soon-needed global qubits
 constexpr bool kInitialPlacement = true;   // start with the latest-used qubits global (free: |0> state)
+constexpr int kPrefixGroupBits = 18;      // product-state prefix: qubits per table (2^18 x 16 B = 4 MiB)
 
 // given: the fused blocks (qubits + gate ids) to use instead of running the fuser
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err,
@@ -121,6 +132,14 @@ uint64_t job_seed(uint64_t base_seed, uint64_t job_id);
 
 // tensor-core pass operands of a plan: which items run on K9, their 6 positions (5-qubit blocks
 // padded with one more local qubit) and the packed fp16 hi/lo matrices (host copy)
+// product-state prefix operands for one (plan, n_local): fp64 group tables + byte gather tables
+struct PrefixPack {
+    std::vector<double> tab[2];            // interleaved complex, 2^|group| entries each
+    std::vector<uint32_t> byt;             // [2][nbytes][256]
+    int nbytes = 0;
+    uint64_t zmask = 0;                    // physical positions of the qubits outside the prefix
+};
+
 struct TcPack {
     std::vector<int> slot;                 // per item, -1 if not a tensor-core pass
     std::vector<std::array<int, 6>> pos;
@@ -136,6 +155,7 @@ struct rcs_circuit {
     std::mutex mu;
     std::map<std::pair<int, int>, std::shared_ptr<const rcs::Plan>> plans;
     std::map<std::tuple<int, int, int>, std::shared_ptr<const rcs::TcPack>> packs;
+    std::map<std::pair<int, int>, std::shared_ptr<const rcs::PrefixPack>> prefix_packs;
 };
 
 struct rcs_plan {

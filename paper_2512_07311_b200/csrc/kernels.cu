@@ -736,6 +736,45 @@ cudaError_t last_nonzero(const double* inc, uint64_t n, unsigned long long* out,
     return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(kThreads) k_product_init(const __grid_constant__ PrefixArgs a) {
+    __shared__ uint32_t bt[2][kPrefixBytes][256];
+    for (int e = threadIdx.x; e < 2 * a.nbytes * 256; e += blockDim.x) {
+        const int G = e / (a.nbytes * 256), r = e % (a.nbytes * 256);
+        bt[G][r >> 8][r & 255] = a.byt[e];
+    }
+    __syncthreads();
+    const uint64_t npair = a.n_amps >> 1;
+    float4* out = reinterpret_cast<float4*>(a.amps);
+    for (uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x; v < npair; v += (uint64_t)gridDim.x * kThreads) {
+        const uint64_t X = a.base + 2 * v;   // even: the pair differs in bit 0 only
+        uint32_t ia = 0, ib = 0;
+        for (int c = 1; c < a.nbytes; c++) {
+            const int by = (int)((X >> (8 * c)) & 255);
+            ia |= bt[0][c][by];
+            ib |= bt[1][c][by];
+        }
+        float r[4];
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const int by = (int)((X & 254) | e);
+            const double2 A = a.tab[0][ia | bt[0][0][by]], B = a.tab[1][ib | bt[1][0][by]];
+            const bool zero = ((X | (uint64_t)e) & a.zmask) != 0;
+            const double re = __dsub_rn(__dmul_rn(A.x, B.x), __dmul_rn(A.y, B.y));
+            const double im = __dadd_rn(__dmul_rn(A.x, B.y), __dmul_rn(A.y, B.x));
+            r[2 * e] = zero ? 0.f : __double2float_rn(re);
+            r[2 * e + 1] = zero ? 0.f : __double2float_rn(im);
+        }
+        out[v] = make_float4(r[0], r[1], r[2], r[3]);
+    }
+}
+
+cudaError_t product_init(const PrefixArgs& a, cudaStream_t st) {
+    if (a.n_amps < 2 || (a.n_amps & 1) || a.nbytes < 1 || a.nbytes > kPrefixBytes) return cudaErrorInvalidValue;
+    note_launch();
+    k_product_init<<<grid_for(a.n_amps / 2), kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t init_basis(float2* amps, uint64_t n_amps, int set_one, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(amps, 0, n_amps * sizeof(float2), st);
     if (e != cudaSuccess) return e;

@@ -441,6 +441,61 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         P.blocks.push_back(std::move(B));
     }
 
+    // ---- 1b. product-state prefix (a function of the blocks only: P-independent).  A block none
+    // of whose qubits an earlier block touches acts on |0...0> and commutes with every earlier
+    // block (disjoint qubits), so it can move to the front; these blocks are pairwise disjoint.
+    {
+        uint64_t seen = 0;
+        std::vector<Block> front, rest;
+        for (Block& B : P.blocks) {
+            uint64_t mk = 0;
+            for (int q : B.qubits) mk |= 1ull << q;
+            if (!(mk & seen)) front.push_back(std::move(B));
+            else rest.push_back(std::move(B));
+            seen |= mk;
+        }
+        int m = (int)front.size();
+        P.blocks = std::move(front);
+        for (Block& B : rest) P.blocks.push_back(std::move(B));
+        // groups: A = the first blocks up to half of the prefix qubits, B = the rest; drop
+        // trailing blocks until each group fits kPrefixGroupBits
+        while (m > 0) {
+            int total = 0;
+            for (int b = 0; b < m; b++) total += (int)P.blocks[b].qubits.size();
+            int a = 0, na = 0;
+            while (a < m && na + (int)P.blocks[a].qubits.size() <= (total + 1) / 2) na += (int)P.blocks[a++].qubits.size();
+            if (a == 0) na += (int)P.blocks[a++].qubits.size();
+            if (na <= kPrefixGroupBits && total - na <= kPrefixGroupBits) {
+                P.prefix = m;
+                for (int G = 0; G < 2; G++) {
+                    const int b0 = G ? a : 0, b1 = G ? m : a;
+                    std::vector<int>& qs = P.pq[G];
+                    for (int b = b0; b < b1; b++) qs.insert(qs.end(), P.blocks[b].qubits.begin(), P.blocks[b].qubits.end());
+                    std::sort(qs.begin(), qs.end());
+                    const size_t N = (size_t)1 << qs.size();
+                    std::vector<cplx>& T = P.tab[G];
+                    T.assign(N, {1.0, 0.0});
+                    for (int b = b0; b < b1; b++) {   // fusion order
+                        const Block& B = P.blocks[b];
+                        const int kb = (int)B.qubits.size(), D = 1 << kb;
+                        int bit[8];
+                        for (int i = 0; i < kb; i++)
+                            bit[i] = (int)(std::find(qs.begin(), qs.end(), B.qubits[i]) - qs.begin());
+                        for (size_t v = 0; v < N; v++) {
+                            int r = 0;
+                            for (int i = 0; i < kb; i++) r |= (int)((v >> bit[i]) & 1) << i;
+                            const cplx f = B.matrix[(size_t)r * D];   // column 0: the block on |0...0>
+                            const cplx t = T[v];
+                            T[v] = {t.re * f.re - t.im * f.im, t.re * f.im + t.im * f.re};
+                        }
+                    }
+                }
+                break;
+            }
+            m--;
+        }
+    }
+
     // ---- 2. layout + remaps
     std::vector<int> pos(n), occ(n);
     for (int q = 0; q < n; q++) pos[q] = occ[q] = q;
@@ -494,8 +549,8 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
     for (int bi = 0; bi < (int)P.blocks.size(); bi++) {
         const Block& blk = P.blocks[bi];
         std::vector<int> need;
-        for (int q : blk.qubits)
-            if (pos[q] >= n_local) need.push_back(q);
+        for (int q : blk.qubits)   // prefix blocks are written by the product kernel: no remap
+            if (pos[q] >= n_local && bi >= P.prefix) need.push_back(q);
         if (!need.empty()) {
             std::vector<int> cand;
             for (int p = pinned; p < n_local; p++) {

@@ -66,10 +66,10 @@ constexpr uint32_t kSBO = (TK / 8) * 128;    // next 8-row group (16 chunks of 1
 constexpr int kPitchF = 128;                 // staging row t: 64 float2, column j at j ^ g(t) (swizzle)
 constexpr uint32_t kStagingBytes = 64 * kPitchF * 4;
 constexpr int kExpSlots = 4;                 // per-tile column exponents in flight (converter -> epilogue)
-constexpr uint32_t kCtlBytes = 2560;   // barriers + offset tables; total <= 227 KB
+constexpr uint32_t kCtlBytes = 3072;   // barriers + offset tables; total <= 227 KB
 // control block: (12 + kExpSlots) mbarriers + 64 run offsets (8 B) + 3 x 64 column maxima (4 B)
 // + 2 x 64 uint16 + kExpSlots x 64 exponents (1 B) + the TMEM slot
-static_assert((12 + kExpSlots) * 8 + 64 * 8 + 3 * 64 * 4 + 2 * 64 * 2 + kExpSlots * 64 + 4 <= kCtlBytes,
+static_assert((12 + kExpSlots) * 8 + 64 * 8 + 3 * 64 * 4 + 2 * 64 * 2 + kExpSlots * 64 * 4 + 4 <= kCtlBytes,
               "control block overflow");
 constexpr uint32_t kSmemBytes = kRaw * kRawBytes + kStages * kStageBytes + kStagingBytes + kCtlBytes;
 constexpr int kAccCols = 2 * TN;             // one D buffer: acc 0 cross terms, acc 1 main term
@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
     int* cmax = reinterpret_cast<int*>(offr + 64);        // [3][64] column max |x| (float bits, atomicMax)
     uint16_t* soft = reinterpret_cast<uint16_t*>(cmax + 3 * 64);   // [64] sub-cube index of target combo t
     uint16_t* sofj = soft + 64;                                    // [64] sub-cube index of column j
-    int8_t* colexp = reinterpret_cast<int8_t*>(sofj + 64);         // [kExpSlots][64] E_j per tile
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colexp + kExpSlots * 64);
+    float* colfac = reinterpret_cast<float*>(sofj + 64);           // [kExpSlots][64] 2^-E_j per tile
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colfac + kExpSlots * 64);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) {
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             // write (and the slot mbarrier's next phase) must come after that wait.
             const int es = (int)(it % kExpSlots);
             if (to == 0) {
-                colexp[es * 64 + j] = (int8_t)E;
+                colfac[es * 64 + j] = pow2f(-E);
                 mbar_arrive(&cready[es]);             // release: the epilogue reads E_j after acquiring
             }
             uint8_t* bhi = stages + s * kStageBytes;
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
             mbar_wait(&tfull[d], (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + 128 + d * kAccCols;
-            const int8_t* ce = colexp + es * 64;
+            const float* ce = colfac + es * 64;
             // per-tile copies of the swizzle terms: hoisting the 64 + 32 swizzled offsets out of
             // the tile loop would hold them in registers (spills)
             int gwt = gw, jbt = jbs;
@@ -535,21 +535,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                 uint32_t a0[32], a1[32];
                 TMEM_LD32(ta + 32 * h, a0);
                 TMEM_LD32(ta + TN + 32 * h, a1);
-                // 2^-E_j of this half's 32 columns (read before the D buffer is released: the
-                // converters rewrite this slot only kExpSlots tiles later)
-                int ev[8];
-#pragma unroll
-                for (int w = 0; w < 8; w++) ev[w] = reinterpret_cast<const int*>(ce + 32 * h)[w];
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
-                if (h == 1) {
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    mbar_arrive(&tempty[d]);
-                }
 #pragma unroll
                 for (int c = 0; c < 32; c += 2) {
-                    const int e0 = (int)(int8_t)(ev[c >> 2] >> (8 * (c & 3)));
-                    const int e1 = (int)(int8_t)(ev[c >> 2] >> (8 * ((c & 3) + 1)));
-                    const float f0 = pow2f(-e0), f1 = pow2f(-e1);
+                    // 2^-E_j of the column pair (written once per column by the converters; this
+                    // slot is rewritten only after this tile's D buffer is released, below)
+                    const float2 f = *reinterpret_cast<const float2*>(ce + 32 * h + c);
+                    const float f0 = f.x, f1 = f.y;
                     float o0, o1;   // ((cross + main) (2^-E_c, 2^-E_c+1)) 2^-F_t
                     asm("{\n.reg .b64 x, y, u, v;\n"
                         "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %7};\nmov.b64 v, {%8, %8};\n"
@@ -559,6 +551,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tc(const __grid_constant
                         : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(f0), "f"(f1), "f"(rowfac));
                     st[2 * ((32 * h + c) ^ gwt)] = o0;
                     st[2 * ((32 * h + c + 1) ^ gwt)] = o1;
+                }
+                if (h == 1) {   // D buffer (and with it this tile's colfac slot) released
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(&tempty[d]);
                 }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");

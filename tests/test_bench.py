@@ -15,7 +15,11 @@ def test_plan_pass_table_matches_planner():
     for cfg in CONFIGS:
         c = Circuit.from_qasm(config_qasm(cfg))
         for k in (3, 4, 5, 6):
-            assert bench.PLAN_PASSES[cfg][k] == Plan(c, k, 0).n_passes, (cfg, k)
+            p = Plan(c, k, 0)
+            assert bench.PLAN_PASSES[cfg][k] == p.n_passes, (cfg, k)
+            assert bench.PLAN_PREFIX[cfg][k] == p.prefix, (cfg, k)
+            if c.n_qubits >= 24:   # a function of the fused blocks, not of the sharding
+                assert p.prefix == Plan(c, k, 2).prefix, (cfg, k)
 
 
 def test_reference_arm_prints_one_json_line(tmp_path):

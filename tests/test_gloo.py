@@ -39,10 +39,17 @@ def run_rank(rank, world, port, text, g, q):
         n = c.n_qubits
         nl = n - g
         plan = Plan(c, 4, g)
-        shard = np.zeros(1 << nl, np.complex128)
-        if rank == 0:
-            shard[0] = 1
-        for it in plan.items():
+        items = plan.items()
+        # product-state prefix (items [0, prefix): disjoint blocks on |0...0>, written by one
+        # kernel on the GPU, possibly on global positions): every rank takes its slice of the
+        # product state, built here on the full vector
+        full0 = np.zeros(1 << n, np.complex128)
+        full0[0] = 1
+        for it in items[:plan.prefix]:
+            assert it["type"] == "pass"
+            apply_block(full0, it["matrix"], it["pos"])
+        shard = full0[rank << nl:(rank + 1) << nl].copy()
+        for it in items[plan.prefix:]:
             if it["type"] == "pass":
                 assert max(it["pos"]) < nl
                 apply_block(shard, it["matrix"], it["pos"])

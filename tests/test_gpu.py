@@ -109,6 +109,28 @@ def test_transposed_pass_matches_k9(rcs, ctx, n):
         check_amps(pa, oracle.build_state(text))
 
 
+@pytest.mark.parametrize("case", ["c1", "c3_24", "w33_24", "grid20_k4"])
+def test_product_prefix_matches_passes(rcs, ctx, case):
+    """The leading fused blocks on disjoint qubits act on |0...0>: the product-state kernel writes
+    their state in one write-only sweep (fp64 products rounded once) instead of init + passes;
+    both agree with the oracle and with each other within the pass rounding."""
+    text, k = {"c1": (config_qasm("c1"), 6), "c3_24": (config_qasm("c3", n_qubits=24, rows=4, cols=6), 6),
+               "w33_24": (config_qasm("w33", n_qubits=24), 6),
+               "grid20_k4": (emit_qasm(generate(4, 5, 12, "ABCDCDAB", seed=2)), 4)}[case]
+    c = rcs.Circuit.from_qasm(text)
+    a = rcs.State.build(ctx, c, fuse_k=k, timing=True)
+    pa = a.copy_out().astype(np.complex128)
+    b = rcs.State.build(ctx, c, fuse_k=k, product_prefix=False)
+    pb = b.copy_out().astype(np.complex128)
+    assert a.report["n_prefix"] > 0 and b.report["n_prefix"] == 0
+    assert a.report["n_passes"] + a.report["n_prefix"] == b.report["n_passes"]
+    assert a.report["n_passes"] == len(a.pass_times()) and a.report["prefix_ms"] > 0
+    ref = oracle.build_state(text)
+    check_amps(pa, ref)
+    check_amps(pb, ref)
+    assert np.abs(pa - pb).max() <= 1e-6
+
+
 @pytest.mark.parametrize("case", ["c2", "c3"])
 def test_dynamic_tile_schedule_bitwise(rcs, ctx, case):
     """K12's optional dynamic scheduler hands tiles to the SMs through a device counter; the
