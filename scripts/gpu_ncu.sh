@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-2 ncu evidence (1 GPU): C4 launch list (serialized per-launch times), one --set full
+# ncu evidence (1 GPU): C4 launch list (serialized per-launch times), one --set full
 # capture per tensor-core kernel variant on C3 (K9 with 2 low targets, K12 without and with a
 # permuted t bit), DRAM bytes of the K12 pass at C4.  Each command first runs without ncu.
 cd "$(dirname "$0")/.."

@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-2 sweep (gpurun --gpus 4): SMs left to the swaps x passes chained behind a remap, C4 at
+# sweep (gpurun --gpus 4): SMs left to the swaps x passes chained behind a remap, C4 at
 # N = 2 and 4, one box
 cd "$(dirname "$0")/.."
 OUT=gpurun_out/sweep4; mkdir -p $OUT
