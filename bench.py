@@ -322,10 +322,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     up_bytes = 0
+    e2e_plan_ms = []
     for _ in range(e2e_steps):
         c2 = rcs.Circuit.from_qasm(text)                       # host QASM in
         st = rcs.State.build(ctx, c2, fuse_k=args.fuse_k, amps=amps, scratch=scratch, keep_layout=keep, **bopts)
         up_bytes = st.report["upload_bytes"]                   # plan operands copied by this build
+        e2e_plan_ms.append(st.report["plan_ms"])
         xh = st.sample(shots, seed=SHOT_SEED)                  # bitstrings to host
         xr_h = st.xeb(xh)                                      # XEB from the host array
         st.free()
@@ -405,7 +407,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "steps": e2e_steps, "ms_per_step": e2e_ms / max(1, e2e_steps),
                     "h2d_bytes_per_step": up_bytes + 8 * shots, "d2h_bytes_per_step": 8 * shots + 8,
-                    "xeb": xr_h["F"] if e2e_steps else None},
+                    "xeb": xr_h["F"] if e2e_steps else None,
+                    "plan_ms": statistics.median(e2e_plan_ms) if e2e_steps else None},
             "gpu_launches": launches,
             "clocks": clk,
         }

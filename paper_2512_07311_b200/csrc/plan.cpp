@@ -24,6 +24,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <thread>
 #include <unordered_map>
@@ -42,6 +43,22 @@ struct FuseTables {
     std::vector<int> gw;                   // 1 or 2: 2q gates count double
 };
 
+// Blocks the plain greedy needs from a fuser state (the per-qubit heads determine it), shared by
+// every rollout of every strategy: rollouts from neighbouring states walk into the same greedy
+// chain, so most stop at a memoized state.  Exact values of a deterministic function: the plan
+// does not depend on which thread filled an entry.
+struct RolloutMemo {
+    struct H {
+        size_t operator()(const std::vector<int>& v) const {
+            uint64_t h = 1469598103934665603ull;
+            for (int x : v) h = (h ^ (uint64_t)(uint32_t)x) * 1099511628211ull;
+            return (size_t)h;
+        }
+    };
+    std::mutex mu;
+    std::unordered_map<std::vector<int>, int, H> left;
+};
+
 struct Fuser {
     const Circuit& C;
     int k, n;
@@ -55,6 +72,7 @@ struct Fuser {
     bool grow_lookahead = false;
     int grow_depth = 1;
     int grow_beam = 0;   // 0: every extension
+    std::shared_ptr<RolloutMemo> memo;
 
     Fuser(const Circuit& c, int k_) : C(c), k(k_), n(c.n) {
         auto t = std::make_shared<FuseTables>();
@@ -111,6 +129,17 @@ struct Fuser {
         return w;
     }
 
+    // closure weights of the sets one grow() visits (the heads do not move during a grow)
+    using WCache = std::unordered_map<uint64_t, int>;
+    int cw(uint64_t S, WCache* c) const {
+        if (!c) return closure(S);
+        auto it = c->find(S);
+        if (it != c->end()) return it->second;
+        const int w = closure(S);
+        c->emplace(S, w);
+        return w;
+    }
+
     // candidate extensions of S: the other qubits of the next gate on a qubit of S (after the
     // closure), or the qubits of a gate that is ready elsewhere, within k qubits
     void extensions(uint64_t S, std::vector<uint64_t>& out) const {
@@ -143,7 +172,7 @@ struct Fuser {
     }
 
     // greedy continuation: the extension with the largest gain per added qubit, until k
-    void grow_from(uint64_t& S, int& w) const {
+    void grow_from(uint64_t& S, int& w, WCache* wc = nullptr) const {
         std::vector<uint64_t> ex;
         while (__builtin_popcountll(S) < k) {
             extensions(S, ex);
@@ -151,7 +180,7 @@ struct Fuser {
             uint64_t best = 0;
             int bw = w;
             for (uint64_t e : ex) {
-                const int w1 = closure(S | e);
+                const int w1 = cw(S | e, wc);
                 const int gain = w1 - w, sz = __builtin_popcountll(e);
                 if (gain <= 0) continue;
                 if (!best || gain * bsize > bgain * sz) {
@@ -170,7 +199,7 @@ struct Fuser {
     // `depth` levels of exhaustive extension choice, then greedy; keeps the heaviest block.
     // Different extension orders reach the same sets: results are memoized per (set, depth).
     using Memo = std::unordered_map<uint64_t, std::pair<uint64_t, int>>;
-    void grow_deep(uint64_t& S, int& w, int depth, Memo& memo) const {
+    void grow_deep(uint64_t& S, int& w, int depth, Memo& memo, WCache* wc) const {
         const uint64_t key = S * 8 + (uint64_t)depth;   // S < 2^61 (n <= 61 here)
         auto f = memo.find(key);
         if (f != memo.end()) {
@@ -180,7 +209,7 @@ struct Fuser {
         }
         const uint64_t S0 = S;
         if (depth == 0 || __builtin_popcountll(S) >= k) {
-            grow_from(S, w);
+            grow_from(S, w, wc);
             memo[key] = {S, w};
             return;
         }
@@ -189,7 +218,7 @@ struct Fuser {
         // keep the `grow_beam` extensions with the best gain per added qubit (0: all)
         std::vector<std::pair<double, uint64_t>> ranked;
         for (uint64_t e : ex) {
-            const int w1 = closure(S | e);
+            const int w1 = cw(S | e, wc);
             if (w1 > w) ranked.push_back({-(double)(w1 - w) / __builtin_popcountll(e), e});
         }
         std::stable_sort(ranked.begin(), ranked.end(),
@@ -201,15 +230,15 @@ struct Fuser {
         uint64_t bS = S;
         for (const auto& re : ranked) {
             uint64_t S1 = S | re.second;
-            int w1 = closure(S1);
-            grow_deep(S1, w1, depth - 1, memo);
+            int w1 = cw(S1, wc);
+            grow_deep(S1, w1, depth - 1, memo, wc);
             if (w1 > best) {
                 best = w1;
                 bS = S1;
             }
         }
         if (best < 0) {
-            grow_from(S, w);
+            grow_from(S, w, wc);
         } else {
             S = bS;
             w = best;
@@ -222,7 +251,8 @@ struct Fuser {
         w = closure(S);
         if (grow_lookahead) {
             Memo memo;
-            grow_deep(S, w, grow_depth, memo);
+            WCache wc;
+            grow_deep(S, w, grow_depth, memo, &wc);
         } else {
             grow_from(S, w);
         }
@@ -254,8 +284,28 @@ struct Fuser {
         f.grow_lookahead = false;
         int cnt = 0;
         uint64_t S;
-        while (f.next_set(S)) cnt++;
-        return cnt;
+        if (!memo) {
+            while (f.next_set(S)) cnt++;
+            return cnt;
+        }
+        std::vector<std::vector<int>> path;
+        int tail = 0;
+        while (f.first_unassigned < f.assigned.size()) {
+            {
+                std::lock_guard<std::mutex> lk(memo->mu);
+                auto it = memo->left.find(f.head);
+                if (it != memo->left.end()) {
+                    tail = it->second;
+                    break;
+                }
+            }
+            path.push_back(f.head);
+            f.next_set(S);
+            cnt++;
+        }
+        std::lock_guard<std::mutex> lk(memo->mu);
+        for (size_t i = 0; i < path.size(); i++) memo->left.emplace(std::move(path[i]), cnt - (int)i + tail);
+        return cnt + tail;
     }
 
     // next block's qubit set (committed): grow from the earliest unassigned gate and from up to
@@ -357,9 +407,11 @@ void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb
 // candidate extension scored by the block it finishes as, 2 exhaustive 3-level extension search
 // (memoized); all with the rollout lookahead over seed gates.  The plan with the fewest blocks
 // wins, ties to the lower index.
-void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) {
+static void fuse_strategy_memo(const Circuit& c, int k, int which, std::vector<Block>& out,
+                               std::shared_ptr<RolloutMemo> memo) {
     const int depth_of[kFuseStrategies] = {0, 1, kFuseDeepDepth};
     Fuser F(c, k);
+    F.memo = std::move(memo);
     F.seeds = kFuseSeeds;
     F.lookahead = kFuseLookahead;
     F.grow_lookahead = depth_of[which] > 0;
@@ -372,10 +424,15 @@ void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) 
     }
 }
 
+void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) {
+    fuse_strategy_memo(c, k, which, out, std::make_shared<RolloutMemo>());
+}
+
 int fuse_best(const Circuit& c, int k, std::vector<Block>* cand) {
     std::vector<std::thread> th;
-    for (int w = 1; w < kFuseStrategies; w++) th.emplace_back([&, w] { fuse_strategy(c, k, w, cand[w]); });
-    fuse_strategy(c, k, 0, cand[0]);
+    auto memo = std::make_shared<RolloutMemo>();
+    for (int w = 1; w < kFuseStrategies; w++) th.emplace_back([&, w] { fuse_strategy_memo(c, k, w, cand[w], memo); });
+    fuse_strategy_memo(c, k, 0, cand[0], memo);
     for (auto& t : th) t.join();
     int win = 0;
     for (int w = 1; w < kFuseStrategies; w++)

@@ -178,3 +178,14 @@ def test_pass_counts_reported(rcs):
     for cfg, cap in want.items():
         p = rcs.Plan(rcs.Circuit.from_qasm(config_qasm(cfg)), 4, 0)
         assert p.n_passes <= cap, (cfg, p.n_passes)
+
+
+def test_plan_deterministic_across_runs(rcs):
+    """The fusion strategies run in threads and share a memo of greedy rollouts:
+    the plan must not depend on thread timing -- the same items, run after run."""
+    c = rcs.Circuit.from_qasm(config_qasm("c2"))
+    def key(p):
+        return [tuple((f, np.asarray(v).tobytes()) for f, v in sorted(it.items())) for it in p.items()]
+    runs = [key(rcs.Plan(c, 6, g)) for g in (0, 0, 0, 2, 2)]
+    assert runs[0] == runs[1] == runs[2]
+    assert runs[3] == runs[4]
