@@ -395,7 +395,7 @@ rcs_status setup_peers(rcs_context* c, void* amps, int remap_mode, rcs_error* er
 }
 
 // Fusion shared by the ranks of a context (world > 1): the strategies are split round-robin
-// over the ranks, the block counts all-gathered, and the winning rank (fewest blocks, ties to
+// over the ranks, their costs (fuse_cost) all-gathered, and the winning rank (lowest cost, ties to
 // the lower strategy -- the single-process rule, so the plan equals the 1-GPU plan) broadcasts
 // its blocks; every rank then derives matrices and remaps itself.
 rcs_status plan_distributed(rcs_context* c, const Circuit& circ, int fuse_k, int plan_g, Plan& out, rcs_error* err) {
@@ -411,7 +411,7 @@ rcs_status plan_distributed(rcs_context* c, const Circuit& circ, int fuse_k, int
         }
         for (auto& t : th) t.join();
         for (int s = 0; s < kFuseStrategies; s++)
-            if (s % c->world == c->rank && k > 0) cnt[s] = (int64_t)mine[s].size();
+            if (s % c->world == c->rank && k > 0) cnt[s] = fuse_cost(mine[s]);
     }
     int64_t* d = nullptr;
     CUDA_TRY(cudaMalloc(&d, sizeof(int64_t) * kFuseStrategies * (c->world + 1)));

@@ -85,7 +85,7 @@ inline int pinned_low(int k) { return k >= 5 ? 7 : kPinnedLow; }
 // the tensor-core pass tiles 6 target + 6 column bits
 constexpr int kTcMinLocal = 12;
 // fuser: ready gates tried as block seeds besides the earliest unassigned one
-constexpr int kFuseSeeds = 4;
+constexpr int kFuseSeeds = 8;
 // fuser: pick among the seeds by the block count of a greedy completion (rollout)
 constexpr bool kFuseLookahead = true;
 constexpr int kFuseDeepDepth = 3;        // strategy 2: extension search depth
@@ -96,7 +96,10 @@ constexpr int kPrefixGroupBits = 18;      // product-state prefix: qubits per ta
 // given: the fused blocks (qubits + gate ids) to use instead of running the fuser
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err,
                       const std::vector<Block>* given = nullptr);
-constexpr int kFuseStrategies = 3;
+// strategies: plain greedy, 3-level extension search, prefix-first greedy, prefix-first 1-level,
+// prefix-first with a 1-level prefix phase and a 3-level rest (plan.cpp fuse_strategy_memo)
+constexpr int kFuseStrategies = 5;
+int64_t fuse_cost(const std::vector<Block>& blocks);   // passes << 20 | blocks (lower is better)
 void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out);
 int fuse_best(const Circuit& c, int k, std::vector<Block>* cand /* [kFuseStrategies] */);
 int plan_block_k(int n, int fuse_k, int n_global);   // the block width build_plan uses

@@ -747,6 +747,10 @@ __global__ void __launch_bounds__(kThreads) k_product_init(const __grid_constant
     float4* out = reinterpret_cast<float4*>(a.amps);
     for (uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x; v < npair; v += (uint64_t)gridDim.x * kThreads) {
         const uint64_t X = a.base + 2 * v;   // even: the pair differs in bit 0 only
+        if (X & a.zmask & ~1ull) {           // a qubit outside the prefix is |1>: both amplitudes 0
+            out[v] = make_float4(0.f, 0.f, 0.f, 0.f);   // (no table reads: most of the state)
+            continue;
+        }
         uint32_t ia = 0, ib = 0;
         for (int c = 1; c < a.nbytes; c++) {
             const int by = (int)((X >> (8 * c)) & 255);

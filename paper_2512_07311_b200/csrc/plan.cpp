@@ -72,6 +72,15 @@ struct Fuser {
     bool grow_lookahead = false;
     int grow_depth = 1;
     int grow_beam = 0;   // 0: every extension
+    // prefix-first: while a ready gate lies on qubits no block has touched yet, the next block
+    // is grown inside the untouched qubits only.  Such blocks act on |0...0> and become the
+    // product-state prefix (written by one kernel, not run as passes), so this maximises the
+    // gates absorbed there; afterwards the fuser continues as usual.
+    bool prefix_first = false;
+    uint64_t touched = 0;         // union of the committed blocks' qubits
+    uint64_t allowed = ~0ull;     // extensions stay inside this set (prefix phase: ~touched)
+    bool last_prefix = false;     // the last next_set() committed a prefix-phase block
+    int prefix_depth = -1;        // >= 0: extension search depth of the prefix phase (else grow_depth)
     std::shared_ptr<RolloutMemo> memo;
 
     Fuser(const Circuit& c, int k_) : C(c), k(k_), n(c.n) {
@@ -148,7 +157,7 @@ struct Fuser {
         closure(S, nullptr, h);
         const int size = __builtin_popcountll(S);
         auto add = [&](uint64_t ext) {
-            if (!ext || size + __builtin_popcountll(ext) > k) return;
+            if (!ext || size + __builtin_popcountll(ext) > k || (ext & ~allowed)) return;
             for (uint64_t e : out)
                 if (e == ext) return;
             out.push_back(ext);
@@ -273,38 +282,53 @@ struct Fuser {
             assigned[g] = 1;
             for (uint64_t m = T->gmask[g]; m; m &= m - 1) head[__builtin_ctzll(m)]++;
         }
+        touched |= S;
         while (first_unassigned < assigned.size() && assigned[first_unassigned]) first_unassigned++;
     }
 
     // number of blocks the plain greedy (earliest-gate seed) needs from the current state
+    // (prefix-first fusers: blocks that run as passes, i.e. not counting prefix-phase blocks; the
+    // state is then the heads plus the touched set)
     int rollout() const {
         Fuser f = *this;
         f.seeds = 0;
         f.lookahead = false;
         f.grow_lookahead = false;
+        f.prefix_depth = -1;   // one rollout function per memo (every prefix-first strategy shares it)
         int cnt = 0;
         uint64_t S;
         if (!memo) {
-            while (f.next_set(S)) cnt++;
+            while (f.next_set(S)) cnt += !f.last_prefix;
             return cnt;
         }
+        auto key = [&]() {
+            std::vector<int> kv = f.head;
+            if (f.prefix_first) {
+                kv.push_back((int)(uint32_t)f.touched);
+                kv.push_back((int)(uint32_t)(f.touched >> 32));
+            }
+            return kv;
+        };
         std::vector<std::vector<int>> path;
+        std::vector<int> pcnt;
         int tail = 0;
         while (f.first_unassigned < f.assigned.size()) {
+            std::vector<int> kv = key();
             {
                 std::lock_guard<std::mutex> lk(memo->mu);
-                auto it = memo->left.find(f.head);
+                auto it = memo->left.find(kv);
                 if (it != memo->left.end()) {
                     tail = it->second;
                     break;
                 }
             }
-            path.push_back(f.head);
+            path.push_back(std::move(kv));
+            pcnt.push_back(cnt);
             f.next_set(S);
-            cnt++;
+            cnt += !f.last_prefix;
         }
         std::lock_guard<std::mutex> lk(memo->mu);
-        for (size_t i = 0; i < path.size(); i++) memo->left.emplace(std::move(path[i]), cnt - (int)i + tail);
+        for (size_t i = 0; i < path.size(); i++) memo->left.emplace(std::move(path[i]), cnt - pcnt[i] + tail);
         return cnt + tail;
     }
 
@@ -313,6 +337,8 @@ struct Fuser {
     // greedy completion needs the fewest blocks (candidates evaluated in parallel threads)
     bool next_set(uint64_t& out) {
         if (first_unassigned >= assigned.size()) return false;
+        last_prefix = prefix_first && next_prefix_set(out);
+        if (last_prefix) return true;
         const int g0 = (int)first_unassigned;
         std::vector<int> cand{g0};
         for (int i = g0 + 1; i < (int)assigned.size() && (int)cand.size() < 1 + seeds; i++)
@@ -343,6 +369,60 @@ struct Fuser {
         for (size_t i = 1; i < nc; i++)
             if (sc[i] > sc[bi]) bi = i;
         out = cS[bi];
+        commit(out);
+        return true;
+    }
+
+    // prefix phase: every ready gate on untouched qubits seeds a block grown inside the untouched
+    // qubits; the heaviest (most absorbed gate weight, ties: earliest seed) is committed
+    bool next_prefix_set(uint64_t& out) {
+        std::vector<int> cand;
+        for (int q = 0; q < n; q++) {
+            if ((touched >> q) & 1) continue;
+            const int g = next_gate(q, head[q]);
+            if (g < 0 || (T->gmask[g] & touched) || !ready(g)) continue;
+            if (std::find(cand.begin(), cand.end(), g) == cand.end()) cand.push_back(g);
+        }
+        if (cand.empty()) return false;
+        std::sort(cand.begin(), cand.end());
+        const uint64_t saved = allowed;
+        const bool sgl = grow_lookahead;
+        const int sgd = grow_depth;
+        allowed = ~touched;
+        if (prefix_depth >= 0) {
+            grow_lookahead = prefix_depth > 0;
+            grow_depth = prefix_depth;
+        }
+        const size_t nc = cand.size();
+        std::vector<uint64_t> cS(nc);
+        std::vector<long> sc(nc);
+        for (size_t i = 0; i < nc; i++) {
+            int w;
+            grow(cand[i], cS[i], w);
+            sc[i] = w;
+        }
+        allowed = saved;
+        grow_lookahead = sgl;
+        grow_depth = sgd;
+        if (lookahead && nc > 1) {   // fewest passes after a greedy completion, then most gates now
+            auto work = [&](size_t i) {
+                Fuser f = *this;
+                f.commit(cS[i]);
+                sc[i] += -1000L * f.rollout();
+            };
+            std::vector<std::thread> th;
+            for (size_t i = 1; i < nc; i++) th.emplace_back(work, i);
+            work(0);
+            for (auto& t : th) t.join();
+        }
+        uint64_t bS = cS[0];
+        long bw = sc[0];
+        for (size_t i = 1; i < nc; i++)
+            if (sc[i] > bw) {
+                bw = sc[i];
+                bS = cS[i];
+            }
+        out = bS;
         commit(out);
         return true;
     }
@@ -409,13 +489,17 @@ void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb
 // wins, ties to the lower index.
 static void fuse_strategy_memo(const Circuit& c, int k, int which, std::vector<Block>& out,
                                std::shared_ptr<RolloutMemo> memo) {
-    const int depth_of[kFuseStrategies] = {0, 1, kFuseDeepDepth};
+    // {prefix-first, extension search depth, prefix-phase depth (-1: the same)}
+    static const int S[kFuseStrategies][3] = {{0, 0, -1}, {0, kFuseDeepDepth, -1}, {1, 0, -1}, {1, 1, -1},
+                                              {1, kFuseDeepDepth, 1}};
     Fuser F(c, k);
+    F.prefix_first = S[which][0] != 0;
+    F.prefix_depth = S[which][2];
     F.memo = std::move(memo);
     F.seeds = kFuseSeeds;
     F.lookahead = kFuseLookahead;
-    F.grow_lookahead = depth_of[which] > 0;
-    F.grow_depth = depth_of[which];
+    F.grow_lookahead = S[which][1] > 0;
+    F.grow_depth = S[which][1];
     out.clear();
     Block B;
     while (F.next_block(B)) {
@@ -430,14 +514,32 @@ void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) 
 
 int fuse_best(const Circuit& c, int k, std::vector<Block>* cand) {
     std::vector<std::thread> th;
-    auto memo = std::make_shared<RolloutMemo>();
-    for (int w = 1; w < kFuseStrategies; w++) th.emplace_back([&, w] { fuse_strategy_memo(c, k, w, cand[w], memo); });
+    auto memo = std::make_shared<RolloutMemo>(), pmemo = std::make_shared<RolloutMemo>();
+    for (int w = 1; w < kFuseStrategies; w++)
+        th.emplace_back([&, w] { fuse_strategy_memo(c, k, w, cand[w], w >= 2 ? pmemo : memo); });
     fuse_strategy_memo(c, k, 0, cand[0], memo);
     for (auto& t : th) t.join();
     int win = 0;
     for (int w = 1; w < kFuseStrategies; w++)
-        if (cand[w].size() < cand[win].size()) win = w;
+        if (fuse_cost(cand[w]) < fuse_cost(cand[win])) win = w;
     return win;
+}
+
+// blocks that run as passes (x 2^20) + all blocks: the product-state prefix (blocks disjoint from
+// every earlier block, up to the two tables' 2 x kPrefixGroupBits qubits) costs no pass
+int64_t fuse_cost(const std::vector<Block>& blocks) {
+    uint64_t seen = 0;
+    int pre = 0, preq = 0;
+    for (const Block& B : blocks) {
+        uint64_t m = 0;
+        for (int q : B.qubits) m |= 1ull << q;
+        if (!(m & seen) && preq + (int)B.qubits.size() <= 2 * kPrefixGroupBits) {
+            pre++;
+            preq += (int)B.qubits.size();
+        }
+        seen |= m;
+    }
+    return ((int64_t)(blocks.size() - pre) << 20) + (int64_t)blocks.size();
 }
 
 int plan_block_k(int n, int fuse_k, int n_global) {
@@ -519,9 +621,15 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         while (m > 0) {
             int total = 0;
             for (int b = 0; b < m; b++) total += (int)P.blocks[b].qubits.size();
-            int a = 0, na = 0;
-            while (a < m && na + (int)P.blocks[a].qubits.size() <= (total + 1) / 2) na += (int)P.blocks[a++].qubits.size();
-            if (a == 0) na += (int)P.blocks[a++].qubits.size();
+            // split point: the most balanced (A non-empty, ties to the earliest)
+            int a = 1, na = (int)P.blocks[0].qubits.size();
+            for (int a1 = 1, n1 = 0; a1 <= m; a1++) {
+                n1 += (int)P.blocks[a1 - 1].qubits.size();   // qubits of blocks [0, a1)
+                if (std::max(n1, total - n1) < std::max(na, total - na)) {
+                    a = a1;
+                    na = n1;
+                }
+            }
             if (na <= kPrefixGroupBits && total - na <= kPrefixGroupBits) {
                 P.prefix = m;
                 for (int G = 0; G < 2; G++) {

@@ -625,7 +625,7 @@ constexpr int kTRing = 8;                             // tile bases in flight (p
 constexpr uint64_t kTileEnd = ~0ull;                  // ring sentinel: no more tiles                  // one tile: 64 KB
 constexpr uint32_t kTMat = 2 * 128 * 128 * 2;         // B hi + lo: 64 KB
 constexpr uint32_t kTCtl = 3584;
-static_assert((10 + kExpSlots) * 8 + 64 * 8 + 64 * 8 + kTRing * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl,
+static_assert((12 + kExpSlots) * 8 + 64 * 8 + 64 * 8 + kTRing * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl,
               "K12 control block");
 constexpr uint32_t kTSmem = 2 * kTRaw + kTMat + kTCtl;
 
@@ -668,9 +668,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
     uint64_t* rempty = rfull + 2;                         // [2]
     uint64_t* afull = rempty + 2;                         // [2]
     uint64_t* aempty = afull + 2;                         // [2]
-    uint64_t* dfull = aempty + 2;                         // [1]
-    uint64_t* dempty = dfull + 1;                         // [1]
-    uint64_t* cready = dempty + 1;                        // [kExpSlots] column exponents of a tile written
+    uint64_t* dfull = aempty + 2;                         // [2] D half h (outputs n in [64 h, +64)) written
+    uint64_t* dempty = dfull + 2;                         // [2] ... and read by the epilogue
+    uint64_t* cready = dempty + 2;                        // [kExpSlots] column exponents of a tile written
     uint64_t* offt = cready + kExpSlots;                  // [64] physical offset of target combination t
     uint64_t* offr = offt + 64;                           // [64] physical offset of TMA run u
     uint64_t* tring = offr + 64;                          // [kTRing] tile base of iteration it (or kTileEnd)
@@ -691,8 +691,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             mbar_init(&afull[i], kLoadWarps * 32);
             mbar_init(&aempty[i], 1);
         }
-        mbar_init(dfull, 1);
-        mbar_init(dempty, kEpiThreads);
+        for (int h = 0; h < 2; h++) {
+            mbar_init(&dfull[h], 1);
+            mbar_init(&dempty[h], kEpiThreads);
+        }
         for (int e = 0; e < kExpSlots; e++) mbar_init(&cready[e], 128);   // the 128 column owners (th == 0)
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
@@ -858,38 +860,52 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             mbar_arrive(&afull[b]);
         }
     } else if (warp == kMmaWarp) {
-        // ---------------- MMA issuer: M = 128 (j), N = 128 (n = 2 t_o + c_o), K = 16 per step
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        // ---------------- MMA issuer: M = 128 (j), N = 64 per half (n = 2 t_o + c_o in [64 h, +64)),
+        // K = 16 per step.  D is split by output half: the epilogue drains half 0 while half 1
+        // is computed, and half 0 of the next tile starts as soon as its columns are read, so
+        // the MMAs overlap the TMEM reads (64 B/cycle: 2048 cycles per tile, the longest stage)
+        // instead of alternating with them.  Each output's K order is unchanged.
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         const uint64_t bh0 = bdesc(su32(mat)), bl0 = bdesc(su32(mat + kTMat / 2));
         for (uint64_t it = 0;; it++) {
             const int b = it & 1;
             mbar_wait(&afull[b], (it >> 1) & 1);
-            mbar_wait(dempty, (it & 1) ^ 1);
+            mbar_wait(&dempty[0], (it & 1) ^ 1);
             if (tring[it % kTRing] == kTileEnd) {   // end: hand the epilogue its last phase
-                if (lane == 0) mbar_arrive(dfull);
+                if (lane == 0) mbar_arrive(&dfull[0]);
                 break;
             }
             asm volatile("tcgen05.fence::after_thread_sync;");
-            if (lane == 0) {
-                const uint32_t d0 = tmem + 256;
-                const uint32_t xh = tmem + 128 * b, xl = xh + 64;   // state hi / lo (A)
-                // cross terms (x_hi u_lo, x_lo u_hi) -> acc 0; main x_hi u_hi (exact) -> acc 1
-                MMA_F16(d0, xh, bl0, idesc, 0);
-                MMA_F16(d0, xl, bh0, idesc, 1);
 #pragma unroll
-                for (int ks = 1; ks < 8; ks++) {
-                    MMA_F16(d0, xh + ks * 8, bl0 + ks * 16, idesc, 1);
-                    MMA_F16(d0, xl + ks * 8, bh0 + ks * 16, idesc, 1);
+            for (int h = 0; h < 2; h++) {
+                if (h) {
+                    mbar_wait(&dempty[1], (it & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
                 }
-                MMA_F16(d0 + 128, xh, bh0, idesc, 0);
+                if (lane == 0) {
+                    const uint32_t dc = tmem + 256 + 64 * h, dm = tmem + 384 + 64 * h;
+                    const uint32_t xh = tmem + 128 * b, xl = xh + 64;   // state hi / lo (A)
+                    const uint64_t bh = bh0 + 1024 * h, bl = bl0 + 1024 * h;   // + 64 n rows (16 KB)
+                    // cross terms (x_hi u_lo, x_lo u_hi) -> acc 0; main x_hi u_hi (exact) -> acc 1
+                    MMA_F16(dc, xh, bl, idesc, 0);
+                    MMA_F16(dc, xl, bh, idesc, 1);
 #pragma unroll
-                for (int ks = 1; ks < 8; ks++) MMA_F16(d0 + 128, xh + ks * 8, bh0 + ks * 16, idesc, 1);
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                    su32(&aempty[b])));
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                    su32(dfull)));
+                    for (int ks = 1; ks < 8; ks++) {
+                        MMA_F16(dc, xh + ks * 8, bl + ks * 16, idesc, 1);
+                        MMA_F16(dc, xl + ks * 8, bh + ks * 16, idesc, 1);
+                    }
+                    MMA_F16(dm, xh, bh, idesc, 0);
+#pragma unroll
+                    for (int ks = 1; ks < 8; ks++) MMA_F16(dm, xh + ks * 8, bh + ks * 16, idesc, 1);
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        su32(&dfull[h])));
+                    if (h)
+                        asm volatile(
+                            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                su32(&aempty[b])));
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ---------------- epilogue: lane quarter q holds columns j = 32 q + lane
@@ -900,7 +916,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             if ((j >> k) & 1) offj |= 1ull << p.jpos[k];
         for (uint64_t it = 0;; it++) {
             const int es = (int)(it % kExpSlots);
-            mbar_wait(dfull, it & 1);
+            mbar_wait(&dfull[0], it & 1);
             // the end marker is visible here (the MMA warp's plain arrive releases it); a tile's
             // base is guaranteed visible after cready (the converters read it after rfull)
             if (tring[it % kTRing] == kTileEnd) break;
@@ -912,13 +928,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256;
 #pragma unroll
             for (int s4 = 0; s4 < 4; s4++) {   // 32 columns n = 16 target combinations (re, im)
+                if (s4 == 2) {
+                    mbar_wait(&dfull[1], it & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
                 uint32_t a0[32], a1[32];
                 TMEM_LD32(ta + 32 * s4, a0);
                 TMEM_LD32(ta + 128 + 32 * s4, a1);
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
-                if (s4 == 3) {
+                if (s4 & 1) {   // half s4 / 2 read: its D columns are free for the next tile
                     asm volatile("tcgen05.fence::before_thread_sync;");
-                    mbar_arrive(dempty);
+                    mbar_arrive(&dempty[s4 >> 1]);
                 }
 #pragma unroll
                 for (int c = 0; c < 32; c += 2) {

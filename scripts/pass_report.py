@@ -10,7 +10,7 @@ c = rcs.Circuit.from_qasm(config_qasm(cfg))
 n = c.n_qubits
 ctx = rcs.Context(0)
 plan = rcs.Plan(c, k, 0)
-passes = [it for it in plan.items() if it["type"] == "pass"]
+passes = [it for it in plan.items()[plan.prefix:] if it["type"] == "pass"]   # prefix blocks: no pass
 st = None
 for rep in range(3):
     if st is not None:

@@ -211,15 +211,21 @@ def product_factors():
     return emit_qasm(circ), kron(range(half, N)), kron(range(half))
 
 
-@pytest.mark.parametrize("mode", ["loopback", "bitswap"])
+@pytest.mark.parametrize("mode", ["loopback", "bitswap", "prefix"])
 def test_product_state_n34_through_remaps(rcs, ctx, mode):
+    """loopback / bitswap: the blocks run as passes (product_prefix off) with 3 virtual global
+    qubits, so every remap path moves the state; prefix: the whole circuit is a product-state
+    prefix (every block acts on untouched qubits), written by the one prefix kernel."""
     text, f_hi, f_lo = product_factors()
-    kw = {"virtual_global": 3, "timing": True}
+    kw = {"virtual_global": 3, "timing": True, "product_prefix": mode == "prefix"}
     if mode == "loopback":
         kw["remap_mode"] = "loopback"
     with built(rcs, ctx, text, fuse_k=6, **kw) as st:
         rep = st.report
-        assert rep["n_remaps"] > 0, rep
+        if mode == "prefix":
+            assert rep["n_passes"] == 0 and rep["n_prefix"] > 0 and rep["n_remaps"] == 0, rep
+        else:
+            assert rep["n_remaps"] > 0 and rep["n_prefix"] == 0, rep
         if mode == "loopback":
             assert rep["n_peer_remaps"] > 0 and rep["remap_kernel_ms"] > 0, rep
         maxd, eps, _ = compare_kron(st.amps, f_hi, f_lo)

@@ -117,7 +117,9 @@ def test_plan_with_global_qubits_restores_canonical_order(rcs, g, grid):
     p = rcs.Plan(c, 6 if n - g >= 12 else 4, g)
     items = p.items()
     nl = n - g
-    for it in items:
+    for i, it in enumerate(items):
+        if i < p.prefix:   # product-state prefix blocks: written by one kernel, any position
+            continue
         if it["type"] == "pass":
             assert max(it["pos"]) < nl                          # blocks only touch local bits
         elif it["type"] == "remap":
