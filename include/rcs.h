@@ -119,6 +119,9 @@ typedef struct {
     int tc_schedule;         /* K12 tiles: 0 = static round robin (blockIdx + k gridDim), 1 = dynamic
                                 (a device counter hands tiles to the SMs as they free up; measured
                                 5 % slower at C4, profiles/r02/tiles_ab.txt)                      */
+    int tc_tma;              /* K12 loads: 0 = a tile whose contiguous runs are short (<= 256
+                                amplitudes) is fetched by a few 5-D tensor-map TMA requests (many
+                                runs each); -1 = one bulk copy per run                            */
 } rcs_build_opts;
 
 typedef struct {

@@ -32,7 +32,7 @@ class rcs_build_opts(C.Structure):
                 ("timing", C.c_int), ("staging_bytes", C.c_uint64), ("keep_layout", C.c_int),
                 ("remap_mode", C.c_int), ("overlap", C.c_int), ("overlap_chunks", C.c_int),
                 ("overlap_sms", C.c_int), ("tc_kernel", C.c_int), ("overlap_passes", C.c_int),
-                ("product_prefix", C.c_int), ("tc_schedule", C.c_int)]
+                ("product_prefix", C.c_int), ("tc_schedule", C.c_int), ("tc_tma", C.c_int)]
 
 
 class rcs_build_report(C.Structure):

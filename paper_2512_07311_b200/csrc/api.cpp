@@ -94,6 +94,7 @@ struct rcs_state {
     int remap_mode = RCS_REMAP_AUTO;
     int virt = 0;                    // virtual global qubits (world 1)
     unsigned* tiles = nullptr;       // K12 dynamic tile counter (the context's), nullptr: static tiles
+    int tc_flags = 0;                // dev::kTcForceK9 | dev::kTcBulkRuns (rcs_build_opts)
 };
 
 namespace {
@@ -243,9 +244,9 @@ rcs_status do_remap_nccl(rcs_state* s, const Item& it, uint64_t* bytes_sent, std
 }
 
 // Tensor-core items of a plan (6-qubit blocks; 5-qubit blocks padded to 6 with the identity on a
-// pinned qubit not in the block -- the lowest one, so the choice is a function of the block --
-// placed as matrix bit 0: then a block's highest qubit, the transposed kernel's converter-half
-// bit, never sits at one of the lowest cube ranks).
+// pinned qubit not in the block -- a function of the block -- placed as matrix bit 0: a block's
+// highest qubit, the transposed kernel's converter-half bit, then never sits at one of the lowest
+// cube ranks).
 void make_tc_pack(const Plan& P, int nl, TcPack& out) {
     out.slot.assign(P.items.size(), -1);
     out.pos.assign(P.items.size(), std::array<int, 6>{});
@@ -253,9 +254,10 @@ void make_tc_pack(const Plan& P, int nl, TcPack& out) {
     for (size_t ii = 0; ii < P.items.size(); ii++) {
         const Item& it = P.items[ii];
         if (it.type != RCS_ITEM_PASS || nl < kTcMinLocal || it.k < 5) continue;
-        if (it.k == 5) {   // pad qubit: lowest of the pinned qubits 0..5 not in the block
-            int pad = -1;
-            for (int b = 0; b < P.pinned && pad < 0; b++) {
+        if (it.k == 5) {   // pad qubit: the first of the pinned positions 4, 5, 6, 0, 1, 2, 3 not in
+            int pad = -1;    // the block (one above 3 keeps a second target out of positions 0..3,
+            for (int c = 0; c < P.pinned && pad < 0; c++) {   // which would send the block to K9)
+                const int b = (c + 4) % P.pinned;
                 bool used = false;
                 for (int i = 0; i < 5; i++) used = used || it.pos[i] == b;
                 if (!used) pad = b;
@@ -398,7 +400,8 @@ rcs_status setup_peers(rcs_context* c, void* amps, int remap_mode, rcs_error* er
 // over the ranks, their costs (fuse_cost) all-gathered, and the winning rank (lowest cost, ties to
 // the lower strategy -- the single-process rule, so the plan equals the 1-GPU plan) broadcasts
 // its blocks; every rank then derives matrices and remaps itself.
-rcs_status plan_distributed(rcs_context* c, const Circuit& circ, int fuse_k, int plan_g, Plan& out, rcs_error* err) {
+rcs_status plan_distributed(rcs_context* c, const Circuit& circ, int fuse_k, int plan_g, Plan& out, rcs_error* err,
+                            bool use_prefix) {
     const int k = plan_block_k(circ.n, fuse_k, plan_g);
     std::vector<Block> mine[kFuseStrategies];
     int64_t cnt[kFuseStrategies];
@@ -474,7 +477,7 @@ rcs_status plan_distributed(rcs_context* c, const Circuit& circ, int fuse_k, int
         for (int64_t i = 0; i < ng; i++) B.gate_ids.push_back((int)buf[at++]);
         blocks.push_back(std::move(B));
     }
-    return build_plan(circ, fuse_k, plan_g, out, err, &blocks);
+    return build_plan(circ, fuse_k, plan_g, out, err, &blocks, use_prefix);
 }
 
 // stream-ordered barrier over all ranks (no rank proceeds past it before every rank reached it)
@@ -612,7 +615,7 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
     // A: all chunks, in order, on the main stream
     for (int ch = 0; ch < nch; ch++) {
         if (pa)
-            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch), force_k9,
+            CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pa->pos, pa->d_a, sms, c->stream, fix, cb, fixval(ch), s->tc_flags,
                                        s->tiles));
         CUDA_TRY(cudaEventRecord(c->ev_a[ch], c->stream));
     }
@@ -650,7 +653,7 @@ rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, c
             if (i == 0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_s[ch], 0));
             cudaEvent_t w = spans ? tev(c->stream) : nullptr;
             CUDA_TRY(dev::gate_pass_tc(s->amps, s->nl, pbs[i].pos, pbs[i].d_a, sms, c->stream, fix, cb, fixval(ch),
-                                       force_k9, s->tiles));
+                                       s->tc_flags, s->tiles));
             if (spans) {
                 cudaEvent_t e = tev(c->stream);
                 spans->push_back({ibs[i], w, e, 1});
@@ -1066,7 +1069,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     if (o.remap_mode < RCS_REMAP_AUTO || o.remap_mode > RCS_REMAP_LOOPBACK ||
         (o.remap_mode == RCS_REMAP_LOOPBACK && (ctx->world != 1 || o.virtual_global < 1 || o.virtual_global > 3)) ||
         o.overlap_chunks < 0 || o.overlap_chunks > 4 || o.overlap_sms < 0 || o.tc_kernel < 0 || o.tc_kernel > 1 ||
-        o.overlap_passes < 0 || o.overlap_passes > 8 || o.tc_schedule < 0 || o.tc_schedule > 1 ||
+        o.overlap_passes < 0 || o.overlap_passes > 8 || o.tc_schedule < 0 || o.tc_schedule > 1 || o.tc_tma < -1 || o.tc_tma > 0 ||
         o.product_prefix < -1 || o.product_prefix > 0 ||
         o.virtual_global < 0) {
         set_error(err, RCS_ERR_ARG, "invalid build options (remap_mode %d, virtual_global %d, overlap_chunks %d)",
@@ -1092,17 +1095,21 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
 
     auto t0 = std::chrono::steady_clock::now();
     std::shared_ptr<const Plan> plan_ptr;
+    // product_prefix off: the plan has no prefix (its blocks are remapped like any other); the
+    // plan and the caches derived from it are keyed on that too
+    const bool use_prefix = o.product_prefix >= 0 && nl >= 6;   // the kernel writes 64-amplitude rows
+    const int pkey = o.fuse_k | (use_prefix ? 0 : 1 << 8);
     {
         rcs_circuit* cc = const_cast<rcs_circuit*>(circ);
         std::lock_guard<std::mutex> lk(cc->mu);
-        auto key = std::make_pair(o.fuse_k, plan_g);
+        auto key = std::make_pair(pkey, plan_g);
         auto f = cc->plans.find(key);
         if (f != cc->plans.end()) {
             plan_ptr = f->second;
         } else {
             auto np = std::make_shared<Plan>();
-            rcs_status pst = ctx->world > 1 ? plan_distributed(ctx, circ->c, o.fuse_k, plan_g, *np, err)
-                                            : build_plan(circ->c, o.fuse_k, plan_g, *np, err);
+            rcs_status pst = ctx->world > 1 ? plan_distributed(ctx, circ->c, o.fuse_k, plan_g, *np, err, use_prefix)
+                                            : build_plan(circ->c, o.fuse_k, plan_g, *np, err, nullptr, use_prefix);
             if (pst) return pst;
             plan_ptr = np;
             cc->plans[key] = plan_ptr;
@@ -1191,7 +1198,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     {
         rcs_circuit* cc = const_cast<rcs_circuit*>(circ);
         std::lock_guard<std::mutex> lk(cc->mu);
-        auto key = std::make_tuple(o.fuse_k, plan_g, nl);
+        auto key = std::make_tuple(pkey, plan_g, nl);
         auto f = cc->packs.find(key);
         if (f != cc->packs.end()) {
             tcp = f->second;
@@ -1215,14 +1222,14 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         ctx->tc_cap = tc_words;
     }
     // product-state prefix: cached per (circuit, plan), device copy per context
-    const int n_prefix = o.product_prefix >= 0 ? P.prefix : 0;
+    const int n_prefix = P.prefix;
     std::shared_ptr<const PrefixPack> pfp;
     size_t pf_bytes[3] = {0, 0, 0};
     bool pf_upload = false;
     if (n_prefix > 0) {
         rcs_circuit* cc = const_cast<rcs_circuit*>(circ);
         std::lock_guard<std::mutex> lk(cc->mu);
-        auto key = std::make_pair(o.fuse_k, plan_g);
+        auto key = std::make_pair(pkey, plan_g);
         auto f = cc->prefix_packs.find(key);
         if (f != cc->prefix_packs.end()) {
             pfp = f->second;
@@ -1251,6 +1258,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     }
     if (n_tc > 0 && !ctx->d_tiles && o.tc_schedule == 1) BUILD_TRY(cudaMalloc(&ctx->d_tiles, 64));
     s->tiles = o.tc_schedule == 1 ? ctx->d_tiles : nullptr;
+    s->tc_flags = (o.tc_kernel == 1 ? dev::kTcForceK9 : 0) | (o.tc_tma == -1 ? dev::kTcBulkRuns : 0);
     BUILD_TRY(cudaEventRecord(eb0, stream));
     cudaEvent_t epf0 = nullptr;
     if (tc_upload) {
@@ -1361,7 +1369,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         }
         if (it.type == RCS_ITEM_PASS && tc_slot[ii] >= 0) {
             BUILD_TRY(dev::gate_pass_tc(s->amps, nl, tcp->pos[ii].data(), ctx->d_tc + (size_t)tc_slot[ii] * tc_words_each,
-                                        ctx->num_sms, stream, nullptr, 0, 0, force_k9, s->tiles));
+                                        ctx->num_sms, stream, nullptr, 0, 0, s->tc_flags, s->tiles));
             pass_bytes += 16ull * n_amps;
         } else if (it.type == RCS_ITEM_PASS) {
             const Block& B = P.blocks[it.block];

@@ -94,8 +94,9 @@ constexpr bool kInitialPlacement = true;   // start with the latest-used qubits 
 constexpr int kPrefixGroupBits = 18;      // product-state prefix: qubits per table (2^18 x 16 B = 4 MiB)
 
 // given: the fused blocks (qubits + gate ids) to use instead of running the fuser
+// use_prefix = false: no product-state prefix (every block is a pass and is remapped as one)
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err,
-                      const std::vector<Block>* given = nullptr);
+                      const std::vector<Block>* given = nullptr, bool use_prefix = true);
 // strategies: plain greedy, 3-level extension search, prefix-first greedy, prefix-first 1-level,
 // prefix-first with a 1-level prefix phase and a 3-level rest (plan.cpp fuse_strategy_memo)
 constexpr int kFuseStrategies = 5;

@@ -285,13 +285,39 @@ __global__ void __launch_bounds__(kSumWarps * 32) k_block_sums(const float2* __r
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t B = 1ull << b;
     double sq = 0.0;
-    for (uint64_t blk = (uint64_t)blockIdx.x * kSumWarps + wid; blk < nblocks; blk += (uint64_t)gridDim.x * kSumWarps) {
+    const uint64_t W = (uint64_t)gridDim.x * kSumWarps;
+    uint64_t blk = (uint64_t)blockIdx.x * kSumWarps + wid;
+    if (B == 64) {
+        // four blocks per warp in flight (the blocks blk + i W of the plain grid-stride loop, in the
+        // same order, so every sum and the running sq are bitwise those of one block at a time)
+        for (; blk < nblocks; blk += 4 * W) {
+            float4 v[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                v[i] = blk + i * W < nblocks ? reinterpret_cast<const float4*>(a + (blk + i * W) * 64)[lane]
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            double p0[4], p1[4], t[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                p0[i] = (double)v[i].x * v[i].x + (double)v[i].y * v[i].y;
+                p1[i] = (double)v[i].z * v[i].z + (double)v[i].w * v[i].w;
+                t[i] = p0[i] + p1[i];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < 4; i++) t[i] += __shfl_xor_sync(0xffffffffu, t[i], o);
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                if (blk + i * W < nblocks) {
+                    if (lane == 0) bsum[blk + i * W] = t[i];
+                    sq += p0[i] * p0[i] + p1[i] * p1[i];
+                }
+        }
+    }
+    for (; B != 64 && blk < nblocks; blk += W) {
         double p0 = 0.0, p1 = 0.0;
-        if (B == 64) {
-            const float4 v = reinterpret_cast<const float4*>(a + blk * 64)[lane];
-            p0 = (double)v.x * v.x + (double)v.y * v.y;
-            p1 = (double)v.z * v.z + (double)v.w * v.w;
-        } else {
+        {
             const uint64_t i0 = 2 * lane, i1 = 2 * lane + 1;
             if (i0 < B) { const float2 v = a[blk * B + i0]; p0 = (double)v.x * v.x + (double)v.y * v.y; }
             if (i1 < B) { const float2 v = a[blk * B + i1]; p1 = (double)v.x * v.x + (double)v.y * v.y; }
@@ -743,39 +769,57 @@ __global__ void __launch_bounds__(kThreads) k_product_init(const __grid_constant
         bt[G][r >> 8][r & 255] = a.byt[e];
     }
     __syncthreads();
-    const uint64_t npair = a.n_amps >> 1;
+    // A warp writes rows of 64 amplitudes (2 per lane, one 16-B store each) from a contiguous
+    // range of rows, four rows (256 amplitudes: byte 0 of X) at a time, so the table-index parts
+    // of X's bytes >= 1 are warp-uniform per group and all 16 table reads of a group are in
+    // flight together.
+    const int lane = threadIdx.x & 31;
+    const uint64_t nrows = a.n_amps >> 6;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kThreads / 32);
+    const uint64_t w = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const uint64_t per = ((nrows + nwarps - 1) / nwarps + 3) & ~3ull;   // rows per warp, multiple of 4
+    const uint64_t r0 = w * per, r1 = r0 + per < nrows ? r0 + per : nrows;
     float4* out = reinterpret_cast<float4*>(a.amps);
-    for (uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x; v < npair; v += (uint64_t)gridDim.x * kThreads) {
-        const uint64_t X = a.base + 2 * v;   // even: the pair differs in bit 0 only
-        if (X & a.zmask & ~1ull) {           // a qubit outside the prefix is |1>: both amplitudes 0
-            out[v] = make_float4(0.f, 0.f, 0.f, 0.f);   // (no table reads: most of the state)
-            continue;
-        }
-        uint32_t ia = 0, ib = 0;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    for (uint64_t g = r0; g < r1; g += 4) {
+        const uint64_t Xg = a.base + (g << 6);   // byte 0 of Xg is 0 (g is a multiple of 4)
+        uint32_t ha = 0, hb = 0;
         for (int c = 1; c < a.nbytes; c++) {
-            const int by = (int)((X >> (8 * c)) & 255);
-            ia |= bt[0][c][by];
-            ib |= bt[1][c][by];
+            const int by = (int)((Xg >> (8 * c)) & 255);
+            ha |= bt[0][c][by];
+            hb |= bt[1][c][by];
         }
-        float r[4];
+        // a qubit outside the prefix set to |1> in bytes >= 1: the whole group is 0
+        const bool zhi = (Xg & a.zmask & ~255ull) != 0;
+        double2 A[8], B[8];
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-            const int by = (int)((X & 254) | e);
-            const double2 A = a.tab[0][ia | bt[0][0][by]], B = a.tab[1][ib | bt[1][0][by]];
-            const bool zero = ((X | (uint64_t)e) & a.zmask) != 0;
-            const double re = __dsub_rn(__dmul_rn(A.x, B.x), __dmul_rn(A.y, B.y));
-            const double im = __dadd_rn(__dmul_rn(A.x, B.y), __dmul_rn(A.y, B.x));
-            r[2 * e] = zero ? 0.f : __double2float_rn(re);
-            r[2 * e + 1] = zero ? 0.f : __double2float_rn(im);
+        for (int k = 0; k < 8; k++) {   // k = 2 rr + e: row g + rr, amplitude 2 lane + e
+            const int by = ((k >> 1) << 6) | (2 * lane) | (k & 1);
+            const bool live = !zhi && g + (k >> 1) < r1 && ((uint64_t)by & a.zmask) == 0;
+            A[k] = live ? __ldg(&a.tab[0][ha | bt[0][0][by]]) : zero2;
+            B[k] = live ? __ldg(&a.tab[1][hb | bt[1][0][by]]) : zero2;
         }
-        out[v] = make_float4(r[0], r[1], r[2], r[3]);
+#pragma unroll
+        for (int rr = 0; rr < 4; rr++) {
+            if (g + rr >= r1) break;
+            float r[4];
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const double2 x = A[2 * rr + e], y = B[2 * rr + e];
+                const double re = __dsub_rn(__dmul_rn(x.x, y.x), __dmul_rn(x.y, y.y));
+                const double im = __dadd_rn(__dmul_rn(x.x, y.y), __dmul_rn(x.y, y.x));
+                r[2 * e] = __double2float_rn(re);
+                r[2 * e + 1] = __double2float_rn(im);
+            }
+            __stcs(out + (((g + rr) << 5) | lane), make_float4(r[0], r[1], r[2], r[3]));
+        }
     }
 }
 
 cudaError_t product_init(const PrefixArgs& a, cudaStream_t st) {
-    if (a.n_amps < 2 || (a.n_amps & 1) || a.nbytes < 1 || a.nbytes > kPrefixBytes) return cudaErrorInvalidValue;
+    if (a.n_amps < 64 || (a.n_amps & 63) || a.nbytes < 1 || a.nbytes > kPrefixBytes) return cudaErrorInvalidValue;
     note_launch();
-    k_product_init<<<grid_for(a.n_amps / 2), kThreads, 0, st>>>(a);
+    k_product_init<<<grid_for(a.n_amps / 64), kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -26,9 +26,12 @@ void tc_pack_matrix(const double* u_re_im, uint32_t* out);
 bool tc_uses_k12(int n_local_bits, const int* pos);
 // tile_counter (one device word, may be nullptr): K12 hands tiles out through it (zeroed here,
 // stream-ordered) instead of the static blockIdx.x + k gridDim.x assignment.
+// tc_flags: kTcForceK9 (every block on K9), kTcBulkRuns (K12 loads its runs with plain bulk copies
+// even when they are short; default: a 5-D tensor-map TMA moves many short runs per request).
+constexpr int kTcForceK9 = 1, kTcBulkRuns = 2;
 cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const uint32_t* d_a, int num_sms,
                          cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0,
-                         bool force_k9 = false, unsigned* tile_counter = nullptr);
+                         int tc_flags = 0, unsigned* tile_counter = nullptr);
 // positions a chunk bit must avoid for this pass: the 12-bit tile sub-cube and the bit above its run
 uint64_t tc_reserved_mask(int n_local_bits, const int* pos);
 // a6 (K1) fused dense gate pass: amps <- M (x) over every group of 2^k amplitudes that

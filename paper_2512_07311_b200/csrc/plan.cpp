@@ -550,7 +550,7 @@ int plan_block_k(int n, int fuse_k, int n_global) {
 }
 
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err,
-                      const std::vector<Block>* given) {
+                      const std::vector<Block>* given, bool use_prefix) {
     if (fuse_k > 6) {
         set_error(err, RCS_ERR_ARG, "fuse_k must be in [1, 6] (got %d)", fuse_k);
         return RCS_ERR_ARG;
@@ -613,7 +613,7 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
             else rest.push_back(std::move(B));
             seen |= mk;
         }
-        int m = (int)front.size();
+        int m = use_prefix ? (int)front.size() : 0;
         P.blocks = std::move(front);
         for (Block& B : rest) P.blocks.push_back(std::move(B));
         // groups: A = the first blocks up to half of the prefix qubits, B = the rest; drop

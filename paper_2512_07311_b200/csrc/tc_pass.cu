@@ -39,6 +39,7 @@
 // Shared memory: raw 4 x 32 KB + B 2 x 32 KB + staging 33 KB + control = 227 KB.
 // TMEM (512 cols): A_hi [0,64), A_lo [64,128) (fp16 pairs), D[d] = [128 + 128 d, +128) holding
 // the cross-term and main-term accumulators (64 columns each).
+#include <cuda.h>   // CUtensorMap (the encoder is fetched through cudaGetDriverEntryPoint)
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -179,6 +180,29 @@ __device__ __forceinline__ float2 f2mul(float2 v, float s) {   // packed f32x2 m
                    "=r"(R[20]), "=r"(R[21]), "=r"(R[22]), "=r"(R[23]), "=r"(R[24]), "=r"(R[25]),              \
                    "=r"(R[26]), "=r"(R[27]), "=r"(R[28]), "=r"(R[29]), "=r"(R[30]), "=r"(R[31])               \
                  : "r"(addr))
+
+// the registers of a tcgen05.ld are defined by tcgen05.wait::ld, not by the ld: pin every use
+// after the wait
+// ... ordered with memory accesses (the epilogue issues the next chunk's loads before its stores)
+#define TMEM_LD32M(addr, R)                                                                                     \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+                 "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"               \
+                 : "=r"(R[0]), "=r"(R[1]), "=r"(R[2]), "=r"(R[3]), "=r"(R[4]), "=r"(R[5]), "=r"(R[6]),        \
+                   "=r"(R[7]), "=r"(R[8]), "=r"(R[9]), "=r"(R[10]), "=r"(R[11]), "=r"(R[12]), "=r"(R[13]),    \
+                   "=r"(R[14]), "=r"(R[15]), "=r"(R[16]), "=r"(R[17]), "=r"(R[18]), "=r"(R[19]),              \
+                   "=r"(R[20]), "=r"(R[21]), "=r"(R[22]), "=r"(R[23]), "=r"(R[24]), "=r"(R[25]),              \
+                   "=r"(R[26]), "=r"(R[27]), "=r"(R[28]), "=r"(R[29]), "=r"(R[30]), "=r"(R[31])               \
+                 : "r"(addr)                                                                                  \
+                 : "memory")
+
+// the registers of a tcgen05.ld are defined by tcgen05.wait::ld, not by the ld: pin every use
+// after the wait
+#define REG_FENCE32(R)                                                                                       \
+    asm volatile("" : "+r"(R[0]), "+r"(R[1]), "+r"(R[2]), "+r"(R[3]), "+r"(R[4]), "+r"(R[5]), "+r"(R[6]),     \
+                 "+r"(R[7]), "+r"(R[8]), "+r"(R[9]), "+r"(R[10]), "+r"(R[11]), "+r"(R[12]), "+r"(R[13]),       \
+                 "+r"(R[14]), "+r"(R[15]), "+r"(R[16]), "+r"(R[17]), "+r"(R[18]), "+r"(R[19]), "+r"(R[20]),    \
+                 "+r"(R[21]), "+r"(R[22]), "+r"(R[23]), "+r"(R[24]), "+r"(R[25]), "+r"(R[26]), "+r"(R[27]),    \
+                 "+r"(R[28]), "+r"(R[29]), "+r"(R[30]), "+r"(R[31]))
 
 #define MMA_F16(d, a, b, idesc, acc)                                                                         \
     asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, " #acc ";" ::"r"(d), "r"(a), "l"(b), \
@@ -618,8 +642,25 @@ struct TcTArgs {
     uint64_t fixval;         // chunk bits (pipelined remaps), as K9
     uint64_t fmask, dstride; // tile-index deposit (as K9)
     unsigned* counter;       // dynamic tile scheduler (zeroed before the launch), nullptr: static
+    // Short runs (r <= 8: 64 or 32 copies of 1-2 KB per tile) go through a 5-D tensor map instead:
+    // dim 0 = the 2^r contiguous amplitudes, dim 1 = the tile base in units of 2^r amplitudes
+    // (box 1), dims 2..4 = the lowest groups of consecutive run positions (extent 2^m, stride 2^p
+    // amplitudes).  Each request fills a contiguous range of the slot in cube-index order; the
+    // run bits the dims do not cover select the request (treq[u], added to the dim-1 coordinate).
+    int nreq;                // 0: one bulk copy per run
+    uint32_t req_bytes;      // bytes per request (8192 * 8 / nreq)
+    int treq[8];             // per request: dim-4 coordinate offset (units of 2^r amplitudes)
+    alignas(64) CUtensorMap tmap;
 };
 
+// build-time variants for A/B measurements (RCS_NVCC_FLAGS=-D...): D split into two N = 64 halves,
+// epilogue loads of the next chunk issued before the current chunk's stores
+#ifndef RCS_K12_NSPLIT
+#define RCS_K12_NSPLIT 1
+#endif
+#ifndef RCS_K12_EPIPIPE
+#define RCS_K12_EPIPIPE 1
+#endif
 constexpr uint32_t kTRaw = 8192 * 8;
 constexpr int kTRing = 8;                             // tile bases in flight (producer -> all roles)
 constexpr uint64_t kTileEnd = ~0ull;                  // ring sentinel: no more tiles                  // one tile: 64 KB
@@ -768,12 +809,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             __syncwarp();
             const float2* src = p.amps + (bp | p.fixval);
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
-            for (int u = lane; u < nruns; u += 32)
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        dst + u * run_bytes),
-                    "l"(src + offr[u]), "r"(run_bytes), "r"(su32(&rfull[slot]))
-                    : "memory");
+            if (p.nreq) {
+                if (lane < p.nreq) {
+                    const int cb = (int)((bp | p.fixval) >> p.r) + p.treq[lane];
+                    asm volatile(
+                        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                        "%3, %4, %5, %6}], [%7];" ::"r"(dst + lane * p.req_bytes),
+                        "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(0), "r"(cb), "r"(0), "r"(0), "r"(0),
+                        "r"(su32(&rfull[slot]))
+                        : "memory");
+                }
+            } else {
+                for (int u = lane; u < nruns; u += 32)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst + u * run_bytes),
+                        "l"(src + offr[u]), "r"(run_bytes), "r"(su32(&rfull[slot]))
+                        : "memory");
+            }
             if (p.counter) {
                 tile = __shfl_sync(0xffffffffu, nxt, 0);
             } else {
@@ -865,19 +918,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         // is computed, and half 0 of the next tile starts as soon as its columns are read, so
         // the MMAs overlap the TMEM reads (64 B/cycle: 2048 cycles per tile, the longest stage)
         // instead of alternating with them.  Each output's K order is unchanged.
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        constexpr int NH = RCS_K12_NSPLIT ? 2 : 1;   // 1: one N = 128 group (both halves at once)
+        const uint32_t idesc = (1u << 4) | ((uint32_t)((128 / NH) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         const uint64_t bh0 = bdesc(su32(mat)), bl0 = bdesc(su32(mat + kTMat / 2));
         for (uint64_t it = 0;; it++) {
             const int b = it & 1;
             mbar_wait(&afull[b], (it >> 1) & 1);
             mbar_wait(&dempty[0], (it & 1) ^ 1);
+            if (NH == 1) mbar_wait(&dempty[1], (it & 1) ^ 1);
             if (tring[it % kTRing] == kTileEnd) {   // end: hand the epilogue its last phase
                 if (lane == 0) mbar_arrive(&dfull[0]);
                 break;
             }
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
+            for (int h = 0; h < NH; h++) {
                 if (h) {
                     mbar_wait(&dempty[1], (it & 1) ^ 1);
                     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -899,7 +954,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                     for (int ks = 1; ks < 8; ks++) MMA_F16(dm, xh + ks * 8, bh + ks * 16, idesc, 1);
                     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                         su32(&dfull[h])));
-                    if (h)
+                    if (NH == 1)
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                            su32(&dfull[1])));
+                    if (h == NH - 1)
                         asm volatile(
                             "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                                 su32(&aempty[b])));
@@ -926,6 +984,54 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             asm volatile("tcgen05.fence::after_thread_sync;");
             float2* dst = p.amps + (tb | offj);
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256;
+#if RCS_K12_EPIPIPE
+            // Four chunks of 32 D columns (16 target combinations, re/im).  The next chunk's TMEM
+            // loads are issued before this chunk's stores, so the stores overlap the TMEM reads
+            // (the epilogue's longest part: 64 B/cycle); two register sets alternate.
+            uint32_t a0[32], a1[32], b0[32], b1[32];
+            TMEM_LD32(ta, a0);
+            TMEM_LD32(ta + 128, a1);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            REG_FENCE32(a0);
+            REG_FENCE32(a1);
+            auto chunk = [&](const int s4, uint32_t(&x0)[32], const uint32_t(&x1)[32], uint32_t(&y0)[32],
+                             uint32_t(&y1)[32]) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {   // in place: x0 <- ((cross + main) 2^-E_j) 2^-F_t
+                    const float rf = rowfac[16 * s4 + c / 2];
+                    asm("{\n.reg .b64 x, y, u, v;\n"
+                        "mov.b64 x, {%0, %1};\nmov.b64 y, {%2, %3};\nmov.b64 u, {%4, %4};\nmov.b64 v, {%5, %5};\n"
+                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\nmul.rn.f32x2 x, x, v;\n"
+                        "mov.b64 {%0, %1}, x;\n}"
+                        : "+r"(x0[c]), "+r"(x0[c + 1])
+                        : "r"(x1[c]), "r"(x1[c + 1]), "f"(cf), "f"(rf));
+                }
+                if (s4 & 1) {   // half s4 / 2 read: its D columns are free for the next tile
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    mbar_arrive(&dempty[s4 >> 1]);
+                }
+                if (s4 < 3) {
+                    if (s4 == 1) {
+                        mbar_wait(&dfull[1], it & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                    }
+                    TMEM_LD32M(ta + 32 * (s4 + 1), y0);
+                    TMEM_LD32M(ta + 128 + 32 * (s4 + 1), y1);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; c += 2)
+                    __stcs(dst + offt[16 * s4 + c / 2], make_float2(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1])));
+                if (s4 < 3) {
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    REG_FENCE32(y0);
+                    REG_FENCE32(y1);
+                }
+            };
+            chunk(0, a0, a1, b0, b1);
+            chunk(1, b0, b1, a0, a1);
+            chunk(2, a0, a1, b0, b1);
+            chunk(3, b0, b1, a0, a1);
+#else
 #pragma unroll
             for (int s4 = 0; s4 < 4; s4++) {   // 32 columns n = 16 target combinations (re, im)
                 if (s4 == 2) {
@@ -953,6 +1059,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                     __stcs(dst + offt[16 * s4 + c / 2], make_float2(o0, o1));
                 }
             }
+#endif
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1015,9 +1122,77 @@ uint64_t tc_reserved_mask(int nl, const int* pos) {
     return m;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link); nullptr if
+// unavailable (the launcher then keeps the bulk copies)
+using TmapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encoder() {
+    static TmapEncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (TmapEncodeFn) nullptr;
+        return reinterpret_cast<TmapEncodeFn>(f);
+    }();
+    return fn;
+}
+
+// the 5-D tensor map of a K12 tile whose runs are 2^r <= 256 amplitudes (TcTArgs::nreq); false:
+// not expressible (the launcher keeps one bulk copy per run)
+static bool tct_tensor_map(TcTArgs& p, int nl) {
+    TmapEncodeFn enc = tmap_encoder();
+    if (!enc || p.r > 8 || nl - p.r > 31) return false;
+    // groups of consecutive run positions, ascending
+    int gp[6], gm[6], ng = 0;
+    for (int i = 0; i < p.nrun_pos; i++) {
+        if (ng && p.run_pos[i] == gp[ng - 1] + gm[ng - 1]) {
+            gm[ng - 1]++;
+        } else {
+            gp[ng] = p.run_pos[i];
+            gm[ng++] = 1;
+        }
+    }
+    // dim 1 (box 1) carries the tile base, so the strides ascend; unused dims: extent 1
+    cuuint64_t dim[5] = {1ull << p.r, 1ull << (nl - p.r), 1, 1, 1};
+    cuuint64_t stride[4] = {8ull << p.r, 0, 0, 0};   // bytes, dims 1..4
+    cuuint32_t box[5] = {1u << p.r, 1, 1, 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const int nd = ng < 3 ? ng : 3;
+    int covered = 0;
+    for (int d = 0; d < 3; d++) {
+        if (d < nd) {
+            dim[2 + d] = 1ull << gm[d];
+            stride[1 + d] = 8ull << gp[d];
+            box[2 + d] = 1u << gm[d];
+            covered += gm[d];
+        } else {
+            stride[1 + d] = stride[d];
+        }
+    }
+    const int rest = p.nrun_pos - covered;   // run bits enumerated by requests
+    if (rest > 3) return false;
+    p.nreq = 1 << rest;
+    p.req_bytes = kTRaw >> rest;
+    int rp[6], nrp = 0;
+    for (int d = nd; d < ng; d++)
+        for (int b = 0; b < gm[d]; b++) rp[nrp++] = gp[d] + b;
+    for (int u = 0; u < p.nreq; u++) {
+        int off = 0;
+        for (int b = 0; b < nrp; b++)
+            if ((u >> b) & 1) off += 1 << (rp[b] - p.r);
+        p.treq[u] = off;
+    }
+    return enc(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, p.amps, dim, stride, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // K12 launcher: any target layout, n_local >= 13 (+ chunk bits)
 static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms,
-                                 cudaStream_t st, const int* fix, int nfix, uint64_t fixval, unsigned* counter) {
+                                 cudaStream_t st, const int* fix, int nfix, uint64_t fixval, unsigned* counter,
+                                 bool bulk_runs) {
     TcTArgs p{};
     p.amps = amps;
     p.a = d_a;
@@ -1050,6 +1225,8 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
     for (int b = p.r; b < nl; b++)
         if ((cube >> b) & 1) p.run_pos[p.nrun_pos++] = b;
     if (p.nrun_pos != 13 - p.r) return cudaErrorInvalidValue;
+    p.nreq = 0;
+    if (!bulk_runs && !tct_tensor_map(p, nl)) p.nreq = 0;
     // bank-conflict-free converter reads: with one target at cube rank < 4, column bit 3 is
     // displaced to rank 4 and the lanes with it set read t ^ (that target's bit); t bit 5 (the
     // converter half) must not be it.  More low targets: K9 (tc_uses_k12).
@@ -1110,9 +1287,10 @@ bool tc_uses_k12(int nl, const int* pos) {
 }
 
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
-                         const int* fix, int nfix, uint64_t fixval, bool force_k9, unsigned* tile_counter) {
-    if (!force_k9 && tc_uses_k12(nl, pos))
-        return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval, tile_counter);
+                         const int* fix, int nfix, uint64_t fixval, int tc_flags, unsigned* tile_counter) {
+    if (!(tc_flags & kTcForceK9) && tc_uses_k12(nl, pos))
+        return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval, tile_counter,
+                             (tc_flags & kTcBulkRuns) != 0);
     if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
     p.amps = amps;

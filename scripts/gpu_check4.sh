@@ -2,7 +2,7 @@
 # 1-GPU check: quick K12/K9 parity vs the oracle, C4 bench, K12 per-launch time at ncu's base
 # clock and unlocked (SM-cycle bound?), prefix-kernel time, whole GPU suite, smoke.
 cd "$(dirname "$0")/.."
-O=gpurun_out/check4; mkdir -p $O
+O=gpurun_out/${CHECK:-check4}; mkdir -p $O
 python -m paper_2512_07311_b200.build > $O/build.log 2>&1 || { echo BUILD FAILED; cat $O/build.log; exit 1; }
 timeout 300 python - > $O/quick.log 2>&1 <<'PY'
 import numpy as np, oracle, paper_2512_07311_b200 as rcs

@@ -150,6 +150,39 @@ def test_dynamic_tile_schedule_bitwise(rcs, ctx, case):
     assert na == b.norm
 
 
+@pytest.mark.parametrize("case", ["c2", "c3", "loop"])
+def test_tensor_map_runs_bitwise(rcs, ctx, case):
+    """K12 fetches tiles whose contiguous runs are short (2^r <= 256 amplitudes) with a few 5-D
+    tensor-map TMA requests instead of one bulk copy per run; only the copy engine's request shape
+    changes, so the state equals the bulk-copy build bit for bit (C3: n = 32, every pass kind;
+    loop: n = 20 with 2 virtual global qubits, pipelined remap chunks as fixed index bits)."""
+    if case == "loop":
+        c = rcs.Circuit.from_qasm(emit_qasm(generate(4, 5, 10, "ABCDCDAB", seed=3)))
+        kw = {"virtual_global": 2, "remap_mode": "loopback"}
+    else:
+        c = rcs.Circuit.from_qasm(config_qasm(case))
+        kw = {}
+    def run(tma):
+        st = rcs.State.build(ctx, c, fuse_k=6, tc_tma=tma, **kw)
+        if case == "c3":
+            out = (st.copy_out(0, 1 << 22), st.copy_out((1 << 31) + (5 << 22), 1 << 22),
+                   st.copy_out((1 << 32) - (1 << 22), 1 << 22))
+        else:
+            out = (st.copy_out(),)
+        nrm = st.norm
+        st.free()
+        return out, nrm
+    pa, na = run("auto")
+    pb, nb = run("bulk")
+    assert all(np.array_equal(x, y) for x, y in zip(pa, pb)) and na == nb
+    if case != "c3":
+        check_amps(pa[0].astype(np.complex128), oracle.build_state(c_text(case)))
+
+
+def c_text(case):
+    return emit_qasm(generate(4, 5, 10, "ABCDCDAB", seed=3)) if case == "loop" else config_qasm(case)
+
+
 @pytest.mark.parametrize("g", [1, 2, 3])
 def test_keep_layout_matches_canonical(rcs, ctx, g):
     """keep_layout skips the final restore; the logical-order CDF over the permuted layout gives
