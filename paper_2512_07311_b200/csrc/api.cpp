@@ -314,8 +314,8 @@ void make_prefix_pack(const Plan& P, PrefixPack& out) {
     for (int G = 0; G < 2; G++) {
         out.tab[G].resize(2 * P.tab[G].size());
         for (size_t i = 0; i < P.tab[G].size(); i++) {
-            out.tab[G][2 * i] = P.tab[G][i].re;
-            out.tab[G][2 * i + 1] = P.tab[G][i].im;
+            out.tab[G][2 * i] = (float)P.tab[G][i].re;
+            out.tab[G][2 * i + 1] = (float)P.tab[G][i].im;
         }
     }
 }
@@ -1239,8 +1239,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
             pfp = np;
             cc->prefix_packs[key] = pfp;
         }
-        pf_bytes[0] = pfp->tab[0].size() * sizeof(double);
-        pf_bytes[1] = pfp->tab[1].size() * sizeof(double);
+        pf_bytes[0] = pfp->tab[0].size() * sizeof(float);
+        pf_bytes[1] = pfp->tab[1].size() * sizeof(float);
         pf_bytes[2] = pfp->byt.size() * sizeof(uint32_t);
         const size_t need = pf_bytes[0] + pf_bytes[1] + pf_bytes[2];
         pf_upload = !(ctx->pf_pack == pfp.get());
@@ -1287,8 +1287,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
         pa.amps = s->amps;
         pa.n_amps = n_amps;
         pa.base = (uint64_t)ctx->rank << nl;
-        pa.tab[0] = reinterpret_cast<const double2*>(ctx->d_pf);
-        pa.tab[1] = reinterpret_cast<const double2*>(ctx->d_pf + pf_bytes[0]);
+        pa.tab[0] = reinterpret_cast<const float2*>(ctx->d_pf);
+        pa.tab[1] = reinterpret_cast<const float2*>(ctx->d_pf + pf_bytes[0]);
         pa.byt = reinterpret_cast<const uint32_t*>(ctx->d_pf + pf_bytes[0] + pf_bytes[1]);
         pa.nbytes = pfp->nbytes;
         pa.zmask = pfp->zmask;

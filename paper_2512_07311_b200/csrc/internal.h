@@ -138,7 +138,7 @@ uint64_t job_seed(uint64_t base_seed, uint64_t job_id);
 // padded with one more local qubit) and the packed fp16 hi/lo matrices (host copy)
 // product-state prefix operands for one (plan, n_local): fp64 group tables + byte gather tables
 struct PrefixPack {
-    std::vector<double> tab[2];            // interleaved complex, 2^|group| entries each
+    std::vector<float> tab[2];             // interleaved complex (fp64 products rounded), 2^|group| each
     std::vector<uint32_t> byt;             // [2][nbytes][256]
     int nbytes = 0;
     uint64_t zmask = 0;                    // physical positions of the qubits outside the prefix

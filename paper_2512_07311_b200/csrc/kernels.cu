@@ -770,17 +770,25 @@ __global__ void __launch_bounds__(kThreads) k_product_init(const __grid_constant
     }
     __syncthreads();
     // A warp writes rows of 64 amplitudes (2 per lane, one 16-B store each) from a contiguous
-    // range of rows, four rows (256 amplitudes: byte 0 of X) at a time, so the table-index parts
-    // of X's bytes >= 1 are warp-uniform per group and all 16 table reads of a group are in
-    // flight together.
+    // range of rows, four rows (256 amplitudes: byte 0 of X) at a time: the table-index parts of
+    // X's bytes >= 1 are warp-uniform per group, the byte-0 parts are per-thread constants, and all
+    // 16 table reads of a group are in flight together.
     const int lane = threadIdx.x & 31;
     const uint64_t nrows = a.n_amps >> 6;
     const uint64_t nwarps = (uint64_t)gridDim.x * (kThreads / 32);
     const uint64_t w = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
     const uint64_t per = ((nrows + nwarps - 1) / nwarps + 3) & ~3ull;   // rows per warp, multiple of 4
     const uint64_t r0 = w * per, r1 = r0 + per < nrows ? r0 + per : nrows;
+    uint32_t iA[8], iB[8];   // k = 2 rr + e: row g + rr, amplitude 2 lane + e of the group
+    uint32_t zlo = 0;        // bit k: amplitude k has a |1> on a non-prefix qubit of byte 0
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int by = ((k >> 1) << 6) | (2 * lane) | (k & 1);
+        iA[k] = bt[0][0][by];
+        iB[k] = bt[1][0][by];
+        zlo |= (uint32_t)(((uint64_t)by & a.zmask) != 0) << k;
+    }
     float4* out = reinterpret_cast<float4*>(a.amps);
-    const double2 zero2 = make_double2(0.0, 0.0);
     for (uint64_t g = r0; g < r1; g += 4) {
         const uint64_t Xg = a.base + (g << 6);   // byte 0 of Xg is 0 (g is a multiple of 4)
         uint32_t ha = 0, hb = 0;
@@ -790,28 +798,29 @@ __global__ void __launch_bounds__(kThreads) k_product_init(const __grid_constant
             hb |= bt[1][c][by];
         }
         // a qubit outside the prefix set to |1> in bytes >= 1: the whole group is 0
-        const bool zhi = (Xg & a.zmask & ~255ull) != 0;
-        double2 A[8], B[8];
+        const uint32_t dead = (Xg & a.zmask & ~255ull) != 0 ? 0xffu : zlo;
+        const float2* TA = a.tab[0] + ha;   // ha | iA[k] == ha + iA[k]: disjoint bits
+        const float2* TB = a.tab[1] + hb;
+        float2 A[8], B[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) {   // k = 2 rr + e: row g + rr, amplitude 2 lane + e
-            const int by = ((k >> 1) << 6) | (2 * lane) | (k & 1);
-            const bool live = !zhi && g + (k >> 1) < r1 && ((uint64_t)by & a.zmask) == 0;
-            A[k] = live ? __ldg(&a.tab[0][ha | bt[0][0][by]]) : zero2;
-            B[k] = live ? __ldg(&a.tab[1][hb | bt[1][0][by]]) : zero2;
+        for (int k = 0; k < 8; k++) {
+            const bool live = !((dead >> k) & 1);
+            A[k] = live ? __ldg(TA + iA[k]) : make_float2(0.f, 0.f);
+            B[k] = live ? __ldg(TB + iB[k]) : make_float2(0.f, 0.f);
         }
+        float4* o = out + (((g - r0) << 5) | lane) + (r0 << 5);
+        const int nr = r1 - g < 4 ? (int)(r1 - g) : 4;
 #pragma unroll
         for (int rr = 0; rr < 4; rr++) {
-            if (g + rr >= r1) break;
+            if (rr >= nr) break;
             float r[4];
 #pragma unroll
-            for (int e = 0; e < 2; e++) {
-                const double2 x = A[2 * rr + e], y = B[2 * rr + e];
-                const double re = __dsub_rn(__dmul_rn(x.x, y.x), __dmul_rn(x.y, y.y));
-                const double im = __dadd_rn(__dmul_rn(x.x, y.y), __dmul_rn(x.y, y.x));
-                r[2 * e] = __double2float_rn(re);
-                r[2 * e + 1] = __double2float_rn(im);
+            for (int e = 0; e < 2; e++) {   // complex product, fixed fp32 operation order
+                const float2 x = A[2 * rr + e], y = B[2 * rr + e];
+                r[2 * e] = __fmaf_rn(x.x, y.x, -__fmul_rn(x.y, y.y));
+                r[2 * e + 1] = __fmaf_rn(x.x, y.y, __fmul_rn(x.y, y.x));
             }
-            __stcs(out + (((g + rr) << 5) | lane), make_float4(r[0], r[1], r[2], r[3]));
+            __stcs(o + 32 * rr, make_float4(r[0], r[1], r[2], r[3]));
         }
     }
 }

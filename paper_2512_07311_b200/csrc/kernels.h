@@ -132,8 +132,9 @@ cudaError_t last_nonzero(const double* inc, uint64_t n, unsigned long long* out,
 
 cudaError_t init_basis(float2* amps, uint64_t n_amps, int set_one, cudaStream_t st);
 
-// Product-state prefix (plan.cpp): amps[i] = tabA[ia] * tabB[ib] (fp64 complex, rounded once to
-// complex64) for the physical index X = base + i, where ia / ib gather X's bits that hold the
+// Product-state prefix (plan.cpp): amps[i] = tabA[ia] * tabB[ib] (the tables are the fp64 block
+// products rounded to complex64; the complex product is fp32 in a fixed operation order) for the
+// physical index X = base + i, where ia / ib gather X's bits that hold the
 // two groups' qubits (OR of per-byte tables byt[G][c][X byte c]); 0 if X has a bit set at a
 // position of zmask (qubits still |0>).  Write-only: 8 B per amplitude.
 constexpr int kPrefixBytes = 8;   // X up to 64 bits
@@ -141,7 +142,7 @@ struct PrefixArgs {
     float2* amps;
     uint64_t n_amps;               // even
     uint64_t base;                 // physical index of amps[0] (rank << n_local)
-    const double2* tab[2];
+    const float2* tab[2];          // the two group tables (fp64 products rounded to fp32)
     const uint32_t* byt;           // [2][nbytes][256]
     int nbytes;
     uint64_t zmask;
