@@ -44,17 +44,17 @@ METRIC = "fused gate-pass HBM GB/s (whole RCS step: state build + shots + XEB)"
 PLAN_PREFIX = {'c1': {3: 4, 4: 2, 5: 2, 6: 2},
                'c2': {3: 8, 4: 6, 5: 5, 6: 4},
                'c3': {3: 11, 4: 8, 5: 7, 6: 6},
-               'c4': {3: 3, 4: 9, 5: 6, 6: 6},
+               'c4': {3: 12, 4: 9, 5: 6, 6: 6},
                'c5': {3: 12, 4: 8, 5: 6, 6: 6},
-               'w33': {3: 3, 4: 9, 5: 7, 6: 6},
+               'w33': {3: 11, 4: 9, 5: 7, 6: 6},
                'w35': {3: 6, 4: 8, 5: 5, 6: 6}}
 PLAN_PASSES = {'c1': {3: 32, 4: 19, 5: 14, 6: 8},
                'c2': {3: 98, 4: 45, 5: 40, 6: 27},
                'c3': {3: 103, 4: 56, 5: 44, 6: 33},
-               'c4': {3: 140, 4: 76, 5: 57, 6: 36},
+               'c4': {3: 149, 4: 76, 5: 57, 6: 36},
                'c5': {3: 157, 4: 82, 5: 63, 6: 39},
-               'w33': {3: 114, 4: 74, 5: 53, 6: 39},
-               'w35': {3: 142, 4: 83, 5: 54, 6: 46}}
+               'w33': {3: 122, 4: 74, 5: 53, 6: 39},
+               'w35': {3: 142, 4: 83, 5: 52, 6: 46}}
 
 
 def parse_args():

@@ -489,14 +489,14 @@ void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb
 // wins, ties to the lower index.
 static void fuse_strategy_memo(const Circuit& c, int k, int which, std::vector<Block>& out,
                                std::shared_ptr<RolloutMemo> memo) {
-    // {prefix-first, extension search depth, prefix-phase depth (-1: the same)}
-    static const int S[kFuseStrategies][3] = {{0, 0, -1}, {0, kFuseDeepDepth, -1}, {1, 0, -1}, {1, 1, -1},
-                                              {1, kFuseDeepDepth, 1}};
+    // {prefix-first, extension search depth, prefix-phase depth (-1: the same), seeds}
+    static const int S[kFuseStrategies][4] = {{0, 2, -1, 4}, {1, 0, -1, kFuseSeeds},
+                                              {1, 1, -1, kFuseSeeds}, {1, kFuseDeepDepth, 1, kFuseSeeds}};
     Fuser F(c, k);
     F.prefix_first = S[which][0] != 0;
     F.prefix_depth = S[which][2];
     F.memo = std::move(memo);
-    F.seeds = kFuseSeeds;
+    F.seeds = S[which][3];
     F.lookahead = kFuseLookahead;
     F.grow_lookahead = S[which][1] > 0;
     F.grow_depth = S[which][1];
@@ -515,13 +515,25 @@ void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out) 
 int fuse_best(const Circuit& c, int k, std::vector<Block>* cand) {
     std::vector<std::thread> th;
     auto memo = std::make_shared<RolloutMemo>(), pmemo = std::make_shared<RolloutMemo>();
+#ifdef RCS_PLAN_DEBUG
+    for (int w = 0; w < kFuseStrategies; w++) {
+        auto t0 = std::chrono::steady_clock::now();
+        fuse_strategy_memo(c, k, w, cand[w], w >= 1 ? pmemo : memo);
+        fprintf(stderr, "strategy %d time %.3f s\n", w, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+#else
     for (int w = 1; w < kFuseStrategies; w++)
-        th.emplace_back([&, w] { fuse_strategy_memo(c, k, w, cand[w], w >= 2 ? pmemo : memo); });
+        th.emplace_back([&, w] { fuse_strategy_memo(c, k, w, cand[w], w >= 1 ? pmemo : memo); });
     fuse_strategy_memo(c, k, 0, cand[0], memo);
+#endif
     for (auto& t : th) t.join();
     int win = 0;
     for (int w = 1; w < kFuseStrategies; w++)
         if (fuse_cost(cand[w]) < fuse_cost(cand[win])) win = w;
+#ifdef RCS_PLAN_DEBUG
+    for (int w = 0; w < kFuseStrategies; w++)
+        fprintf(stderr, "strategy %d: %zu blocks, %lld passes%s\n", w, cand[w].size(), (long long)(fuse_cost(cand[w]) >> 20), w == win ? " *" : "");
+#endif
     return win;
 }
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # multi-GPU check (gpurun --gpus 4): parity tests; C4 N = 1, 2 and 4; C5 N = 4 (defaults)
 cd "$(dirname "$0")/.."
-OUT=gpurun_out/mgpu; mkdir -p $OUT
+OUT=gpurun_out/${MOUT:-mgpu}; mkdir -p $OUT
 python -m paper_2512_07311_b200.build > $OUT/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
 timeout 2400 python -m pytest tests/test_multigpu.py -q -p no:cacheprovider > $OUT/mgpu_tests.log 2>&1; echo "mgpu tests rc=$?"
 grep -E "^(FAILED|ERROR)|passed|failed" $OUT/mgpu_tests.log | tail -20
