@@ -690,7 +690,7 @@ rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs
         std::vector<int> movable;
         for (int q = pinned; q < n; q++) movable.push_back(q);
         std::stable_sort(movable.begin(), movable.end(), [&](int a, int b2) {
-            const int fa = next_use(a, 0), fb = next_use(b2, 0);
+            const int fa = next_use(a, P.prefix), fb = next_use(b2, P.prefix);   // prefix blocks need no remap
             if (fa != fb) return fa > fb;
             return a > b2;
         });

@@ -647,6 +647,8 @@ struct TcTArgs {
     int r;                   // cube ranks 0..r-1 are positions 0..r-1 (runs of 2^r amplitudes)
     int nrun_pos;            // 13 - r: cube positions above the runs ...
     int run_pos[6];          // ... (the TMA run index is deposited into them)
+    int lane_t[4];           // PT = kPermMulti: lane bit b XORs t bit lane_t[b] into the reads (-1: none)
+    int pmask;               // ... the t bits so permuted
     int phi_t;               // lanes with column bit 3 set read t XOR (1 << phi_t) (bank-conflict
                              // free); -1 if no target sits in cube ranks 0..3
     int nins;                // 13 cube positions + chunk bits, ascending
@@ -712,7 +714,20 @@ __device__ __forceinline__ void unpermute16(uint32_t (&w)[16], bool f) {
     }
 }
 
-// PT: the t bit the lanes with column bit 3 set flip (-1: none, no permutation)
+// every t bit of pmask whose lane flag (phi) is set: undo the XOR (stages commute)
+__device__ __forceinline__ void unpermute_mask(uint32_t (&w)[16], int pmask, uint32_t phi) {
+    if (pmask & 1) unpermute16<0>(w, phi & 1);
+    if (pmask & 2) unpermute16<1>(w, (phi >> 1) & 1);
+    if (pmask & 4) unpermute16<2>(w, (phi >> 2) & 1);
+    if (pmask & 8) unpermute16<3>(w, (phi >> 3) & 1);
+    if (pmask & 16) unpermute16<4>(w, (phi >> 4) & 1);
+}
+
+// PT: the t bit the lanes with column bit 3 set flip (-1: none, no permutation); kPermMulti:
+// two to four targets at cube ranks 0..3 -- lane bits 4-a..3 (the column bits displaced above
+// rank 3) each flip one of them (TcTArgs::lane_t), so the 16 reads of a half-warp hit 16 bank
+// pairs; the packed words are put back by one select / byte-permute stage per flipped t bit
+constexpr int kPermMulti = 8;
 template <int PT>
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constant__ TcTArgs p) {
     constexpr bool PERM = PT >= 0;
@@ -854,7 +869,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
         const int q = warp & 3, th = warp >> 2;
         const int j = 32 * q + lane;
         const bool pf = PERM && ((lane >> 3) & 1);   // this lane reads t ^ (1 << PT)
-        const uint32_t phi = pf ? 1u << (PERM ? PT : 0) : 0u;
+        uint32_t phi = pf ? 1u << (PERM ? PT & 7 : 0) : 0u;
+        if (PT == kPermMulti) {
+            phi = 0;
+            for (int b = 0; b < 4; b++)
+                if (p.lane_t[b] >= 0 && ((lane >> b) & 1)) phi |= 1u << p.lane_t[b];
+        }
         // cube index of (t = 32 th + (u ^ phi), j) = base ^ cube_t(u) with cube_t linear in u
         uint32_t base = 0;
         for (int k = 0; k < 7; k++)
@@ -920,9 +940,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                     const float x0 = (c ? v[2 * u].y : v[2 * u].x) * sc, x1 = (c ? v[2 * u + 1].y : v[2 * u + 1].x) * sc;
                     split_exact_h2(x0, x1, hw[u], lw[u]);
                 }
-                if (PERM) {
-                    unpermute16<PT>(hw, pf);
-                    unpermute16<PT>(lw, pf);
+                if (PT == kPermMulti) {
+                    unpermute_mask(hw, p.pmask, phi);
+                    unpermute_mask(lw, p.pmask, phi);
+                } else if (PERM) {
+                    unpermute16<PT & 7>(hw, pf);
+                    unpermute16<PT & 7>(lw, pf);
                 }
                 TMEM_ST16(ta + 32 * c, hw);        // hi: re words [16 th, +16), im words [32 + 16 th, +16)
                 TMEM_ST16(ta + 64 + 32 * c, lw);   // lo
@@ -1259,13 +1282,24 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
     // displaced to rank 4 and the lanes with it set read t ^ (that target's bit); t bit 5 (the
     // converter half) must not be it.  More low targets: K9 (tc_uses_k12).
     p.phi_t = -1;
+    int nlow = 0, lowt[6];
     for (int i = 0; i < 6; i++)
         if (p.tcube[i] < 4) {
-            if (p.phi_t >= 0 || i >= 5) return cudaErrorInvalidValue;
-            p.phi_t = i;
+            if (i >= 5) return cudaErrorInvalidValue;
+            lowt[nlow++] = i;
         }
+    if (nlow == 1) p.phi_t = lowt[0];
+    if (nlow >= 2) {   // lane bits 4 - nlow .. 3 (column bits at ranks >= 4) -> the low t bits
+        p.phi_t = kPermMulti;
+        p.pmask = 0;
+        for (int b = 0; b < 4; b++) p.lane_t[b] = -1;
+        for (int m = 0; m < nlow; m++) {
+            p.lane_t[4 - nlow + m] = lowt[m];
+            p.pmask |= 1 << lowt[m];
+        }
+    }
     const bool perm = p.phi_t >= 0;
-    if (perm && p.jcube[3] < 4) return cudaErrorInvalidValue;
+    if (perm && p.jcube[4 - nlow] < 4) return cudaErrorInvalidValue;
     uint64_t insmask = cube, fixmask = 0;
     for (int i = 0; i < nfix; i++) {
         if (fix[i] < 0 || fix[i] >= nl || ((insmask >> fix[i]) & 1)) return cudaErrorInvalidValue;
@@ -1296,6 +1330,7 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
         case 2: kern = k_pass_tct<2>; break;
         case 3: kern = k_pass_tct<3>; break;
         case 4: kern = k_pass_tct<4>; break;
+        case kPermMulti: kern = k_pass_tct<kPermMulti>; break;
         default: return cudaErrorInvalidValue;
     }
     (void)perm;
@@ -1308,10 +1343,13 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
 }
 
 bool tc_uses_k12(int nl, const int* pos) {
-    if (nl < 13) return false;
+    // K12 for at most 2 targets in positions 0..3 (kPermMulti for 2) unless the converter-half
+    // bit (matrix bit 5) sits there (K12 cannot flip it).  Measured per pass on one box
+    // (profiles/r02/k12multi): 2 low targets 15.1-17.0 ms vs K9 17.3-17.6 (C3 size); 3-4 low
+    // targets 31-44 ms vs K9 17.0-17.2 -- the epilogue's stores then scatter over 32 sectors
     int low = 0;
     for (int i = 0; i < 6; i++) low += pos[i] < 4;
-    return low <= 1;
+    return nl >= 13 && pos[5] >= 4 && low <= 2;
 }
 
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,

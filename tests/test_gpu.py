@@ -109,6 +109,26 @@ def test_transposed_pass_matches_k9(rcs, ctx, n):
         check_amps(pa, oracle.build_state(text))
 
 
+@pytest.mark.parametrize("grid", [(4, 5, 12, "ABCDCDAB"), (3, 7, 12, "EFGH"), (4, 6, 15, "ABCDCDAB")])
+def test_multi_low_target_blocks_on_k12(rcs, ctx, grid):
+    """Blocks with 2-4 targets in positions 0..3 (row 0 of the grid) run on K12 with a lane
+    permutation of up to four t bits (round 2; K9 before): equal to the K9 build up to the cross
+    terms' rounding order and to the oracle within the BASELINE tolerance."""
+    rows, cols, cyc, pat = grid
+    text = emit_qasm(generate(rows, cols, cyc, pat, seed=1))
+    c = rcs.Circuit.from_qasm(text)
+    plan = rcs.Plan(c, 6, 0)
+    multi = [it for it in plan.items()[plan.prefix:]
+             if it["type"] == "pass" and sum(x < 4 for x in it["pos"]) >= 2]
+    assert len(multi) >= 3   # >= 2 low targets: K12 (kPermMulti) for 2, K9 for 3-4
+    a = rcs.State.build(ctx, c, fuse_k=6)
+    pa = a.copy_out().astype(np.complex128)
+    b = rcs.State.build(ctx, c, fuse_k=6, tc_kernel="k9")
+    pb = b.copy_out().astype(np.complex128)
+    assert np.abs(pa - pb).max() <= 1e-8 and abs(a.norm - b.norm) <= 1e-7
+    check_amps(pa, oracle.build_state(text))
+
+
 @pytest.mark.parametrize("case", ["c1", "c3_24", "w33_24", "grid20_k4"])
 def test_product_prefix_matches_passes(rcs, ctx, case):
     """The leading fused blocks on disjoint qubits act on |0...0>: the product-state kernel writes
