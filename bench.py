@@ -73,6 +73,7 @@ def parse_args():
     ap.add_argument("--overlap-passes", type=int, default=0, help="passes after a remap pipelined behind it (0: default)")
     ap.add_argument("--dynamic-tiles", action="store_true", help="K12 dynamic tile scheduler (default: static)")
     ap.add_argument("--overlap-sms", type=int, default=0, help="SMs left to the pipelined swaps (0: default)")
+    ap.add_argument("--overlap-chunks", type=int, default=0, help="pipelined remaps: 2^k chunks (0: default 2)")
     ap.add_argument("--no-prefix", action="store_true", help="run the product-state prefix blocks as passes")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     return ap.parse_args()
@@ -259,7 +260,7 @@ def run_ours(args):
     amps = torch.empty(1 << (n - g), dtype=torch.complex64, device=dev)
     keep = not args.canonical   # skip the final layout restore: samples/XEB are layout-independent
     bopts = {"overlap": not args.no_overlap, "overlap_passes": args.overlap_passes,
-             "overlap_sms": args.overlap_sms, "tc_schedule": "dynamic" if args.dynamic_tiles else "static",
+             "overlap_sms": args.overlap_sms, "overlap_chunks": args.overlap_chunks, "tc_schedule": "dynamic" if args.dynamic_tiles else "static",
              "product_prefix": not args.no_prefix}
     st0 = rcs.State.build(ctx, circuit, fuse_k=args.fuse_k, amps=amps, keep_layout=keep, **bopts)   # sizes scratch
     scratch = st0.scratch
