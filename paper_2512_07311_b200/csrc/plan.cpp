@@ -531,8 +531,16 @@ int fuse_best(const Circuit& c, int k, std::vector<Block>* cand) {
     for (int w = 1; w < kFuseStrategies; w++)
         if (fuse_cost(cand[w]) < fuse_cost(cand[win])) win = w;
 #ifdef RCS_PLAN_DEBUG
-    for (int w = 0; w < kFuseStrategies; w++)
-        fprintf(stderr, "strategy %d: %zu blocks, %lld passes%s\n", w, cand[w].size(), (long long)(fuse_cost(cand[w]) >> 20), w == win ? " *" : "");
+    for (int w = 0; w < kFuseStrategies; w++) {
+        int k9 = 0;
+        for (const Block& B : cand[w]) {
+            int low = 0;
+            for (int q : B.qubits) low += q < 4;
+            k9 += low >= 3;
+        }
+        fprintf(stderr, "strategy %d: %zu blocks, %lld passes, %d blocks with >= 3 of qubits 0..3%s\n", w, cand[w].size(),
+                (long long)(fuse_cost(cand[w]) >> 20), k9, w == win ? " *" : "");
+    }
 #endif
     return win;
 }

@@ -109,24 +109,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(su32(b)) : "memory");
 }
-#ifndef RCS_MBAR_HINT
-#define RCS_MBAR_HINT 0x2000
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     uint32_t done = 0;
-#if RCS_MBAR_HINT == 0   // build-time A/B: plain try_wait (no suspend-time hint)
-    do {
-        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(done)
-                     : "r"(su32(b)), "r"(parity)
-                     : "memory");
-    } while (!done);
-    return;
-#endif
     do {
         asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}"
                      : "=r"(done)
-                     : "r"(su32(b)), "r"(parity), "r"(RCS_MBAR_HINT)   // suspend-time hint (ns): sleep, don't spin
+                     : "r"(su32(b)), "r"(parity), "r"(0x2000)   // suspend-time hint (ns): sleep, don't spin
                      : "memory");
     } while (!done);
 }
@@ -675,9 +663,6 @@ struct TcTArgs {
 #ifndef RCS_K12_EPIPIPE
 #define RCS_K12_EPIPIPE 1
 #endif
-#ifndef RCS_K12_DIAG
-#define RCS_K12_DIAG 0
-#endif
 constexpr uint32_t kTRaw = 8192 * 8;
 constexpr int kTRing = 8;                             // tile bases in flight (producer -> all roles)
 constexpr uint64_t kTileEnd = ~0ull;                  // ring sentinel: no more tiles                  // one tile: 64 KB
@@ -911,13 +896,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             mbar_arrive(&rempty[slot]);
             // column max over the two threads of column j (warps q and q + 4), as K9
             const int cb = (int)(it % 3);
-#if RCS_K12_DIAG == 5   // diagnostic: per-thread max, no cross-warp agreement (wrong results)
-            const int E = col_exponent(__float_as_int(mx));
-#else
             atomicMax(&cmax[cb * 128 + j], __float_as_int(mx));
             asm volatile("bar.sync 2, 256;" ::: "memory");
             const int E = col_exponent(cmax[cb * 128 + j]);
-#endif
             if (th == 0) cmax[((it + 2) % 3) * 128 + j] = 0;
             const float sc = pow2f(E);
             mbar_wait(&aempty[b], ((it >> 1) & 1) ^ 1);
@@ -984,7 +965,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                     const uint32_t xh = tmem + 128 * b, xl = xh + 64;   // state hi / lo (A)
                     const uint64_t bh = bh0 + 1024 * h, bl = bl0 + 1024 * h;   // + 64 n rows (16 KB)
                     // cross terms (x_hi u_lo, x_lo u_hi) -> acc 0; main x_hi u_hi (exact) -> acc 1
-#if RCS_K12_DIAG != 2   // diagnostic builds only (wrong results): 2 = no cross-term MMAs
                     MMA_F16(dc, xh, bl, idesc, 0);
                     MMA_F16(dc, xl, bh, idesc, 1);
 #pragma unroll
@@ -992,7 +972,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                         MMA_F16(dc, xh + ks * 8, bl + ks * 16, idesc, 1);
                         MMA_F16(dc, xl + ks * 8, bh + ks * 16, idesc, 1);
                     }
-#endif
                     MMA_F16(dm, xh, bh, idesc, 0);
 #pragma unroll
                     for (int ks = 1; ks < 8; ks++) MMA_F16(dm, xh + ks * 8, bh + ks * 16, idesc, 1);
@@ -1034,13 +1013,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             // (the epilogue's longest part: 64 B/cycle); two register sets alternate.
             uint32_t a0[32], a1[32], b0[32], b1[32];
             TMEM_LD32(ta, a0);
-#if RCS_K12_DIAG == 1   // diagnostic: one accumulator read (wrong results)
-            (void)0;
-#define TMEM_LD_DIAG(addr, R) _Pragma("unroll") for (int z = 0; z < 32; z++) R[z] = 0u
-#else
-#define TMEM_LD_DIAG(addr, R) TMEM_LD32M(addr, R)
-#endif
-            TMEM_LD_DIAG(ta + 128, a1);
+            TMEM_LD32M(ta + 128, a1);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             REG_FENCE32(a0);
             REG_FENCE32(a1);
@@ -1066,12 +1039,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                         asm volatile("tcgen05.fence::after_thread_sync;");
                     }
                     TMEM_LD32M(ta + 32 * (s4 + 1), y0);
-                    TMEM_LD_DIAG(ta + 128 + 32 * (s4 + 1), y1);
+                    TMEM_LD32M(ta + 128 + 32 * (s4 + 1), y1);
                 }
 #pragma unroll
                 for (int c = 0; c < 32; c += 2)
-                    if (RCS_K12_DIAG != 3 || x0[c] == 0x7fc00001u)   // diagnostic 3: no stores
-                        __stcs(dst + offt[16 * s4 + c / 2], make_float2(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1])));
+                    __stcs(dst + offt[16 * s4 + c / 2], make_float2(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1])));
                 if (s4 < 3) {
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     REG_FENCE32(y0);
