@@ -59,10 +59,29 @@ struct RolloutMemo {
     std::unordered_map<std::vector<int>, int, H> left;
 };
 
+FuseTables make_tables(const Circuit& c) {
+    FuseTables t;
+    t.per_q.assign(c.n, {});
+    for (int i = 0; i < (int)c.gates.size(); i++) {
+        const Gate& g = c.gates[i];
+        t.per_q[g.q0].push_back(i);
+        uint64_t m = 1ull << g.q0;
+        if (g.q1 >= 0) {
+            t.per_q[g.q1].push_back(i);
+            m |= 1ull << g.q1;
+        }
+        t.gmask.push_back(m);
+        t.gw.push_back(g.q1 >= 0 ? 2 : 1);
+    }
+    return t;
+}
+
+// Copied for every rollout and lookahead candidate (plain pointers to the shared read-only
+// tables and memo: no reference counting on the hot path).
 struct Fuser {
     const Circuit& C;
     int k, n;
-    std::shared_ptr<const FuseTables> T;
+    const FuseTables* T;
     std::vector<int> head;                 // first unassigned position in per_q[q]
     std::vector<char> assigned;
     size_t first_unassigned = 0;
@@ -81,23 +100,9 @@ struct Fuser {
     uint64_t allowed = ~0ull;     // extensions stay inside this set (prefix phase: ~touched)
     bool last_prefix = false;     // the last next_set() committed a prefix-phase block
     int prefix_depth = -1;        // >= 0: extension search depth of the prefix phase (else grow_depth)
-    std::shared_ptr<RolloutMemo> memo;
+    RolloutMemo* memo = nullptr;
 
-    Fuser(const Circuit& c, int k_) : C(c), k(k_), n(c.n) {
-        auto t = std::make_shared<FuseTables>();
-        t->per_q.assign(c.n, {});
-        for (int i = 0; i < (int)c.gates.size(); i++) {
-            const Gate& g = c.gates[i];
-            t->per_q[g.q0].push_back(i);
-            uint64_t m = 1ull << g.q0;
-            if (g.q1 >= 0) {
-                t->per_q[g.q1].push_back(i);
-                m |= 1ull << g.q1;
-            }
-            t->gmask.push_back(m);
-            t->gw.push_back(g.q1 >= 0 ? 2 : 1);
-        }
-        T = t;
+    Fuser(const Circuit& c, int k_, const FuseTables* t) : C(c), k(k_), n(c.n), T(t) {
         head.assign(c.n, 0);
         assigned.assign(c.gates.size(), 0);
     }
@@ -114,6 +119,33 @@ struct Fuser {
         int h[64];
         for (uint64_t m = S; m; m &= m - 1) h[__builtin_ctzll(m)] = head[__builtin_ctzll(m)];
         int w = 0;
+        if (!got) {   // weight / heads only: the absorbed set is unique (a least fixed point), so a
+            uint64_t pend = S;   // worklist of qubits whose head moved finds it in any order
+            while (pend) {
+                const int q = __builtin_ctzll(pend);
+                const int g = next_gate(q, h[q]);
+                if (g < 0 || (T->gmask[g] & ~S)) {
+                    pend &= pend - 1;
+                    continue;
+                }
+                const uint64_t other = T->gmask[g] & ~(1ull << q);
+                if (other) {
+                    const int qq = __builtin_ctzll(other);
+                    if (next_gate(qq, h[qq]) != g) {
+                        pend &= pend - 1;
+                        continue;
+                    }
+                    h[qq]++;
+                    pend |= other;
+                }
+                h[q]++;
+                w += T->gw[g];
+            }
+            if (hout)
+                for (uint64_t m = S; m; m &= m - 1) hout[__builtin_ctzll(m)] = h[__builtin_ctzll(m)];
+            return w;
+        }
+        // with the gate list: absorption in the order of the scan below (the block's gate order)
         bool progress = true;
         while (progress) {
             progress = false;
@@ -492,10 +524,11 @@ static void fuse_strategy_memo(const Circuit& c, int k, int which, std::vector<B
     // {prefix-first, extension search depth, prefix-phase depth (-1: the same), seeds}
     static const int S[kFuseStrategies][4] = {{0, 2, -1, 4}, {1, 0, -1, kFuseSeeds},
                                               {1, 1, -1, kFuseSeeds}, {1, kFuseDeepDepth, 1, kFuseSeeds}};
-    Fuser F(c, k);
+    const FuseTables tabs = make_tables(c);
+    Fuser F(c, k, &tabs);
     F.prefix_first = S[which][0] != 0;
     F.prefix_depth = S[which][2];
-    F.memo = std::move(memo);
+    F.memo = memo.get();   // memo outlives F (held by this frame)
     F.seeds = S[which][3];
     F.lookahead = kFuseLookahead;
     F.grow_lookahead = S[which][1] > 0;
