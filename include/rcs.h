@@ -108,9 +108,11 @@ typedef struct {
     int overlap_chunks;      /* log2 chunks, 1..4 (0 -> 2)                                         */
     int overlap_sms;         /* SMs left to the swaps while passes run (0 -> 32 at world 2, 16 at
                                 world >= 4 and in loopback)                                        */
-    int tc_kernel;           /* 0: the transposed kernel K12 (any layout) when n_local >= 13 and at
-                                most one target sits in positions 0..3, K9 otherwise (a function of
-                                the block: P-invariant); 1: K9 only (tests, comparisons)           */
+    int tc_kernel;           /* 0: the transposed kernel K12 when n_local >= 13 and at most two
+                                targets sit in positions 0..3 (not matrix bit 5), or the block is
+                                positions 0..5 in order (K12's row variant, unchunked passes); K9
+                                otherwise -- a function of the block: P-invariant; 1: K9 only
+                                (tests, comparisons); 2: as 0 without the row variant            */
     int overlap_passes;      /* pipelined remaps: how many tensor-core passes after the remap run
                                 chunk by chunk behind its swaps (0 -> 3; 1 = the next pass only)  */
     int product_prefix;      /* 0: the leading fused blocks on pairwise disjoint qubits (they act on

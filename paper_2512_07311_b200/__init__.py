@@ -220,14 +220,15 @@ class State:
               overlap_sms: int = 0, tc_kernel: str = "auto", overlap_passes: int = 0,
               tc_schedule: str = "static", product_prefix: bool = True, tc_tma: str = "auto") -> "State":
         """rcs_state_build.  remap_mode: "auto" | "nccl" | "loopback" (world 1 + virtual_global: remaps
-        through the NVLink peer-swap kernel between regions of this GPU); tc_kernel: "auto" | "k9";
+        through the NVLink peer-swap kernel between regions of this GPU); tc_kernel: "auto" | "k9" |
+        "norow" (auto, but blocks on positions 0..5 on K9 instead of K12's row variant);
         tc_tma: "auto" (short K12 runs through tensor-map TMA) | "bulk" (one bulk copy per run)."""
         import torch
         n = circuit.n_qubits
         g = ctx.world.bit_length() - 1
         opts = rcs_build_opts(fuse_k, block_bits, virtual_global, 1 if timing else 0, staging_bytes,
                               1 if keep_layout else 0, REMAP_MODES[remap_mode], 0 if overlap else -1,
-                              overlap_chunks, overlap_sms, {"auto": 0, "k9": 1}[tc_kernel], overlap_passes,
+                              overlap_chunks, overlap_sms, {"auto": 0, "k9": 1, "norow": 2}[tc_kernel], overlap_passes,
                               0 if product_prefix else -1, {"static": 0, "dynamic": 1}[tc_schedule],
                               {"auto": 0, "bulk": -1}[tc_tma])
         sb = C.c_uint64()

@@ -1068,7 +1068,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     }
     if (o.remap_mode < RCS_REMAP_AUTO || o.remap_mode > RCS_REMAP_LOOPBACK ||
         (o.remap_mode == RCS_REMAP_LOOPBACK && (ctx->world != 1 || o.virtual_global < 1 || o.virtual_global > 3)) ||
-        o.overlap_chunks < 0 || o.overlap_chunks > 4 || o.overlap_sms < 0 || o.tc_kernel < 0 || o.tc_kernel > 1 ||
+        o.overlap_chunks < 0 || o.overlap_chunks > 4 || o.overlap_sms < 0 || o.tc_kernel < 0 || o.tc_kernel > 2 ||
         o.overlap_passes < 0 || o.overlap_passes > 8 || o.tc_schedule < 0 || o.tc_schedule > 1 || o.tc_tma < -1 || o.tc_tma > 0 ||
         o.product_prefix < -1 || o.product_prefix > 0 ||
         o.virtual_global < 0) {
@@ -1258,7 +1258,8 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     }
     if (n_tc > 0 && !ctx->d_tiles && o.tc_schedule == 1) BUILD_TRY(cudaMalloc(&ctx->d_tiles, 64));
     s->tiles = o.tc_schedule == 1 ? ctx->d_tiles : nullptr;
-    s->tc_flags = (o.tc_kernel == 1 ? dev::kTcForceK9 : 0) | (o.tc_tma == -1 ? dev::kTcBulkRuns : 0);
+    s->tc_flags = (o.tc_kernel == 1 ? dev::kTcForceK9 : 0) | (o.tc_kernel == 2 ? dev::kTcNoRow : 0) |
+                  (o.tc_tma == -1 ? dev::kTcBulkRuns : 0);
     BUILD_TRY(cudaEventRecord(eb0, stream));
     cudaEvent_t epf0 = nullptr;
     if (tc_upload) {

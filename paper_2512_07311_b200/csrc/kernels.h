@@ -28,7 +28,7 @@ bool tc_uses_k12(int n_local_bits, const int* pos);
 // stream-ordered) instead of the static blockIdx.x + k gridDim.x assignment.
 // tc_flags: kTcForceK9 (every block on K9), kTcBulkRuns (K12 loads its runs with plain bulk copies
 // even when they are short; default: a 5-D tensor-map TMA moves many short runs per request).
-constexpr int kTcForceK9 = 1, kTcBulkRuns = 2;
+constexpr int kTcForceK9 = 1, kTcBulkRuns = 2, kTcNoRow = 4;   // kTcNoRow: [0..5] blocks on K9
 cudaError_t gate_pass_tc(float2* amps, int n_local_bits, const int* pos, const uint32_t* d_a, int num_sms,
                          cudaStream_t st, const int* fix = nullptr, int nfix = 0, uint64_t fixval = 0,
                          int tc_flags = 0, unsigned* tile_counter = nullptr);

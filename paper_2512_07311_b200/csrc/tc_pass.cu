@@ -653,15 +653,13 @@ struct TcTArgs {
     uint32_t req_bytes;      // bytes per request (8192 * 8 / nreq)
     int treq[8];             // per request: dim-4 coordinate offset (units of 2^r amplitudes)
     alignas(64) CUtensorMap tmap;
+    alignas(64) CUtensorMap tmap_st;   // PT = kRow: the epilogue's TMA store map
 };
 
 // build-time variants for A/B measurements (RCS_NVCC_FLAGS=-D...): D split into two N = 64 halves,
 // epilogue loads of the next chunk issued before the current chunk's stores
 #ifndef RCS_K12_NSPLIT
 #define RCS_K12_NSPLIT 1
-#endif
-#ifndef RCS_K12_EPIPIPE
-#define RCS_K12_EPIPIPE 1
 #endif
 constexpr uint32_t kTRaw = 8192 * 8;
 constexpr int kTRing = 8;                             // tile bases in flight (producer -> all roles)
@@ -671,6 +669,7 @@ constexpr uint32_t kTCtl = 3584;
 static_assert((12 + kExpSlots) * 8 + 64 * 8 + 64 * 8 + kTRing * 8 + 3 * 128 * 4 + 64 * 4 + kExpSlots * 128 + 4 <= kTCtl,
               "K12 control block");
 constexpr uint32_t kTSmem = 2 * kTRaw + kTMat + kTCtl;
+constexpr uint32_t kTRowStage = 2 * 8 * 128 * 8;      // kRow: 2 staging buffers of 8 t x 128 j (float2)
 
 // 32-bit conditional swap (select) of a and b
 __device__ __forceinline__ void cswap(bool f, uint32_t& a, uint32_t& b) {
@@ -713,13 +712,21 @@ __device__ __forceinline__ void unpermute_mask(uint32_t (&w)[16], int pmask, uin
 // rank 3) each flip one of them (TcTArgs::lane_t), so the 16 reads of a half-warp hit 16 bank
 // pairs; the packed words are put back by one select / byte-permute stage per flipped t bit
 constexpr int kPermMulti = 8;
+// kRow: the block's targets are positions 0..5 in matrix-bit order (a row of 64 contiguous
+// amplitudes per column j).  K12's column-per-thread reads and stores would hit one bank / 32
+// sectors per instruction there, so this variant moves the tile with tensor-map TMA both ways:
+// loaded into shared memory with the 128-B swizzle (rows j, 16-B chunks XOR j & 7: a half-warp's
+// 16-B reads of one t-pair hit distinct banks) and stored from a 64-B-swizzled staging buffer
+// (8 t x 128 j per TMA store, double buffered), no register permutation either way.
+constexpr int kRow = 9;
+
 template <int PT>
 __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constant__ TcTArgs p) {
-    constexpr bool PERM = PT >= 0;
+    constexpr bool PERM = PT >= 0 && PT != kRow;   // kRow reads its rows conflict-free without it
     extern __shared__ __align__(1024) uint8_t smem[];
     float2* raw = reinterpret_cast<float2*>(smem);                       // [2][8192] by cube index
     uint8_t* mat = smem + 2 * kTRaw;                                      // B hi | B lo (K-major)
-    uint8_t* ctl = mat + kTMat;
+    uint8_t* ctl = mat + kTMat + (PT == kRow ? kTRowStage : 0);   // kRow: staging after the matrix
     uint64_t* rfull = reinterpret_cast<uint64_t*>(ctl);   // [2]
     uint64_t* rempty = rfull + 2;                         // [2]
     uint64_t* afull = rempty + 2;                         // [2]
@@ -824,7 +831,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             __syncwarp();
             const float2* src = p.amps + (bp | p.fixval);
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
-            if (p.nreq) {
+            if (PT == kRow) {   // one 4-D tensor load of the whole tile (tile base = tile << 13)
+                if (lane == 0)
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                        "%3, %4, %5}], [%6];" ::"r"(dst),
+                        "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(0), "r"(0), "r"(0), "r"((int)(bp >> 13)),
+                        "r"(su32(&rfull[slot]))
+                        : "memory");
+            } else if (p.nreq) {
                 if (lane < p.nreq) {
                     const int cb = (int)((bp | p.fixval) >> p.r) + p.treq[lane];
                     asm volatile(
@@ -882,12 +897,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             const float2* rb = raw + (size_t)slot * 8192;
             float2 v[32];   // v[u] = x(32 th + (u ^ phi), j)
             float mx = 0.f;
+            if (PT == kRow) {   // row j = 128 (t >> 4) + j of 128 B, 16-B chunk (t & 15) / 2 ^ (j & 7)
+                const uint8_t* sb = reinterpret_cast<const uint8_t*>(rb);
+#pragma unroll
+                for (int u2 = 0; u2 < 16; u2++) {
+                    const int t = 32 * th + 2 * u2;
+                    const uint32_t rho = (uint32_t)j + 128u * (uint32_t)(t >> 4);
+                    const float4 w = *reinterpret_cast<const float4*>(sb + rho * 128 + (((uint32_t)((t & 15) >> 1) ^ (rho & 7)) << 4));
+                    v[2 * u2] = make_float2(w.x, w.y);
+                    v[2 * u2 + 1] = make_float2(w.z, w.w);
+                    mx = absmax2(absmax2(mx, v[2 * u2]), v[2 * u2 + 1]);
+                }
+            }
             uint32_t ci = base;
             // keep the 32 addresses out of registers across tiles: recomputing them costs one XOR
             // each, hoisting them out of the loop spills (local-memory traffic every tile)
             asm volatile("" : "+r"(ci));
 #pragma unroll
-            for (int g = 0; g < 32; g++) {   // Gray-code walk of u: one XOR per element
+            for (int g = 0; g < 32 && PT != kRow; g++) {   // Gray-code walk of u: one XOR per element
                 const int u = g ^ (g >> 1);
                 if (g) ci ^= R[(g & 1) ? 0 : (g & 2) ? 1 : (g & 4) ? 2 : (g & 8) ? 3 : 4];
                 v[u] = rb[ci];
@@ -1007,7 +1034,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             asm volatile("tcgen05.fence::after_thread_sync;");
             float2* dst = p.amps + (tb | offj);
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + 256;
-#if RCS_K12_EPIPIPE
+            const int tile_c = (int)(tb >> 13);   // kRow: tile coordinate of the store map
             // Four chunks of 32 D columns (16 target combinations, re/im).  The next chunk's TMEM
             // loads are issued before this chunk's stores, so the stores overlap the TMEM reads
             // (the epilogue's longest part: 64 B/cycle); two register sets alternate.
@@ -1041,9 +1068,37 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                     TMEM_LD32M(ta + 32 * (s4 + 1), y0);
                     TMEM_LD32M(ta + 128 + 32 * (s4 + 1), y1);
                 }
+                if (PT == kRow) {   // two staging chunks of 8 t; a TMA store each (4-D map, 64-B swizzle)
 #pragma unroll
-                for (int c = 0; c < 32; c += 2)
-                    __stcs(dst + offt[16 * s4 + c / 2], make_float2(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1])));
+                    for (int h8 = 0; h8 < 2; h8++) {
+                        const int k8 = 2 * s4 + h8;
+                        uint8_t* sg = smem + 2 * kTRaw + kTMat + (k8 & 1) * (kTRowStage / 2);
+                        if (warp == kEpiWarp0 && lane == 0)   // the store issued two chunks ago has read sg
+                            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        asm volatile("bar.sync 3, 128;" ::: "memory");
+#pragma unroll
+                        for (int m = 0; m < 4; m++) {   // t pair (8 k8 + 2 m, +1) of column j
+                            const int c = 2 * (8 * h8 + 2 * m);
+                            *reinterpret_cast<float4*>(sg + j * 64 + (((uint32_t)m ^ ((uint32_t)(j >> 1) & 3)) << 4)) =
+                                make_float4(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1]), __uint_as_float(x0[c + 2]),
+                                            __uint_as_float(x0[c + 3]));
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        asm volatile("bar.sync 3, 128;" ::: "memory");
+                        if (warp == kEpiWarp0 && lane == 0) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                                    reinterpret_cast<uint64_t>(&p.tmap_st)),
+                                "r"(0), "r"(0), "r"(k8), "r"(tile_c), "r"(su32(sg))
+                                : "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2)
+                        __stcs(dst + offt[16 * s4 + c / 2], make_float2(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1])));
+                }
                 if (s4 < 3) {
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     REG_FENCE32(y0);
@@ -1054,36 +1109,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             chunk(1, b0, b1, a0, a1);
             chunk(2, a0, a1, b0, b1);
             chunk(3, b0, b1, a0, a1);
-#else
-#pragma unroll
-            for (int s4 = 0; s4 < 4; s4++) {   // 32 columns n = 16 target combinations (re, im)
-                if (s4 == 2) {
-                    mbar_wait(&dfull[1], it & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                }
-                uint32_t a0[32], a1[32];
-                TMEM_LD32(ta + 32 * s4, a0);
-                TMEM_LD32(ta + 128 + 32 * s4, a1);
-                asm volatile("tcgen05.wait::ld.sync.aligned;");
-                if (s4 & 1) {   // half s4 / 2 read: its D columns are free for the next tile
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    mbar_arrive(&dempty[s4 >> 1]);
-                }
-#pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                    const float rf = rowfac[16 * s4 + c / 2];
-                    float o0, o1;   // ((cross + main) 2^-E_j) 2^-F_t of (re, im) of t = 16 s4 + c / 2
-                    asm("{\n.reg .b64 x, y, u, v;\n"
-                        "mov.b64 x, {%2, %3};\nmov.b64 y, {%4, %5};\nmov.b64 u, {%6, %6};\nmov.b64 v, {%7, %7};\n"
-                        "add.rn.f32x2 x, x, y;\nmul.rn.f32x2 x, x, u;\nmul.rn.f32x2 x, x, v;\n"
-                        "mov.b64 {%0, %1}, x;\n}"
-                        : "=f"(o0), "=f"(o1)
-                        : "r"(a0[c]), "r"(a0[c + 1]), "r"(a1[c]), "r"(a1[c + 1]), "f"(cf), "f"(rf));
-                    __stcs(dst + offt[16 * s4 + c / 2], make_float2(o0, o1));
-                }
-            }
-#endif
         }
+        if (PT == kRow && warp == kEpiWarp0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -1212,6 +1239,34 @@ static bool tct_tensor_map(TcTArgs& p, int nl) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// kRow tensor maps (load: 128-B swizzle, box 16 t x 128 j x 4 t-quads; store: 64-B swizzle, box
+// 8 t x 128 j): dims are the state's bit fields (t bits 0..3 or 0..2 contiguous, j = positions
+// 6..12, the remaining t bits, the tile = positions 13..), so the strides do not ascend; false if
+// the encoder refuses (the block then runs on K9)
+static bool row_tensor_maps(TcTArgs& p, int nl) {
+    TmapEncodeFn enc = tmap_encoder();
+    if (!enc || nl < 13 || nl - 13 > 31) return false;
+    const cuuint64_t ntile = 1ull << (nl - 13);
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    cuuint64_t ld_dim[4] = {16, 128, 4, ntile}, ld_str[3] = {512, 128, 65536};
+    cuuint32_t ld_box[4] = {16, 128, 4, 1};
+    cuuint64_t st_dim[4] = {8, 128, 8, ntile}, st_str[3] = {512, 64, 65536};
+    cuuint32_t st_box[4] = {8, 128, 1, 1};
+    return enc(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, p.amps, ld_dim, ld_str, ld_box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+           enc(&p.tmap_st, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, p.amps, st_dim, st_str, st_box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool is_row_layout(int nl, const int* pos, int nfix) {
+    if (nl < 13 || nfix != 0) return false;
+    for (int i = 0; i < 6; i++)
+        if (pos[i] != i) return false;
+    return true;
+}
+
 // K12 launcher: any target layout, n_local >= 13 (+ chunk bits)
 static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms,
                                  cudaStream_t st, const int* fix, int nfix, uint64_t fixval, unsigned* counter,
@@ -1270,8 +1325,14 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
             p.pmask |= 1 << lowt[m];
         }
     }
+    const bool row = is_row_layout(nl, pos, nfix);
+    if (row) {
+        if (!row_tensor_maps(p, nl)) return cudaErrorNotSupported;   // caller falls back to K9
+        p.phi_t = kRow;
+        p.nreq = 0;
+    }
     const bool perm = p.phi_t >= 0;
-    if (perm && p.jcube[4 - nlow] < 4) return cudaErrorInvalidValue;
+    if (perm && !row && p.jcube[4 - nlow] < 4) return cudaErrorInvalidValue;
     uint64_t insmask = cube, fixmask = 0;
     for (int i = 0; i < nfix; i++) {
         if (fix[i] < 0 || fix[i] >= nl || ((insmask >> fix[i]) & 1)) return cudaErrorInvalidValue;
@@ -1303,14 +1364,16 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
         case 3: kern = k_pass_tct<3>; break;
         case 4: kern = k_pass_tct<4>; break;
         case kPermMulti: kern = k_pass_tct<kPermMulti>; break;
+        case kRow: kern = k_pass_tct<kRow>; break;
         default: return cudaErrorInvalidValue;
     }
+    const uint32_t smem_bytes = kTSmem + (row ? kTRowStage : 0);
     (void)perm;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
     if (counter && (e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     count_launch();
-    kern<<<(unsigned)grid, kThreadsTC, kTSmem, st>>>(p);
+    kern<<<(unsigned)grid, kThreadsTC, smem_bytes, st>>>(p);
     return cudaGetLastError();
 }
 
@@ -1321,14 +1384,17 @@ bool tc_uses_k12(int nl, const int* pos) {
     // targets 31-44 ms vs K9 17.0-17.2 -- the epilogue's stores then scatter over 32 sectors
     int low = 0;
     for (int i = 0; i < 6; i++) low += pos[i] < 4;
-    return nl >= 13 && pos[5] >= 4 && low <= 2;
+    return nl >= 13 && ((pos[5] >= 4 && low <= 2) || is_row_layout(nl, pos, 0));
 }
 
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
                          const int* fix, int nfix, uint64_t fixval, int tc_flags, unsigned* tile_counter) {
-    if (!(tc_flags & kTcForceK9) && tc_uses_k12(nl, pos))
-        return gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval, tile_counter,
-                             (tc_flags & kTcBulkRuns) != 0);
+    if (!(tc_flags & kTcForceK9) && tc_uses_k12(nl, pos) && !(is_row_layout(nl, pos, 0) && (nfix != 0 || (tc_flags & kTcNoRow)))) {
+        const cudaError_t e = gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval, tile_counter,
+                                            (tc_flags & kTcBulkRuns) != 0);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();   // kRow maps refused by the encoder: K9 below
+    }
     if (nl < 12 + nfix || nfix < 0 || nfix > 4) return cudaErrorInvalidValue;
     TcArgs p{};
     p.amps = amps;

@@ -129,6 +129,24 @@ def test_multi_low_target_blocks_on_k12(rcs, ctx, grid):
     check_amps(pa, oracle.build_state(text))
 
 
+@pytest.mark.parametrize("grid", [(3, 7, 12, "ABCDCDAB", 1), (3, 7, 12, "ABCDCDAB", 2)])
+def test_row_variant_blocks(rcs, ctx, grid):
+    """Blocks on positions 0..5 (grid row 0) run on K12's row variant -- tensor-map TMA load with
+    the 128-B swizzle, TMA stores from a 64-B-swizzled staging buffer: equal to the K9 build of
+    the same blocks (tc_kernel="norow") up to the cross terms' rounding order, and to the oracle."""
+    rows, cols, cyc, pat, seed = grid
+    text = emit_qasm(generate(rows, cols, cyc, pat, seed=seed))
+    c = rcs.Circuit.from_qasm(text)
+    plan = rcs.Plan(c, 6, 0)
+    assert any(it["type"] == "pass" and it["pos"] == [0, 1, 2, 3, 4, 5] for it in plan.items()[plan.prefix:])
+    a = rcs.State.build(ctx, c, fuse_k=6)
+    pa = a.copy_out().astype(np.complex128)
+    b = rcs.State.build(ctx, c, fuse_k=6, tc_kernel="norow")
+    pb = b.copy_out().astype(np.complex128)
+    assert np.abs(pa - pb).max() <= 1e-8 and abs(a.norm - b.norm) <= 1e-7
+    check_amps(pa, oracle.build_state(text))
+
+
 @pytest.mark.parametrize("case", ["c1", "c3_24", "w33_24", "grid20_k4"])
 def test_product_prefix_matches_passes(rcs, ctx, case):
     """The leading fused blocks on disjoint qubits act on |0...0>: the product-state kernel writes
