@@ -110,7 +110,7 @@ typedef struct {
                                 world >= 4 and in loopback)                                        */
     int tc_kernel;           /* 0: the transposed kernel K12 when n_local >= 13 and at most two
                                 targets sit in positions 0..3 (not matrix bit 5), or the block is
-                                positions 0..5 in order (K12's row variant, unchunked passes); K9
+                                positions 0..5 in order (K12's row variant); K9
                                 otherwise -- a function of the block: P-invariant; 1: K9 only
                                 (tests, comparisons); 2: as 0 without the row variant            */
     int overlap_passes;      /* pipelined remaps: how many tensor-core passes after the remap run

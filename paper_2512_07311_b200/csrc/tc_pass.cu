@@ -831,12 +831,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
             __syncwarp();
             const float2* src = p.amps + (bp | p.fixval);
             const uint32_t dst = su32(raw + (size_t)slot * 8192);
-            if (PT == kRow) {   // one 4-D tensor load of the whole tile (tile base = tile << 13)
+            if (PT == kRow) {   // one 4-D tensor load of the whole tile (its base, all bits >= 13, / 2^13)
                 if (lane == 0)
                     asm volatile(
                         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
                         "%3, %4, %5}], [%6];" ::"r"(dst),
-                        "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(0), "r"(0), "r"(0), "r"((int)(bp >> 13)),
+                        "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(0), "r"(0), "r"(0), "r"((int)((bp | p.fixval) >> 13)),
                         "r"(su32(&rfull[slot]))
                         : "memory");
             } else if (p.nreq) {
@@ -1260,8 +1260,8 @@ static bool row_tensor_maps(TcTArgs& p, int nl) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool is_row_layout(int nl, const int* pos, int nfix) {
-    if (nl < 13 || nfix != 0) return false;
+static bool is_row_layout(int nl, const int* pos) {
+    if (nl < 13) return false;
     for (int i = 0; i < 6; i++)
         if (pos[i] != i) return false;
     return true;
@@ -1325,7 +1325,7 @@ static cudaError_t gate_pass_tct(float2* amps, int nl, const int* pos, const uin
             p.pmask |= 1 << lowt[m];
         }
     }
-    const bool row = is_row_layout(nl, pos, nfix);
+    const bool row = is_row_layout(nl, pos);   // also chunked (pipelined remaps): the chunk bits are >= 13
     if (row) {
         if (!row_tensor_maps(p, nl)) return cudaErrorNotSupported;   // caller falls back to K9
         p.phi_t = kRow;
@@ -1384,12 +1384,12 @@ bool tc_uses_k12(int nl, const int* pos) {
     // targets 31-44 ms vs K9 17.0-17.2 -- the epilogue's stores then scatter over 32 sectors
     int low = 0;
     for (int i = 0; i < 6; i++) low += pos[i] < 4;
-    return nl >= 13 && ((pos[5] >= 4 && low <= 2) || is_row_layout(nl, pos, 0));
+    return nl >= 13 && ((pos[5] >= 4 && low <= 2) || is_row_layout(nl, pos));
 }
 
 cudaError_t gate_pass_tc(float2* amps, int nl, const int* pos, const uint32_t* d_a, int num_sms, cudaStream_t st,
                          const int* fix, int nfix, uint64_t fixval, int tc_flags, unsigned* tile_counter) {
-    if (!(tc_flags & kTcForceK9) && tc_uses_k12(nl, pos) && !(is_row_layout(nl, pos, 0) && (nfix != 0 || (tc_flags & kTcNoRow)))) {
+    if (!(tc_flags & kTcForceK9) && tc_uses_k12(nl, pos) && !(is_row_layout(nl, pos) && (tc_flags & kTcNoRow))) {
         const cudaError_t e = gate_pass_tct(amps, nl, pos, d_a, num_sms, st, fix, nfix, fixval, tile_counter,
                                             (tc_flags & kTcBulkRuns) != 0);
         if (e != cudaErrorNotSupported) return e;

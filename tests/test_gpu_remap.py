@@ -34,6 +34,8 @@ CASES = {
     "grid20_k4": (emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=3)), 4),
     "grid20_k6": (emit_qasm(generate(4, 5, 16, "ABCDCDAB", seed=3)), 6),
     "c2_k6": (config_qasm("c2"), 6),
+    # a block on positions 0..5 (K12's row variant), also inside pipelined (chunked) passes
+    "row21_k6": (emit_qasm(generate(3, 7, 12, "ABCDCDAB", seed=1)), 6),
 }
 
 
