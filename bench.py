@@ -49,11 +49,11 @@ PLAN_PREFIX = {'c1': {3: 4, 4: 2, 5: 2, 6: 2},
                'w33': {3: 11, 4: 9, 5: 7, 6: 6},
                'w35': {3: 6, 4: 8, 5: 5, 6: 6}}
 PLAN_PASSES = {'c1': {3: 32, 4: 19, 5: 14, 6: 8},
-               'c2': {3: 98, 4: 45, 5: 40, 6: 27},
-               'c3': {3: 103, 4: 56, 5: 44, 6: 33},
-               'c4': {3: 149, 4: 76, 5: 57, 6: 36},
-               'c5': {3: 157, 4: 82, 5: 63, 6: 39},
-               'w33': {3: 122, 4: 74, 5: 53, 6: 39},
+               'c2': {3: 98, 4: 45, 5: 38, 6: 27},
+               'c3': {3: 102, 4: 56, 5: 44, 6: 33},
+               'c4': {3: 143, 4: 76, 5: 55, 6: 36},
+               'c5': {3: 157, 4: 82, 5: 63, 6: 36},
+               'w33': {3: 119, 4: 74, 5: 53, 6: 39},
                'w35': {3: 142, 4: 83, 5: 52, 6: 46}}
 
 

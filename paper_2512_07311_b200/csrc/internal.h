@@ -97,9 +97,9 @@ constexpr int kPrefixGroupBits = 18;      // product-state prefix: qubits per ta
 // use_prefix = false: no product-state prefix (every block is a pass and is remapped as one)
 rcs_status build_plan(const Circuit& c, int fuse_k, int n_global, Plan& out, rcs_error* err,
                       const std::vector<Block>* given = nullptr, bool use_prefix = true);
-// strategies: 3-level extension search, prefix-first greedy, prefix-first 1-level, prefix-first
-// with a 1-level prefix phase and a 3-level rest (plan.cpp fuse_strategy_memo)
-constexpr int kFuseStrategies = 4;
+// strategies: 2-level extension search, prefix-first greedy, prefix-first 1-level, prefix-first
+// with a 1-level prefix phase and a 3-level rest, prefix-first beam search (plan.cpp)
+constexpr int kFuseStrategies = 5;
 int64_t fuse_cost(const std::vector<Block>& blocks);   // passes << 20 | blocks (lower is better)
 void fuse_strategy(const Circuit& c, int k, int which, std::vector<Block>& out);
 int fuse_best(const Circuit& c, int k, std::vector<Block>* cand /* [kFuseStrategies] */);

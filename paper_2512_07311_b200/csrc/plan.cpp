@@ -459,6 +459,43 @@ struct Fuser {
         return true;
     }
 
+    // beam strategy: every candidate next set (prefix phase: all seeds inside the untouched
+    // qubits; else the earliest gate and `seeds` ready gates) with its lookahead score -- gate
+    // weight now minus 1000 x the passes of a greedy completion -- without committing
+    void candidates(std::vector<std::pair<long, uint64_t>>& out) {
+        out.clear();
+        if (first_unassigned >= assigned.size()) return;
+        std::vector<int> cand;
+        bool pre = false;
+        if (prefix_first) {
+            for (int q = 0; q < n; q++) {
+                if ((touched >> q) & 1) continue;
+                const int g = next_gate(q, head[q]);
+                if (g < 0 || (T->gmask[g] & touched) || !ready(g)) continue;
+                if (std::find(cand.begin(), cand.end(), g) == cand.end()) cand.push_back(g);
+            }
+            std::sort(cand.begin(), cand.end());
+            pre = !cand.empty();
+        }
+        if (!pre) {
+            cand.assign(1, (int)first_unassigned);
+            for (int i = (int)first_unassigned + 1; i < (int)assigned.size() && (int)cand.size() < 1 + seeds; i++)
+                if (!assigned[i] && ready(i)) cand.push_back(i);
+        }
+        const uint64_t saved = allowed;
+        if (pre) allowed = ~touched;
+        for (int g : cand) {
+            uint64_t S;
+            int w;
+            grow(g, S, w);
+            Fuser f = *this;
+            f.allowed = saved;
+            f.commit(S);
+            out.push_back({-1000L * (f.rollout() + (pre ? 0 : 1)) + w, S});
+        }
+        allowed = saved;
+    }
+
     bool next_block(Block& B) {
         // the gates are those the committed set absorbs from the heads BEFORE the commit
         const std::vector<int> head0 = head;
@@ -519,11 +556,80 @@ void apply_to_block(std::vector<cplx>& U, int kb, const Gate& g, int lb0, int lb
 // candidate extension scored by the block it finishes as, 2 exhaustive 3-level extension search
 // (memoized); all with the rollout lookahead over seed gates.  The plan with the fewest blocks
 // wins, ties to the lower index.
+// Beam search over whole fusions (prefix-first): each state expands into its kBeamWidth best
+// candidate blocks, the kBeamWidth states with the fewest passes + best lookahead survive
+// (duplicates by per-qubit heads dropped).  Deterministic (stable order everywhere).
+static void fuse_beam(const Circuit& c, int k, std::vector<Block>& out, std::shared_ptr<RolloutMemo> memo) {
+    constexpr int kBeamWidth = 4, kBeamExpand = 4;
+    const FuseTables tabs = make_tables(c);
+    struct Node {
+        Fuser f;
+        int passes;
+        long score;
+        std::vector<uint64_t> sets;
+    };
+    auto root = std::make_shared<Node>(Node{Fuser(c, k, &tabs), 0, 0, {}});
+    root->f.prefix_first = true;
+    root->f.memo = memo.get();
+    root->f.seeds = kFuseSeeds;
+    root->f.lookahead = true;
+    std::vector<std::shared_ptr<Node>> beam{root};
+    std::shared_ptr<Node> best;
+    while (!beam.empty()) {
+        std::vector<std::shared_ptr<Node>> next;
+        for (auto& nd : beam) {
+            if (nd->f.first_unassigned >= nd->f.assigned.size()) {
+                if (!best || nd->passes < best->passes) best = nd;
+                continue;
+            }
+            std::vector<std::pair<long, uint64_t>> cands;
+            nd->f.candidates(cands);
+            std::stable_sort(cands.begin(), cands.end(),
+                             [](const std::pair<long, uint64_t>& a, const std::pair<long, uint64_t>& b) {
+                                 return a.first > b.first;
+                             });
+            for (int m = 0; m < (int)cands.size() && m < kBeamExpand; m++) {
+                auto ch = std::make_shared<Node>(Node{nd->f, nd->passes, 0, nd->sets});
+                const uint64_t S = cands[m].second;
+                ch->passes += (S & nd->f.touched) != 0;   // a block on untouched qubits is prefix
+                ch->f.commit(S);
+                ch->sets.push_back(S);
+                ch->score = -1000L * ch->passes + cands[m].first;
+                next.push_back(ch);
+            }
+        }
+        std::stable_sort(next.begin(), next.end(),
+                         [](const std::shared_ptr<Node>& a, const std::shared_ptr<Node>& b) { return a->score > b->score; });
+        std::vector<std::shared_ptr<Node>> kept;
+        for (auto& nd : next) {
+            bool dup = false;
+            for (auto& kd : kept) dup = dup || (kd->f.head == nd->f.head && kd->f.touched == nd->f.touched);
+            if (!dup) kept.push_back(nd);
+            if ((int)kept.size() >= kBeamWidth) break;
+        }
+        beam.swap(kept);
+    }
+    // replay the winner's sets: the gates of each block in absorption order
+    Fuser F(c, k, &tabs);
+    out.clear();
+    for (uint64_t S : best->sets) {
+        Block B;
+        F.closure(S, &B.gate_ids);
+        F.commit(S);
+        for (uint64_t m = S; m; m &= m - 1) B.qubits.push_back(__builtin_ctzll(m));
+        out.push_back(std::move(B));
+    }
+}
+
 static void fuse_strategy_memo(const Circuit& c, int k, int which, std::vector<Block>& out,
                                std::shared_ptr<RolloutMemo> memo) {
+    if (which == kFuseStrategies - 1) {
+        fuse_beam(c, k, out, std::move(memo));
+        return;
+    }
     // {prefix-first, extension search depth, prefix-phase depth (-1: the same), seeds}
-    static const int S[kFuseStrategies][4] = {{0, 2, -1, 4}, {1, 0, -1, kFuseSeeds},
-                                              {1, 1, -1, kFuseSeeds}, {1, kFuseDeepDepth, 1, kFuseSeeds}};
+    static const int S[kFuseStrategies - 1][4] = {{0, 2, -1, 4}, {1, 0, -1, kFuseSeeds},
+                                                  {1, 1, -1, kFuseSeeds}, {1, kFuseDeepDepth, 1, kFuseSeeds}};
     const FuseTables tabs = make_tables(c);
     Fuser F(c, k, &tabs);
     F.prefix_first = S[which][0] != 0;
