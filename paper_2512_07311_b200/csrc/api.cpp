@@ -591,7 +591,7 @@ struct PassRef {
 };
 
 rcs_status do_remap_pipelined(rcs_state* s, const Item& it, const PassRef* pa, const PassRef* pbs, int nb,
-                              const int* fix, int cb, int reserve, bool force_k9, uint64_t* bytes_sent,
+                              const int* fix, int cb, int reserve, uint64_t* bytes_sent,
                               uint64_t* pass_bytes, size_t ia, size_t ir, const size_t* ibs, std::vector<Span>* spans,
                               std::vector<cudaEvent_t>* owned, rcs_error* err) {
     rcs_context* c = s->ctx;
@@ -1303,7 +1303,6 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
     int n_pipelined = 0, n_peer = 0;
     std::vector<float> mbuf;
     std::vector<Span> spans;
-    const bool force_k9 = o.tc_kernel == 1;
     const bool peer_path = (ctx->world > 1 && ctx->p2p) || loopback(s);
     // pipelined remaps (f1): 2^cb chunks, `reserve` SMs left to the swaps (sweeps: profiles/r01_ovl*)
     const int ov_cb = o.overlap_chunks > 0 ? o.overlap_chunks : 2;
@@ -1352,7 +1351,7 @@ rcs_status rcs_state_build(rcs_context* ctx, const rcs_circuit* circ, const rcs_
                 if ((has_a || !rb.empty()) && choose_chunk_bits(nl_loc, excl, ov_cb, fix)) {
                     PassRef ra = has_a ? tc_ref(ii) : PassRef{};
                     rcs_status r = do_remap_pipelined(s, rm, has_a ? &ra : nullptr, rb.data(), (int)rb.size(), fix,
-                                                      ov_cb, ov_res, force_k9, &remap_bytes, &pass_bytes, ii, ir,
+                                                      ov_cb, ov_res, &remap_bytes, &pass_bytes, ii, ir,
                                                       ib.data(), o.timing ? &spans : nullptr, &owned, err);
                     if (r) return fail(r);
                     n_pipelined++;
