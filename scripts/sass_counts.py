@@ -12,7 +12,7 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2512_07311_b200", "librcs.so")
-OPS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UBLKCP", "UTMALDG", "SYNCS", "FFMA", "FFMA2", "FMUL2",
+OPS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UBLKCP", "UTMALDG", "UTMASTG", "SYNCS", "FFMA", "FFMA2", "FMUL2",
        "FADD2", "F2FP", "FRND", "LDS", "STS", "LDG", "STG", "ATOMS", "PRMT"]
 
 
