@@ -32,6 +32,7 @@ def test_separable_c5_n36_sharded(world, tmp_path, cuda_ok):
                        text=True, timeout=1800)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.load(open(tmp_path / "fullscale.json"))
+    print(json.dumps({k: v for k, v in res.items() if k != "report"}))
     assert res["report"]["n_remaps"] > 0 and res["report"]["n_tc_passes"] > 0, res["report"]
     assert res["maxd"] <= 1e-5 and res["eps"] <= 1e-5, res
     assert abs(res["norm"] - 1) <= 1e-5
