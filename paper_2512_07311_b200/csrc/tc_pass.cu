@@ -661,6 +661,11 @@ struct TcTArgs {
 #ifndef RCS_K12_NSPLIT
 #define RCS_K12_NSPLIT 1
 #endif
+#ifdef RCS_K12_WB_STORES   // A/B: write-back stores instead of streaming (evict-first) ones
+#define K12_STORE(p, v) (*(p) = (v))
+#else
+#define K12_STORE(p, v) __stcs((p), (v))
+#endif
 constexpr uint32_t kTRaw = 8192 * 8;
 constexpr int kTRing = 8;                             // tile bases in flight (producer -> all roles)
 constexpr uint64_t kTileEnd = ~0ull;                  // ring sentinel: no more tiles                  // one tile: 64 KB
@@ -1097,7 +1102,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) k_pass_tct(const __grid_constan
                 } else {
 #pragma unroll
                     for (int c = 0; c < 32; c += 2)
-                        __stcs(dst + offt[16 * s4 + c / 2], make_float2(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1])));
+                        K12_STORE(dst + offt[16 * s4 + c / 2], make_float2(__uint_as_float(x0[c]), __uint_as_float(x0[c + 1])));
                 }
                 if (s4 < 3) {
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
