@@ -147,14 +147,18 @@ def test_row_variant_blocks(rcs, ctx, grid):
     check_amps(pa, oracle.build_state(text))
 
 
-@pytest.mark.parametrize("case", ["c1", "c3_24", "w33_24", "grid20_k4"])
+@pytest.mark.parametrize("case", ["c1", "c3_24", "w33_24", "grid20_k4", "idle22"])
 def test_product_prefix_matches_passes(rcs, ctx, case):
     """The leading fused blocks on disjoint qubits act on |0...0>: the product-state kernel writes
-    their state in one write-only sweep (fp64 products rounded once) instead of init + passes;
-    both agree with the oracle and with each other within the pass rounding."""
+    their state in one write-only sweep (fp64 block products rounded to complex64, one fixed-order
+    complex product) instead of init + passes; both agree with the oracle and with each other
+    within the pass rounding.  idle22: qubits 19..21 carry no gate, so the prefix kernel's zero
+    path (amplitudes with a |1> outside the prefix) is exercised, rows and single amplitudes."""
+    idle = random_qasm(19, 260, 7).replace("qreg q[19];", "qreg q[22];")
     text, k = {"c1": (config_qasm("c1"), 6), "c3_24": (config_qasm("c3", n_qubits=24, rows=4, cols=6), 6),
                "w33_24": (config_qasm("w33", n_qubits=24), 6),
-               "grid20_k4": (emit_qasm(generate(4, 5, 12, "ABCDCDAB", seed=2)), 4)}[case]
+               "grid20_k4": (emit_qasm(generate(4, 5, 12, "ABCDCDAB", seed=2)), 4),
+               "idle22": (idle, 6)}[case]
     c = rcs.Circuit.from_qasm(text)
     a = rcs.State.build(ctx, c, fuse_k=k, timing=True)
     pa = a.copy_out().astype(np.complex128)
