@@ -3,7 +3,7 @@
 cd "$(dirname "$0")/.."
 OUT=gpurun_out/${MOUT:-mgpu}; mkdir -p $OUT
 python -m paper_2512_07311_b200.build > $OUT/build.log 2>&1 || { echo BUILD FAILED; exit 1; }
-timeout 2400 python -m pytest tests/test_multigpu.py -q -p no:cacheprovider > $OUT/mgpu_tests.log 2>&1; echo "mgpu tests rc=$?"
+timeout 2400 python -m pytest tests/test_multigpu.py tests/test_multigpu_fullscale.py -q -s -p no:cacheprovider > $OUT/mgpu_tests.log 2>&1; echo "mgpu tests rc=$?"
 grep -E "^(FAILED|ERROR)|passed|failed" $OUT/mgpu_tests.log | tail -20
 for M in 2 4; do
   DEV=$(seq -s, 0 $((M-1)))
