@@ -182,12 +182,25 @@ def test_pass_counts_reported(rcs):
         assert p.n_passes <= cap, (cfg, p.n_passes)
 
 
+def key_of(p):
+    return [tuple((f, np.asarray(v).tobytes()) for f, v in sorted(it.items())) for it in p.items()]
+
+
 def test_plan_deterministic_across_runs(rcs):
     """The fusion strategies run in threads and share a memo of greedy rollouts:
     the plan must not depend on thread timing -- the same items, run after run."""
     c = rcs.Circuit.from_qasm(config_qasm("c2"))
-    def key(p):
-        return [tuple((f, np.asarray(v).tobytes()) for f, v in sorted(it.items())) for it in p.items()]
-    runs = [key(rcs.Plan(c, 6, g)) for g in (0, 0, 0, 2, 2)]
+    runs = [key_of(rcs.Plan(c, 6, g)) for g in (0, 0, 0, 2, 2)]
     assert runs[0] == runs[1] == runs[2]
     assert runs[3] == runs[4]
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
+def test_plan_deterministic_all_widths(rcs, cfg):
+    """Every block width, fresh circuit objects each run (no per-circuit plan cache): identical
+    items and matrices.  A memo shared between strategies with different rollout functions once
+    made C4's k = 5 plan vary between runs (56 / 57 passes); this would catch it."""
+    text = config_qasm(cfg)
+    for k in (4, 5, 6):
+        runs = [key_of(rcs.Plan(rcs.Circuit.from_qasm(text), k, 0)) for _ in range(3)]
+        assert runs[0] == runs[1] == runs[2], (cfg, k)
